@@ -1,0 +1,167 @@
+/*
+ * gumap.h -- C ABI of libgumap.so, the B200 (sm_100a) hot path of the
+ * graph_umap layouts (GUMAP / SS / SL / SSSL, arXiv 2509.19703).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Array arguments are DEVICE pointers
+ *     unless the name starts with host_.  `stream` is a cudaStream_t (NULL =
+ *     legacy default stream).  Every call is asynchronous on `stream` unless
+ *     documented otherwise.
+ *   - Return value: 0 = ok; 1 = bad argument; 2 = CUDA error; 3 = workspace too
+ *     small; 4 = unsupported input.  gu_last_error() gives the message.  The
+ *     Python layer maps these to the reference's exceptions (ValueError etc.).
+ *   - CSR graphs use int32 row offsets (2m < 2^31, every BASELINE config) and
+ *     int32 neighbour ids sorted ascending per row, as graph_umap's Graph
+ *     (graph.py:16-71) after the int64 -> int32 offset narrowing done by the
+ *     device CSR store.
+ *   - Caller-owned outputs, fixed stride k per source ("records"), as the
+ *     reference's numba kernels write them (_kernels.py:61 nbr_out/dist_out/
+ *     counts_out).
+ *
+ * Each entry point cites the reference interface it replaces
+ * (/root/reference/pkg/src/graph_umap/...).
+ */
+#ifndef GUMAP_H
+#define GUMAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ library */
+int gu_version(void);                 /* ABI version, currently 1 */
+const char* gu_last_error(void);      /* thread-local message of the last failure */
+int gu_device_sync(void* stream);     /* cudaStreamSynchronize + error check */
+
+/* ---------------------------------------------- C0+C1 partial BFS-kNN
+ * Replaces _kernels.py:60-131 partial_bfs_all(indptr, indices, k, seed,
+ * nbr_out, dist_out, counts_out), reached via neighbors.py:137 partial_bfs.
+ * Sources [src_begin, src_end); row r = s - src_begin of out_nbr/out_dist
+ * (stride k) holds the k hop-nearest others of s sorted by (dist, id), ties at
+ * the crossing level chosen by the reference's splitmix64 partial
+ * Fisher-Yates.  out_count[r] < k only when the component is smaller.
+ * work_counters (nullable, 2 x uint64): adjacency entries scanned and vertices
+ * expanded, summed over sources (the TE work unit).
+ * tier2_warps: per-warp n-int scratch slots for sources whose BFS ball exceeds
+ * the shared-memory tiers; workspace size from gu_partial_bfs_workspace_size. */
+size_t gu_partial_bfs_workspace_size(int64_t n, int64_t nsrc, int32_t tier2_warps);
+int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_t* indices,
+                       int32_t k, uint64_t seed, int64_t src_begin, int64_t src_end,
+                       int32_t* out_nbr, int32_t* out_dist, int32_t* out_count,
+                       uint64_t* work_counters, void* workspace, size_t ws_bytes,
+                       int32_t tier2_warps, void* stream);
+/* synchronous: how many sources fell to tier 1b / tier 2 in the last call */
+int gu_partial_bfs_overflow_counts(void* workspace, int64_t nsrc, int32_t* host_out2);
+
+/* ----------------------------------------------- C0 full BFS (bitset)
+ * Replaces _kernels.py:33-57 apsp_rows via neighbors.py:120 all_pairs_bfs:
+ * int32 hop-distance rows for sources [src_begin, src_end) into out_rows
+ * (row r = s - src_begin, n entries, INT32_MAX = unreachable).  64 sources per
+ * bitset word, level-synchronous. */
+size_t gu_full_bfs_workspace_size(int64_t n, int32_t k, int32_t batches_in_flight);
+int gu_apsp_rows(int64_t n, const int32_t* indptr, const int32_t* indices,
+                 int64_t src_begin, int64_t src_end, int32_t* out_rows,
+                 void* workspace, size_t ws_bytes, int32_t batches_in_flight,
+                 void* stream);
+
+/* ----------------------------------------------- C0+C1 full BFS-kNN fused
+ * Replaces all_pairs_bfs (neighbors.py:120) + knn_from_full_distances
+ * (neighbors.py:183-237) without materialising the n x n matrix: bitset BFS
+ * with per-source early exit at the k-th distance, k-th distance ties chosen
+ * by numpy's SeedSequence(seed, spawn_key=(v,)) -> PCG64 -> permutation
+ * restated on device.  Records as gu_partial_bfs_knn.
+ * work_counters: adjacency entries scanned (TE) and BFS levels run. */
+int gu_full_bfs_knn(int64_t n, const int32_t* indptr, const int32_t* indices,
+                    int32_t k, uint64_t seed, int64_t src_begin, int64_t src_end,
+                    int32_t* out_nbr, int32_t* out_dist, int32_t* out_count,
+                    uint64_t* work_counters, void* workspace, size_t ws_bytes,
+                    int32_t batches_in_flight, void* stream);
+
+/* kNN selection from explicit int32 distance rows (neighbors.py:199-221), for
+ * SparseDistanceSet objects that arrive with a materialised matrix.
+ * rows: nrows x n (row r belongs to vertex row_begin + r).  scratch: 2*n int32
+ * per warp slot (gu_knn_from_rows_workspace_size). */
+size_t gu_knn_from_rows_workspace_size(int64_t n, int32_t slots);
+int gu_knn_from_rows(int64_t n, const int32_t* rows, int64_t row_begin, int64_t nrows,
+                     int32_t k, uint64_t seed, int32_t* out_nbr, int32_t* out_dist,
+                     int32_t* out_count, void* workspace, size_t ws_bytes,
+                     int32_t slots, void* stream);
+
+/* ---------------------------------------------------- record packing
+ * Fixed-stride records -> CSR (neighbors.py:166-175, the Python packing loop
+ * the reference runs per vertex).  out_indptr int64[nrows+1]. */
+int gu_pack_records(int64_t nrows, int32_t k, const int32_t* rec_nbr,
+                    const int32_t* rec_dist, const int32_t* rec_count,
+                    int64_t* out_indptr, int32_t* out_dst, int32_t* out_dist,
+                    void* workspace, size_t ws_bytes, void* stream);
+size_t gu_pack_records_workspace_size(int64_t nrows);
+
+/* --------------------------------------------------- C1 smooth kNN rho/sigma
+ * Replaces neighbors.py:261-318: rho = row min, sigma by the reference's
+ * 64-step bisection on [1e-3, 1e3] (tol 1e-5, numpy pairwise row sums over
+ * rows padded to kmax, non-converged rows take the next midpoint), weights
+ * w = exp(-(d - rho) / sigma).  target = np.log2(k) computed by the caller. */
+int gu_smooth_knn(int64_t n, const int64_t* indptr, const int32_t* dist, int32_t kmax,
+                  double target, double* rho, double* sigma, double* w, void* stream);
+
+/* ----------------------------------------------- C1 fuzzy-union symmetrise
+ * Replaces neighbors.py:320-350 (dedupe first occurrence, w + w^T - w o w^T
+ * with exact zeros dropped, lexsort by (src, dst), CSR neighbour lookup).
+ * Outputs have capacity 2*nnz; *host_E receives the edge count (synchronous).
+ * nbr_indptr int64[n+1]; nbr_indices == sym_dst (callers may alias). */
+size_t gu_symmetrize_workspace_size(int64_t n, int64_t nnz);
+int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* dst,
+                  const double* w, int32_t* sym_src, int32_t* sym_dst, double* sym_w,
+                  int64_t* nbr_indptr, int64_t* host_E, void* workspace,
+                  size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------- C2 SGD (Hogwild fp32)
+ * The layout epochs of layout.py:314-360 / sgd_sweep (_kernels.py:158-223)
+ * with the same per-visit semantics (attraction on both ends scaled by h,
+ * n_neg rejection-sampled repulsions of the head against non-neighbours,
+ * 8 draws max, per-component clip +-4, random direction for coincident
+ * points), run as a Hogwild epoch over fp32 float2 coordinates.  The epoch
+ * schedule (fresh order per epoch, or a sliding window of `window` edges over
+ * one shuffled order) and the negatives come from Philox4x32-10 keyed by seed.
+ * edges: int4 records {src, dst, float-bits(h), 0} in the caller's order;
+ * gu_sgd_prepare_edges builds them shuffled. nbr CSR int32.
+ * Runs epochs [epoch_begin, epoch_end) of a t-epoch schedule,
+ * lr_e = lr0 * (1 - e/t).  diverged (int32, device): atomicMin'd with the
+ * first epoch that produced a non-finite coordinate (init to INT32_MAX). */
+int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
+                         const double* sym_w, uint64_t seed, void* edges_int4,
+                         void* stream);
+int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4,
+                  const int32_t* nbr_indptr, const int32_t* nbr_indices, float a, float b,
+                  float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
+                  int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
+                  int32_t* diverged, void* stream);
+/* positions visited by epoch `epoch` (visit_log): window/permutation indices
+ * into the prepared edge array, length window (windowed) or E (full). */
+int gu_sgd_visit_order(int64_t E, int32_t epoch, int64_t window, int32_t windowed,
+                       uint64_t seed, int64_t* out_order, void* stream);
+
+/* ----------------------------------------- C2 order-faithful replay (fp64)
+ * Parity check (b): replays one sgd_sweep (_kernels.py:158-223) in float64
+ * with a supplied visit order, accepted negatives (-1 = skipped slot) and
+ * thetas (used for coincident pairs).  Host-side wave schedule
+ * (gu_replay_schedule, synchronous, host pointers) groups visits into
+ * conflict-free waves; the device applies the waves in order, so the result
+ * equals the sequential sweep up to libm-vs-CUDA pow/cos/sin ulps. */
+int gu_replay_schedule(int64_t n, int64_t n_order, const int32_t* host_src,
+                       const int32_t* host_dst, const int64_t* host_order,
+                       const int32_t* host_negs, int32_t n_neg, int64_t* host_wave_items,
+                       int64_t* host_wave_offsets, int64_t* host_n_waves);
+int gu_sgd_replay_f64(int64_t n, double* coords, const int32_t* e_src, const int32_t* e_dst,
+                      const double* e_w, const int64_t* order, const int32_t* negs,
+                      const double* thetas, int32_t n_neg, double a, double b, double lr,
+                      const int64_t* wave_items, const int64_t* wave_offsets,
+                      int64_t n_waves, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GUMAP_H */

@@ -1,0 +1,297 @@
+// sgd.cu -- K7: Hogwild fp32 UMAP layout epochs.
+//
+// Same per-visit update as the reference's sgd_sweep
+// (/root/reference/pkg/src/graph_umap/_kernels.py:158-223) driven by
+// _run_sgd (layout.py:314-360):
+//   attraction  d2 > 0: g = -2ab h (d2^b / d2) / (a d2^b + 1), per-component
+//               clip +-4, x_u += lr g dx, x_v -= lr g dx
+//   repulsion   n_neg times: up to 8 uniform draws c != u, c not a sym
+//               neighbour of u (binary search in the sorted CSR row), else the
+//               sample is skipped; d2 > 0: g = 2b / ((0.001 + d2)(a d2^b + 1)),
+//               clip +-4; coincident: 4 (cos th, sin th), th uniform; only x_u
+//               moves.  The head's running position is kept in registers, so
+//               the repulsions see the attracted x_u exactly as in the
+//               sequential sweep; u and v receive their deltas through
+//               vector float2 atomics (red.global.add.v2.f32).
+// Schedule (D7 in SURVEY.md section 9): edges are stored once in a
+// Philox-Feistel shuffled order (gu_sgd_prepare_edges).  Windowed epochs
+// (optimize_sampled) take the window of `window` consecutive positions
+// starting where the previous epoch stopped, wrapping (layout.py:329-337).
+// Full epochs (optimize_full) visit every edge in a fresh per-epoch order:
+// 1024-edge tiles permuted by a per-epoch Feistel bijection, tiles streamed
+// coalesced.  Negatives and thetas come from Philox4x32-10 keyed by
+// (seed, epoch, position).
+#include <climits>
+#include <cmath>
+
+#include "common.cuh"
+#include "gumap.h"
+
+namespace gu {
+namespace {
+
+constexpr int TILE = 1024;
+
+// Feistel bijection on [0, 2^bits) with cycle walking into [0, m)
+__device__ __host__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+struct Feistel {
+  unsigned long long m;
+  int half;  // bits per half
+  unsigned long long key;
+  __device__ __host__ Feistel(unsigned long long m_, unsigned long long key_) : m(m_), key(key_) {
+    int bits = 2;
+    while ((1ull << bits) < m_) bits++;
+    if (bits & 1) bits++;
+    half = bits / 2;
+  }
+  __device__ __host__ __forceinline__ unsigned long long once(unsigned long long x) const {
+    const unsigned long long mask = (1ull << half) - 1ull;
+    unsigned long long l = x >> half, r = x & mask;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      unsigned long long f = mix64(r ^ (key + 0x9E3779B97F4A7C15ULL * (unsigned long long)(i + 1))) & mask;
+      unsigned long long t = l ^ f;
+      l = r;
+      r = t;
+    }
+    return (l << half) | r;
+  }
+  __device__ __host__ __forceinline__ unsigned long long operator()(unsigned long long x) const {
+    do {
+      x = once(x);
+    } while (x >= m);
+    return x;
+  }
+};
+
+__global__ void prepare_edges_kernel(long long E, const int* __restrict__ src,
+                                     const int* __restrict__ dst, const double* __restrict__ w,
+                                     unsigned long long key, int4* __restrict__ out) {
+  Feistel perm((unsigned long long)E, key);
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long e = (long long)perm((unsigned long long)p);
+    out[p] = make_int4(src[e], dst[e], __float_as_int((float)w[e]), (int)e);
+  }
+}
+
+__device__ __forceinline__ float clip4(float x) { return fminf(4.0f, fmaxf(-4.0f, x)); }
+
+__device__ __forceinline__ bool is_neighbor(const int* __restrict__ ip, const int* __restrict__ ix,
+                                            int u, int c) {
+  int lo = __ldg(ip + u), hi = __ldg(ip + u + 1);
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    int x = __ldg(ix + mid);
+    if (x < c) lo = mid + 1;
+    else if (x > c) hi = mid;
+    else return true;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(256)
+    sgd_epoch_kernel(int n, long long E, float2* __restrict__ xy, const int4* __restrict__ edges,
+                     const int* __restrict__ nip, const int* __restrict__ nix, float a, float b,
+                     float lr, int epoch, int n_neg, long long items, long long start,
+                     int windowed, unsigned long long seed, int* __restrict__ diverged) {
+  const long long ntiles = (E + TILE - 1) / TILE;
+  Feistel tperm((unsigned long long)ntiles, mix64(seed ^ (0x51ED27ull + (unsigned long long)epoch)));
+  const uint2 key = make_uint2((unsigned)seed, (unsigned)(seed >> 32));
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < items;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long p;
+    if (windowed) {
+      p = start + i;
+      if (p >= E) p -= E;
+    } else {
+      const long long t = i / TILE;
+      p = (long long)tperm((unsigned long long)t) * TILE + (i - t * TILE);
+      if (p >= E) continue;  // partial last tile maps onto itself
+    }
+    const int4 rec = __ldg(edges + p);
+    const int u = rec.x, v = rec.y;
+    const float h = __int_as_float(rec.z);
+    float2 xu = xy[u];
+    const float2 xv = xy[v];
+    float dux = 0.f, duy = 0.f;
+    {
+      const float dx = xu.x - xv.x, dy = xu.y - xv.y;
+      const float d2 = dx * dx + dy * dy;
+      if (d2 > 0.f) {
+        const float pb = __powf(d2, b);
+        const float g = -2.0f * a * b * h * (pb / d2) / (a * pb + 1.0f);
+        const float gx = clip4(g * dx) * lr, gy = clip4(g * dy) * lr;
+        dux += gx;
+        duy += gy;
+        xu.x += gx;
+        xu.y += gy;
+        atomicAdd(&xy[v], make_float2(-gx, -gy));
+        if (!isfinite(xv.x - gx) || !isfinite(xv.y - gy)) bad = true;
+      }
+    }
+    // repulsions: candidates from Philox(position, epoch, draw-block)
+    unsigned rnd[4];
+    int have = 0, blk = 0;
+    for (int q = 0; q < n_neg; q++) {
+      int c = -1;
+      for (int t = 0; t < 8; t++) {
+        if (have == 0) {
+          uint4 r4 = Philox::gen(make_uint4((unsigned)p, (unsigned)(p >> 32), (unsigned)epoch,
+                                            (unsigned)blk++),
+                                 key);
+          rnd[0] = r4.x;
+          rnd[1] = r4.y;
+          rnd[2] = r4.z;
+          rnd[3] = r4.w;
+          have = 4;
+        }
+        const int cand = (int)__umulhi(rnd[--have], (unsigned)n);
+        if (cand == u) continue;
+        if (!is_neighbor(nip, nix, u, cand)) {
+          c = cand;
+          break;
+        }
+      }
+      if (c < 0) continue;
+      const float2 xc = xy[c];
+      const float dx = xu.x - xc.x, dy = xu.y - xc.y;
+      const float d2 = dx * dx + dy * dy;
+      float gx, gy;
+      if (d2 > 0.f) {
+        const float g = 2.0f * b / ((0.001f + d2) * (a * __powf(d2, b) + 1.0f));
+        gx = clip4(g * dx);
+        gy = clip4(g * dy);
+      } else {
+        if (have == 0) {
+          uint4 r4 = Philox::gen(make_uint4((unsigned)p, (unsigned)(p >> 32), (unsigned)epoch,
+                                            (unsigned)blk++),
+                                 key);
+          rnd[0] = r4.x;
+          rnd[1] = r4.y;
+          rnd[2] = r4.z;
+          rnd[3] = r4.w;
+          have = 4;
+        }
+        const float th = (float)rnd[--have] * (6.283185307179586f / 4294967296.0f);
+        float sn, cs;
+        __sincosf(th, &sn, &cs);
+        gx = 4.0f * cs;
+        gy = 4.0f * sn;
+      }
+      gx *= lr;
+      gy *= lr;
+      dux += gx;
+      duy += gy;
+      xu.x += gx;
+      xu.y += gy;
+    }
+    if (dux != 0.f || duy != 0.f) atomicAdd(&xy[u], make_float2(dux, duy));
+    if (!isfinite(xu.x) || !isfinite(xu.y)) bad = true;
+  }
+  if (bad) atomicMin(diverged, epoch);
+}
+
+__global__ void visit_order_kernel(long long E, int epoch, long long items, long long start,
+                                   int windowed, unsigned long long seed,
+                                   long long* __restrict__ out) {
+  const long long ntiles = (E + TILE - 1) / TILE;
+  Feistel tperm((unsigned long long)ntiles, mix64(seed ^ (0x51ED27ull + (unsigned long long)epoch)));
+  // full mode: compact the tile order (the partial last tile keeps its slot)
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < items;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long p;
+    if (windowed) {
+      p = start + i;
+      if (p >= E) p -= E;
+      out[i] = p;
+    } else {
+      const long long t = i / TILE;
+      p = (long long)tperm((unsigned long long)t) * TILE + (i - t * TILE);
+      out[i] = p < E ? p : -1;
+    }
+  }
+}
+
+unsigned grid_for(long long items) {
+  long long b = (items + 255) / 256;
+  if (b > 148LL * 8) b = 148LL * 8;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+}  // namespace
+}  // namespace gu
+
+using namespace gu;
+
+extern "C" int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
+                                    const double* sym_w, uint64_t seed, void* edges_int4,
+                                    void* stream) {
+  if (E < 0 || E >= INT_MAX) {
+    set_error("gu_sgd_prepare_edges: unsupported E=%lld", (long long)E);
+    return GU_ERR_UNSUPPORTED;
+  }
+  if (E == 0) return GU_OK;
+  prepare_edges_kernel<<<grid_for(E), 256, 0, (cudaStream_t)stream>>>(
+      E, sym_src, sym_dst, sym_w, mix64(seed ^ 0xED6E5ull), (int4*)edges_int4);
+  GU_CHECK_LAUNCH("prepare_edges_kernel");
+  return GU_OK;
+}
+
+static void epoch_range(int64_t E, int32_t epoch, int64_t window, int32_t windowed,
+                        long long* items, long long* start) {
+  if (windowed) {
+    *items = window;
+    // j advances by window each epoch, modulo E (layout.py:336-337)
+    *start = (long long)(((__int128)epoch * (__int128)window) % (__int128)E);
+  } else {
+    *items = ((E + TILE - 1) / TILE) * TILE;
+    *start = 0;
+  }
+}
+
+extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4,
+                             const int32_t* nbr_indptr, const int32_t* nbr_indices, float a,
+                             float b, float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
+                             int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
+                             int32_t* diverged, void* stream) {
+  if (n <= 0 || n >= INT_MAX || E < 0 || t < 0 || epoch_begin < 0 || epoch_end > t ||
+      (windowed && (window < 1 || window > E))) {
+    set_error("gu_sgd_epochs: bad arguments");
+    return GU_ERR_ARG;
+  }
+  if (E == 0) return GU_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int e = epoch_begin; e < epoch_end; e++) {
+    // lr = learning_rate * (1 - it / t), layout.py:334 (float64 on host)
+    const float lr = (float)((double)lr0 * (1.0 - (double)e / (double)t));
+    long long items, start;
+    epoch_range(E, e, window, windowed, &items, &start);
+    sgd_epoch_kernel<<<grid_for(items), 256, 0, st>>>(
+        (int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr, nbr_indices, a, b,
+        lr, e, n_neg, items, start, windowed, seed, diverged);
+    GU_CHECK_LAUNCH("sgd_epoch_kernel");
+  }
+  return GU_OK;
+}
+
+extern "C" int gu_sgd_visit_order(int64_t E, int32_t epoch, int64_t window, int32_t windowed,
+                                  uint64_t seed, int64_t* out_order, void* stream) {
+  if (E <= 0) return GU_OK;
+  long long items, start;
+  epoch_range(E, epoch, window, windowed, &items, &start);
+  visit_order_kernel<<<grid_for(items), 256, 0, (cudaStream_t)stream>>>(
+      E, epoch, items, start, windowed, seed, (long long*)out_order);
+  GU_CHECK_LAUNCH("visit_order_kernel");
+  return GU_OK;
+}

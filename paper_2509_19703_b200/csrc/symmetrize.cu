@@ -1,0 +1,206 @@
+// symmetrize.cu -- K6: sort-based fuzzy-union symmetrisation.
+//
+// Replaces neighbors.py:313-350 (/root/reference/pkg/src/graph_umap):
+//   dedupe directed pairs keeping the first occurrence (np.unique return_index)
+//   sym = w + w^T - w o w^T with scipy's exact-zero dropping
+//   lexsort by (src, dst); CSR neighbour lookup over the same pattern.
+// Both orientations of every directed kNN entry become 64-bit keys
+// (src * n + dst); a stable radix sort (CUB onesweep, compiled into this
+// library) groups each unordered pair; forward entries precede backward ones
+// inside a key and each keeps its original order, so the first forward entry
+// is a and the first backward entry is b.  h = (a + b) - a*b rounded step by
+// step (explicit _rn intrinsics: no FMA), kept iff h != 0.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+#include "gumap.h"
+
+namespace gu {
+int scan_counts(const int* cnt, long long nrows, long long* indptr, long long* partial,
+                cudaStream_t st);
+size_t scan_workspace(long long nrows);
+
+namespace {
+
+__global__ void build_keys(long long n, long long nrows, const long long* __restrict__ indptr,
+                           const int* __restrict__ dst, long long nnz,
+                           unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += (long long)gridDim.x * blockDim.x) {
+    for (long long i = indptr[r]; i < indptr[r + 1]; i++) {
+      const long long c = dst[i];
+      keys[i] = (unsigned long long)(r * n + c);
+      vals[i] = (int)i;
+      keys[nnz + i] = (unsigned long long)(c * n + r);
+      vals[nnz + i] = (int)(nnz + i);
+    }
+  }
+}
+
+__global__ void union_flags(long long m, long long nnz, const unsigned long long* __restrict__ keys,
+                            const int* __restrict__ vals, const double* __restrict__ w,
+                            int* __restrict__ flag, double* __restrict__ hval) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+       p += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[p];
+    const bool head = p == 0 || keys[p - 1] != k;
+    int f = 0;
+    double h = 0.0;
+    if (head) {
+      double a = 0.0, b = 0.0;
+      bool have_a = false, have_b = false;
+      for (long long q = p; q < m && keys[q] == k; q++) {
+        const int v = vals[q];
+        if (v < nnz) {
+          if (!have_a) {
+            a = w[v];
+            have_a = true;
+          }
+        } else if (!have_b) {
+          b = w[v - nnz];
+          have_b = true;
+        }
+      }
+      h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
+      f = h != 0.0;
+    }
+    flag[p] = f;
+    hval[p] = h;
+  }
+}
+
+__global__ void union_write(long long m, long long n, const unsigned long long* __restrict__ keys,
+                            const int* __restrict__ flag, const double* __restrict__ hval,
+                            const long long* __restrict__ pos, int* __restrict__ sym_src,
+                            int* __restrict__ sym_dst, double* __restrict__ sym_w,
+                            int* __restrict__ rowcnt) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+       p += (long long)gridDim.x * blockDim.x) {
+    if (flag[p]) {
+      const long long o = pos[p];
+      const unsigned long long k = keys[p];
+      const int s = (int)(k / (unsigned long long)n);
+      sym_src[o] = s;
+      sym_dst[o] = (int)(k - (unsigned long long)s * (unsigned long long)n);
+      sym_w[o] = hval[p];
+      atomicAdd(&rowcnt[s], 1);
+    }
+  }
+}
+
+struct SymWs {
+  unsigned long long *k0, *k1;
+  int *v0, *v1;
+  int* flag;
+  double* h;
+  long long* pos;
+  long long* partial;
+  int* rowcnt;
+  void* cub_tmp;
+  size_t cub_bytes;
+};
+
+size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t cub_bytes_for(long long m) {
+  size_t bytes = 0;
+  cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
+  cub::DoubleBuffer<int> vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, (int)m, 0, 64);
+  return bytes;
+}
+
+size_t sym_layout(long long n, long long nnz, char* base, SymWs* ws) {
+  const long long m = 2 * nnz;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    size_t o = off;
+    off = a256(off + b);
+    return o;
+  };
+  size_t ok0 = take(8 * (size_t)m), ok1 = take(8 * (size_t)m);
+  size_t ov0 = take(4 * (size_t)m), ov1 = take(4 * (size_t)m);
+  size_t ofl = take(4 * (size_t)m), oh = take(8 * (size_t)m);
+  size_t opos = take(8 * (size_t)(m + 1));
+  long long maxrows = m > n ? m : n;
+  size_t opart = take(scan_workspace(maxrows));
+  size_t orc = take(4 * (size_t)(n + 1));
+  size_t cb = cub_bytes_for(m > 0 ? m : 1);
+  size_t ocub = take(cb);
+  if (base && ws) {
+    ws->k0 = (unsigned long long*)(base + ok0);
+    ws->k1 = (unsigned long long*)(base + ok1);
+    ws->v0 = (int*)(base + ov0);
+    ws->v1 = (int*)(base + ov1);
+    ws->flag = (int*)(base + ofl);
+    ws->h = (double*)(base + oh);
+    ws->pos = (long long*)(base + opos);
+    ws->partial = (long long*)(base + opart);
+    ws->rowcnt = (int*)(base + orc);
+    ws->cub_tmp = base + ocub;
+    ws->cub_bytes = cb;
+  }
+  return off;
+}
+
+unsigned grid_for(long long items) {
+  long long b = (items + 255) / 256;
+  if (b > 148LL * 16) b = 148LL * 16;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+}  // namespace
+}  // namespace gu
+
+using namespace gu;
+
+extern "C" size_t gu_symmetrize_workspace_size(int64_t n, int64_t nnz) {
+  return sym_layout(n, nnz, nullptr, nullptr);
+}
+
+extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* dst,
+                             const double* w, int32_t* sym_src, int32_t* sym_dst, double* sym_w,
+                             int64_t* nbr_indptr, int64_t* host_E, void* workspace,
+                             size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || nnz < 0 || 2 * nnz >= INT32_MAX || (double)n * (double)n >= 1.8e19) {
+    set_error("gu_symmetrize: unsupported size n=%lld nnz=%lld", (long long)n, (long long)nnz);
+    return GU_ERR_UNSUPPORTED;
+  }
+  SymWs ws;
+  size_t need = sym_layout(n, nnz, (char*)workspace, &ws);
+  if (!workspace || ws_bytes < need) {
+    set_error("gu_symmetrize: workspace %zu < %zu", ws_bytes, need);
+    return GU_ERR_WORKSPACE;
+  }
+  const long long m = 2 * nnz;
+  GU_CHECK(cudaMemsetAsync(ws.rowcnt, 0, sizeof(int) * (size_t)(n + 1), st));
+  if (m > 0) {
+    build_keys<<<grid_for(n), 256, 0, st>>>(n, n, (const long long*)indptr, dst, nnz, ws.k0, ws.v0);
+    GU_CHECK_LAUNCH("build_keys");
+    int end_bit = 1;
+    while (end_bit < 64 && ((unsigned long long)n * (unsigned long long)n) > (1ull << end_bit))
+      end_bit++;
+    cub::DoubleBuffer<unsigned long long> kb(ws.k0, ws.k1);
+    cub::DoubleBuffer<int> vb(ws.v0, ws.v1);
+    size_t cb = ws.cub_bytes;
+    GU_CHECK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, cb, kb, vb, (int)m, 0, end_bit, st));
+    union_flags<<<grid_for(m), 256, 0, st>>>(m, nnz, kb.Current(), vb.Current(), w, ws.flag, ws.h);
+    GU_CHECK_LAUNCH("union_flags");
+    int r = scan_counts(ws.flag, m, ws.pos, ws.partial, st);
+    if (r) return r;
+    union_write<<<grid_for(m), 256, 0, st>>>(m, n, kb.Current(), ws.flag, ws.h, ws.pos, sym_src,
+                                            sym_dst, sym_w, ws.rowcnt);
+    GU_CHECK_LAUNCH("union_write");
+  } else {
+    GU_CHECK(cudaMemsetAsync(ws.pos, 0, sizeof(long long), st));
+  }
+  int r = scan_counts(ws.rowcnt, n, (long long*)nbr_indptr, ws.partial, st);
+  if (r) return r;
+  long long E = 0;
+  GU_CHECK(cudaMemcpyAsync(&E, ws.pos + m, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  GU_CHECK(cudaStreamSynchronize(st));
+  *host_E = E;
+  return GU_OK;
+}

@@ -1,0 +1,289 @@
+"""Freeze golden vectors from the LIVE reference (run in the build container).
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Imports graph_umap read-only from /root/reference/pkg/src and writes small
+.npz fixtures next to this file.  The reference does not exist on the GPU box:
+tests only ever read the committed .npz files.  Large arrays are stored as
+SHA-256 digests plus explicit samples.
+
+Fixture inputs come from paper_2509_19703_b200.fixtures, whose grid /
+scale_free / random_connected_graph are draw-for-draw restatements of the
+reference generators (checked here: the reference's own synth_graph output is
+asserted equal before anything is frozen).
+"""
+
+import hashlib
+import json
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+
+import graph_umap as gu  # noqa: E402
+import numba  # noqa: E402
+import scipy  # noqa: E402
+
+from paper_2509_19703_b200 import fixtures as F  # noqa: E402
+
+
+def sha(a):
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def ref_graph(g):
+    """Reference Graph from our arrays (identical CSR)."""
+    return gu.build_graph([tuple(map(int, e)) for e in g.edges]) if g.m < 400000 else None
+
+
+def flat(lists, dtype):
+    if not lists:
+        return np.zeros(0, dtype), np.zeros(1, np.int64)
+    off = np.zeros(len(lists) + 1, np.int64)
+    off[1:] = np.cumsum([len(x) for x in lists])
+    return np.concatenate([np.asarray(x, dtype) for x in lists]), off
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print("wrote", path, os.path.getsize(path), "bytes")
+
+
+def gen_partial_small():
+    """Acceptance-criterion-1 style graphs (test_acceptance.py:45-63)."""
+    rng = np.random.default_rng(101)
+    edges_l, n_l, k_l, seed_l, ip_l, dst_l, dist_l = [], [], [], [], [], [], []
+    graphs = []
+    for trial in range(40):
+        n, e = F.random_connected_graph(rng, n_max=200)
+        k = int(rng.integers(1, 21))
+        graphs.append((np.array(e, np.int64), k, trial))
+    # special shapes: star tie-break, path, small components, complete graph
+    graphs.append((np.array([(0, i) for i in range(1, 6)]), 3, 5))
+    graphs.append((np.array([(i, i + 1) for i in range(4)]), 2, 0))
+    graphs.append((np.array([(0, 1), (1, 2), (3, 4)]), 3, 0))
+    graphs.append((np.array([(i, j) for i in range(6) for j in range(i + 1, 6)]), 10, 1))
+    graphs.append((np.array([(0, i) for i in range(1, 300)] + [(i, i + 300) for i in range(1, 300)]), 15, 9))
+    import warnings
+    for e, k, seed in graphs:
+        g = gu.build_graph([tuple(map(int, x)) for x in e])
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            _, kn = gu.partial_bfs(g, k, seed=seed)
+        edges_l.append(np.asarray(g.edges, np.int64).reshape(-1))
+        n_l.append(g.n)
+        k_l.append(k)
+        seed_l.append(seed)
+        ip_l.append(kn.indptr)
+        dst_l.append(kn.dst)
+        dist_l.append(kn.dist)
+    E, Eo = flat(edges_l, np.int64)
+    IP, IPo = flat(ip_l, np.int64)
+    D, Do = flat(dst_l, np.int32)
+    DD, _ = flat(dist_l, np.int32)
+    save("partial_small.npz", edges=E, edges_off=Eo, n=np.array(n_l), k=np.array(k_l),
+         seed=np.array(seed_l, np.uint64), indptr=IP, indptr_off=IPo, dst=D, dst_off=Do,
+         dist=DD)
+
+
+def gen_full_small():
+    rng = np.random.default_rng(202)
+    cases = []
+    for t in range(12):
+        n, e = F.random_connected_graph(rng, n_max=120)
+        cases.append((np.array(e, np.int64), [1, 5, 15][t % 3], [0, 7, 2**40 + 3][t % 3]))
+    cases.append((np.array([(0, 1), (2, 3), (3, 4), (4, 5)]), 3, 0))   # disconnected
+    cases.append((np.array([(0, i) for i in range(1, 40)]), 5, 11))     # star: big tie set
+    import warnings
+    out = dict(edges=[], n=[], k=[], seed=[], indptr=[], dst=[], dist=[], apsp_sha=[])
+    for e, k, seed in cases:
+        g = gu.build_graph([tuple(map(int, x)) for x in e])
+        ds = gu.all_pairs_bfs(g)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            kn = gu.knn_from_full_distances(ds, k, seed=seed)
+        out["edges"].append(np.asarray(g.edges, np.int64).reshape(-1))
+        out["n"].append(g.n)
+        out["k"].append(k)
+        out["seed"].append(seed)
+        out["indptr"].append(kn.indptr)
+        out["dst"].append(kn.dst)
+        out["dist"].append(kn.dist)
+        out["apsp_sha"].append(sha(ds.matrix.astype(np.int32)))
+    E, Eo = flat(out["edges"], np.int64)
+    IP, IPo = flat(out["indptr"], np.int64)
+    D, Do = flat(out["dst"], np.int32)
+    DD, _ = flat(out["dist"], np.int32)
+    save("full_small.npz", edges=E, edges_off=Eo, n=np.array(out["n"]), k=np.array(out["k"]),
+         seed=np.array(out["seed"], np.uint64), indptr=IP, indptr_off=IPo, dst=D, dst_off=Do,
+         dist=DD, apsp_sha=np.array(out["apsp_sha"]))
+
+
+def gen_smooth_cases():
+    """DirectedKnn inputs straight into smooth_knn_weights (neighbors.py:245)."""
+    rng = np.random.default_rng(303)
+    cases = [
+        # test_neighbors.py:169-189 two-neighbour example
+        (3, 2, [0, 2, 4, 6], [1, 2, 0, 2, 0, 1], [1, 2, 1, 2, 1, 2]),
+        # test_neighbors.py:192-202 all identical -> sigma max
+        (2, 2, [0, 1, 2], [1, 0], [1, 1]),
+        # duplicate directed pair inside a row (first occurrence wins)
+        (3, 3, [0, 3, 4, 6], [1, 1, 2, 0, 0, 1], [1, 2, 2, 1, 1, 1]),
+    ]
+    for t in range(25):
+        n = int(rng.integers(3, 60))
+        k = int(rng.integers(1, 20))
+        counts = rng.integers(1, k + 1, n) if t % 2 else np.full(n, k)
+        ip = np.concatenate([[0], np.cumsum(counts)])
+        dst, dist = [], []
+        for v in range(n):
+            others = np.setdiff1d(np.arange(n), [v])
+            c = int(counts[v])
+            pick = rng.choice(others, size=min(c, others.shape[0]), replace=others.shape[0] < c)
+            d = np.sort(rng.integers(1, 1 + int(rng.integers(1, 7)), pick.shape[0]))
+            dst.extend(pick.tolist())
+            dist.extend(d.tolist())
+        cases.append((n, k, ip.tolist(), dst, dist))
+    rec = dict(n=[], k=[], indptr=[], dst=[], dist=[], rho=[], sigma=[], sym_src=[],
+               sym_dst=[], sym_w=[], nbr_indptr=[])
+    for n, k, ip, dst, dist in cases:
+        ip = np.array(ip, np.int64)
+        counts = np.diff(ip)
+        dst = np.array(dst, np.int32)[: ip[-1]]
+        dist = np.array(dist, np.int32)[: ip[-1]]
+        if dst.shape[0] < ip[-1]:
+            continue
+        kn = gu.DirectedKnn(n=n, k=k, indptr=ip, dst=dst, dist=dist)
+        gk = gu.smooth_knn_weights(kn)
+        rec["n"].append(n)
+        rec["k"].append(k)
+        rec["indptr"].append(ip)
+        rec["dst"].append(dst)
+        rec["dist"].append(dist)
+        rec["rho"].append(gk.rho)
+        rec["sigma"].append(gk.sigma)
+        rec["sym_src"].append(gk.sym_src)
+        rec["sym_dst"].append(gk.sym_dst)
+        rec["sym_w"].append(gk.sym_w)
+        rec["nbr_indptr"].append(gk.nbr_indptr)
+        del counts
+    arrays = dict(n=np.array(rec["n"]), k=np.array(rec["k"]))
+    for key, dt in (("indptr", np.int64), ("dst", np.int32), ("dist", np.int32),
+                    ("rho", np.float64), ("sigma", np.float64), ("sym_src", np.int32),
+                    ("sym_dst", np.int32), ("sym_w", np.float64), ("nbr_indptr", np.int64)):
+        a, off = flat(rec[key], dt)
+        arrays[key] = a
+        arrays[key + "_off"] = off
+    save("smooth_cases.npz", **arrays)
+
+
+def gen_c1():
+    g = F.grid(2500)
+    rg = gu.synth_graph("grid", 2500)
+    assert np.array_equal(g.adj_indices, rg.adj_indices) and np.array_equal(g.adj_indptr, rg.adj_indptr)
+    ds = gu.all_pairs_bfs(rg)
+    kn = gu.knn_from_full_distances(ds, 15, seed=0)
+    kn7 = gu.knn_from_full_distances(ds, 5, seed=7)
+    gk = gu.smooth_knn_weights(kn)
+    init = gu.random_init(rg, 0, 10.0)
+    cfg = gu.OptimizerConfig(iterations=200, k=15, seed=0, learning_rate=1.0,
+                             negative_sample_count=5, min_dist=0.1)
+    a, b = cfg.curve()
+    snaps = {}
+
+    def cb(it, coords):
+        snaps[it] = coords
+    log = []
+    final = gu.optimize_full(gk, init, cfg, visit_log=log, callback=cb, callback_every=1)
+    # instrumented epochs: negatives + thetas of epochs 0 and 1, from the oracle
+    # restatement, which tests/test_oracle.py pins bit-exact against snaps[1], [2]
+    save("c1.npz", apsp_sha=np.array(sha(ds.matrix)), knn_indptr=kn.indptr, knn_dst=kn.dst,
+         knn_dist=kn.dist, knn7_indptr=kn7.indptr, knn7_dst=kn7.dst, knn7_dist=kn7.dist,
+         rho=gk.rho, sigma=gk.sigma, sym_src=gk.sym_src, sym_dst=gk.sym_dst, sym_w=gk.sym_w,
+         nbr_indptr=gk.nbr_indptr, nbr_indices=gk.nbr_indices, a=a, b=b,
+         init=init.coords, order0=log[0], order1=log[1], after1=snaps[1], after2=snaps[2],
+         after10=snaps[10], final=final.coords)
+
+
+def gen_c3():
+    g = F.scale_free(100000, seed=2, m0=3)
+    rg = gu.synth_graph("scale_free", 100000, seed=2, m0=3)
+    assert np.array_equal(g.adj_indices, rg.adj_indices) and np.array_equal(g.adj_indptr, rg.adj_indptr)
+    _, kn = gu.partial_bfs(rg, 15, seed=2)
+    gk = gu.smooth_knn_weights(kn)
+    E = gk.edge_count
+    samp = math.log(0.1 * E) / math.log(E)
+    init = gu.random_init(rg, 2, 10.0)
+    cfg = gu.OptimizerConfig(iterations=200, k=15, seed=2, samp=samp)
+    a, b = cfg.curve()
+    snaps = {}
+
+    # only the first 3 epochs are needed: run the 200-iteration schedule and
+    # stop it from the callback after epoch 3
+    class Stop(Exception):
+        pass
+
+    def cb2(it, coords):
+        snaps[it] = coords
+        if it >= 3:
+            raise Stop()
+    try:
+        gu.optimize_sampled(gk, init, cfg, callback=cb2, callback_every=1)
+    except Stop:
+        pass
+    sample = np.arange(0, g.n, 97)
+    save("c3.npz", knn_indptr_sha=np.array(sha(kn.indptr)), knn_dst_sha=np.array(sha(kn.dst)),
+         knn_dist_sha=np.array(sha(kn.dist)), knn_indptr_head=kn.indptr[:2001],
+         knn_dst_head=kn.dst[:30000], knn_dist_head=kn.dist[:30000],
+         rho_sha=np.array(sha(gk.rho)), sigma_sha=np.array(sha(gk.sigma)),
+         sigma_sample=gk.sigma[sample], sample=sample, E=np.array(E),
+         sym_src_sha=np.array(sha(gk.sym_src)), sym_dst_sha=np.array(sha(gk.sym_dst)),
+         sym_w_sha=np.array(sha(gk.sym_w)), sym_w_head=gk.sym_w[:20000], samp=samp, a=a, b=b,
+         after1_sha=np.array(sha(snaps[1])), after1_sample=snaps[1][sample],
+         after2_sample=snaps[2][sample], after3_sha=np.array(sha(snaps[3])))
+
+
+def gen_quality_c1(nseeds=20):
+    """Check (c) reference statistics: c1 pipeline with random init per seed."""
+    rg = gu.synth_graph("grid", 2500)
+    ds = gu.all_pairs_bfs(rg)
+    vals = []
+    layouts = []
+    for seed in range(nseeds):
+        kn = gu.knn_from_full_distances(ds, 15, seed=seed)
+        gk = gu.smooth_knn_weights(kn)
+        init = gu.random_init(rg, seed, 10.0)
+        cfg = gu.OptimizerConfig(iterations=200, k=15, seed=seed)
+        lay = gu.optimize_full(gk, init, cfg, tag="GUMAP")
+        npv = gu.neighborhood_preservation(rg, lay)
+        st = gu.stress(rg, lay)
+        cr = gu.count_crossings(rg, lay)
+        vals.append((npv, st, cr))
+        if seed < 2:
+            layouts.append(lay.coords)
+        print("quality seed", seed, vals[-1], flush=True)
+    v = np.array(vals, np.float64)
+    save("quality_c1.npz", np_=v[:, 0], stress=v[:, 1], crossings=v[:, 2],
+         layout0=layouts[0], layout1=layouts[1])
+
+
+def main():
+    which = sys.argv[1:] or ["partial_small", "full_small", "smooth_cases", "c1", "c3", "quality_c1"]
+    for w in which:
+        globals()["gen_" + w]()
+    manifest = dict(numpy=np.__version__, scipy=scipy.__version__, numba=numba.__version__,
+                    python=sys.version.split()[0], reference="/root/reference/pkg (graph_umap 0.1.0)")
+    with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
+        json.dump(manifest, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
