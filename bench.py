@@ -1,0 +1,432 @@
+"""Benchmark: BFS-kNN GTEPS (headline), SGD edge-updates/s, end-to-end layout s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1)
+
+Workload (BASELINE.json configs[4], the scaling-sweep config): partial-BFS
+kNN, k = 15, on a random geometric graph in the unit square, n = 4,000,000,
+radius for average degree 12, seed 4, largest component (3,999,956
+vertices, 23,983,705 edges).  One step = one pass of the C0 hot path over
+every source of this rank's shard (sources sharded across ranks, records
+all-gathered over NCCL when N > 1).  The graph CSR (208 MB) is larger than
+the 126 MB L2 and L2 is additionally flushed (256 MB write) before every
+timed step, outside the step's CUDA events.
+
+Work unit: TE = adjacency entries the reference algorithm
+scans (sum over sources of the degrees of expanded vertices), counted by the
+kernel itself; GTEPS = TE / step time.  Roofline: algorithmic bytes per
+launch = 8 * expanded + 4 * scanned + 8 * k * sources (two int32 offsets per
+expanded vertex, one int32 per scanned entry, k (id, dist) int32 pairs
+written) over the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+
+Secondary lines inside the same JSON object:
+  sgd         Hogwild fp32 full epochs on the c5 kNN graph (E = sym edges),
+              edge-updates/s (one positive visit + 5 negatives), 88 B/update
+  layout_e2e  SL-GUMAP on c3 (BA n=100k, 200 epochs, 10% window, random
+              init) through the public API from host arrays: seconds
+The CPU baseline is the oracle's C port of the reference algorithm
+(oracle/oracle.c, all host threads) on a bounded sample of sources; the
+reference itself is Python/numba and cannot travel to the GPU box.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K_NN = 15
+SEED = 4
+WORKLOAD = "c5: partial-BFS kNN k=15 on RGG(n=4M, avg deg 12, seed 4) LCC"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _profile_traffic(kernel):
+    """dram bytes per launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_graph(name="c5"):
+    from paper_2509_19703_b200 import fixtures
+    t = time.time()
+    g = fixtures.config_graph(name)
+    return g, time.time() - t
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = _dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    import paper_2509_19703_b200 as gu
+    from paper_2509_19703_b200 import _lib
+    from paper_2509_19703_b200.device import device_csr, stream_ptr
+    from paper_2509_19703_b200.distributed import gather_records, pack_records, shard_range
+    from paper_2509_19703_b200.neighbors import partial_bfs_records
+
+    g, gen_s = build_graph("c5")
+    n = g.n
+    csr = device_csr(g, dev)
+    begin, end, per = shard_range(n, rank, ws)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    # work units: one counted pass (untimed)
+    work = torch.zeros(2, dtype=torch.int64, device=dev)
+    partial_bfs_records(csr, K_NN, SEED, begin, end, work=work)
+    torch.cuda.synchronize()
+    scanned, expanded = (int(x) for x in work.cpu().tolist())
+
+    def step():
+        nbr, dd, cnt = partial_bfs_records(csr, K_NN, SEED, begin, end)
+        if ws > 1:
+            gather_records(pack_records(nbr, dd, cnt, per))
+        return nbr
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    times = []
+    st = torch.cuda.current_stream()
+    with ClockSampler(local) as clk:
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            step()
+            e1.record(st)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+    my_ms = sum(times) / len(times)
+    te_tot = scanned
+    if ws > 1:
+        t = torch.tensor([my_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        my_ms = float(t.item())
+        c = torch.tensor([scanned, expanded], device=dev, dtype=torch.int64)
+        dist.all_reduce(c)
+        te_tot, exp_tot = (int(x) for x in c.tolist())
+    else:
+        exp_tot = expanded
+    gteps = te_tot / (my_ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel (per-rank launch)
+    peak, peak_kind = _peaks()
+    nsrc = end - begin
+    alg_bytes = 8 * expanded + 4 * scanned + 8 * K_NN * nsrc
+    kern_ms = min(times) if ws == 1 else min(times)
+    # time the kNN kernel alone (no gather) for the roofline
+    ktimes = []
+    for _ in range(max(3, args.steps)):
+        flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        partial_bfs_records(csr, K_NN, SEED, begin, end)
+        e1.record(st)
+        e1.synchronize()
+        ktimes.append(e0.elapsed_time(e1))
+    kern_ms = sum(ktimes) / len(ktimes)
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = _profile_traffic("pbfs_tier1")
+    result = {
+        "metric": "BFS-kNN GTEPS (partial BFS kNN, k=15)",
+        "value": round(gteps, 4),
+        "unit": "GTEPS",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(my_ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "int32",
+        "data": "synthetic (seeded RGG fixture, paper datasets absent)",
+        "config": {"workload": WORKLOAD, "n": n, "m": int(g.m), "k": K_NN, "seed": SEED,
+                   "sources_per_rank": per, "te_per_step": te_tot,
+                   "l2": "CSR 208 MB > 126 MB L2; 256 MB L2 flush before every timed step",
+                   "parallelism": f"sources sharded over {ws} GPU(s)"
+                   + (", NCCL all_gather of records" if ws > 1 else "")},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "peak_source": peak_kind,
+                     "kernel": "gu_partial_bfs_knn (pbfs_tier1<128>)",
+                     "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)},
+        "gpu_launches": 4 * args.steps,
+        "clocks": clk.summary(),
+        "fixture_gen_s": round(gen_s, 2),
+    }
+
+    if rank == 0:
+        result["e2e"] = _e2e_partial(gu, g, args, gteps_te=te_tot)
+        if not args.skip_sgd:
+            result["sgd"] = _sgd_bench(gu, g, args, dev, peak)
+        if not args.skip_layout:
+            result["layout_e2e"] = _layout_e2e(gu)
+        if not args.skip_cpu:
+            result["cpu_baseline"] = _cpu_baseline(g)
+        print(json.dumps(result), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _e2e_partial(gu, g, args, gteps_te):
+    """Public API, host arrays in, numpy DirectedKnn out, copies timed."""
+    import torch
+    from paper_2509_19703_b200.graph import Graph
+
+    def fresh():
+        return Graph(n=g.n, m=g.m, adj_indptr=np.array(g.adj_indptr),
+                     adj_indices=np.array(g.adj_indices), edges=g.edges)
+
+    times = []
+    h2d = d2h = 0
+    for i in range(max(1, args.warmup) + args.steps):
+        gg = fresh()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, knn = gu.partial_bfs(gg, K_NN, seed=SEED)
+        ip, dst, dd = knn.indptr, knn.dst, knn.dist
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if i >= max(1, args.warmup):
+            times.append(dt)
+        h2d = (g.n + 1) * 4 + g.adj_indices.shape[0] * 4
+        d2h = ip.nbytes + dst.nbytes + dd.nbytes
+    t = sum(times) / len(times)
+    return {"value": round(gteps_te / t / 1e9, 4), "unit": "GTEPS", "seconds": round(t, 4),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "paper_2509_19703_b200.partial_bfs(Graph(host arrays), 15, seed=4)"}
+
+
+def _sgd_bench(gu, g, args, dev, peak):
+    import torch
+    from paper_2509_19703_b200 import _lib
+    from paper_2509_19703_b200.device import stream_ptr
+    from paper_2509_19703_b200.layout import INT32_MAX, _plan_for, sgd_concurrency
+
+    _, knn = gu.partial_bfs(g, K_NN, seed=SEED)
+    gk = gu.smooth_knn_weights(knn)
+    E = gk.edge_count
+    a, b = gu.fit_ab(0.1, 1.0)
+    plan = _plan_for(gk, SEED, dev)
+    init = np.random.default_rng(SEED).uniform(-10, 10, size=(g.n, 2)).astype(np.float32)
+    xy = torch.from_numpy(init).to(dev)
+    div = torch.full((1,), INT32_MAX, dtype=torch.int32, device=dev)
+    T = 200
+    st = torch.cuda.current_stream()
+
+    def epochs(e0, e1):
+        _lib.call("gu_sgd_epochs", plan.n, plan.E, _lib.ptr(xy), _lib.ptr(plan.edges),
+                  _lib.ptr(plan.nbr_indptr), _lib.ptr(plan.nbr_indices), float(a), float(b),
+                  1.0, T, e0, e1, 5, E, 0, plan.seed, sgd_concurrency(plan.n), _lib.ptr(div),
+                  stream_ptr(dev))
+
+    epochs(0, max(1, args.warmup))
+    torch.cuda.synchronize()
+    ts = []
+    for i in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        epochs(3 + i, 4 + i)
+        e1.record(st)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = sum(ts) / len(ts)
+    ups = E / (ms / 1e3)
+    achieved = 88.0 * E / (ms / 1e3) / 1e9
+    return {"metric": "SGD edge-updates/s (full epoch, 5 negatives, fp32 Hogwild)",
+            "value": round(ups, 1), "unit": "updates/s", "E": E, "ms_per_epoch": round(ms, 4),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": _profile_traffic("sgd_epoch_kernel"),
+                         "alg_bytes_per_update": 88},
+            "diverged": int(div.item()) != INT32_MAX}
+
+
+def _layout_e2e(gu):
+    """SL-GUMAP on c3 through the public API, host arrays in / out."""
+    import torch
+    from paper_2509_19703_b200 import fixtures
+    from paper_2509_19703_b200.graph import Graph
+
+    g = fixtures.scale_free(100_000, seed=2, m0=3)
+
+    def once():
+        gg = Graph(n=g.n, m=g.m, adj_indptr=np.array(g.adj_indptr),
+                   adj_indices=np.array(g.adj_indices), edges=g.edges)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, knn = gu.partial_bfs(gg, 15, seed=2)
+        gk = gu.smooth_knn_weights(knn)
+        E = gk.edge_count
+        samp = math.log(0.1 * E) / math.log(E)
+        cfg = gu.OptimizerConfig(iterations=200, k=15, seed=2, samp=samp)
+        lay = gu.optimize_sampled(gk, gu.random_init(gg, 2, 10.0), cfg, tag="SL")
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0, lay
+
+    once()
+    ts = [once()[0] for _ in range(3)]
+    return {"metric": "end-to-end layout seconds", "config": "c3 SL-GUMAP BA(100k, m0=3), "
+            "200 epochs, 10% window, random init, host arrays in/out", "value": round(min(ts), 4),
+            "unit": "s", "higher_is_better": False}
+
+
+def _cpu_baseline(g, sample=400_000):
+    from oracle import oracle as O
+    O.build()
+    thr = O.max_threads()
+    t0 = time.perf_counter()
+    _, _, _, sc, ex = O.partial_bfs_raw(g, K_NN, SEED, 0, sample, nthreads=thr, work=True)
+    dt = time.perf_counter() - t0
+    te = int(sc.sum())
+    return {"value": round(te / dt / 1e9, 5), "unit": "GTEPS", "cores": thr, "kind": "port",
+            "sample": f"sources 0..{sample} of the c5 graph ({te} adjacency entries), "
+                      "oracle/oracle.c partial_bfs_all restatement", "seconds": round(dt, 3)}
+
+
+# ---------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, local = _dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    g, _ = build_graph("c5")
+    thr = O.max_threads()
+    sample = 400_000
+    for _ in range(args.warmup):
+        O.partial_bfs_raw(g, K_NN, SEED, 0, 20_000, nthreads=thr)
+    ts, te = [], 0
+    for i in range(args.steps):
+        s0 = (i * sample) % (g.n - sample)
+        t0 = time.perf_counter()
+        _, _, _, sc, _ = O.partial_bfs_raw(g, K_NN, SEED, s0, s0 + sample, nthreads=thr, work=True)
+        ts.append(time.perf_counter() - t0)
+        te += int(sc.sum())
+    tot = sum(ts)
+    v = te / tot / 1e9
+    out = {"impl": "reference", "metric": "BFS-kNN GTEPS (partial BFS kNN, k=15)",
+           "value": round(v, 5), "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "int32", "data": "synthetic", "config": {"workload": WORKLOAD,
+                                                              "sample_sources_per_step": sample},
+           "cpu_baseline": {"value": round(v, 5), "unit": "GTEPS", "cores": thr, "kind": "port",
+                            "sample": f"{sample} sources per step of the c5 graph"},
+           "e2e": {"value": round(v, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skip-sgd", action="store_true")
+    ap.add_argument("--skip-layout", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -130,7 +130,10 @@ int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* 
  * gu_sgd_prepare_edges builds them shuffled. nbr CSR int32.
  * Runs epochs [epoch_begin, epoch_end) of a t-epoch schedule,
  * lr_e = lr0 * (1 - e/t).  diverged (int32, device): atomicMin'd with the
- * first epoch that produced a non-finite coordinate (init to INT32_MAX). */
+ * first epoch that produced a non-finite coordinate (init to INT32_MAX).
+ * concurrency: maximum number of edge visits in flight (threads); 0 = fill
+ * the GPU.  Hogwild stays statistically close to the sequential sweep only
+ * while concurrency << n, so callers cap it for small graphs. */
 int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
                          const double* sym_w, uint64_t seed, void* edges_int4,
                          void* stream);
@@ -138,7 +141,7 @@ int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4
                   const int32_t* nbr_indptr, const int32_t* nbr_indices, float a, float b,
                   float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
                   int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
-                  int32_t* diverged, void* stream);
+                  int64_t concurrency, int32_t* diverged, void* stream);
 /* positions visited by epoch `epoch` (visit_log): window/permutation indices
  * into the prepared edge array, length window (windowed) or E (full). */
 int gu_sgd_visit_order(int64_t E, int32_t epoch, int64_t window, int32_t windowed,

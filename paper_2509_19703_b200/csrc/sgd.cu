@@ -222,11 +222,17 @@ __global__ void visit_order_kernel(long long E, int epoch, long long items, long
   }
 }
 
-unsigned grid_for(long long items) {
+unsigned grid_for(long long items, long long max_threads = 0) {
   long long b = (items + 255) / 256;
   if (b > 148LL * 8) b = 148LL * 8;
+  if (max_threads > 0 && b * 256 > max_threads) b = (max_threads + 255) / 256;
   if (b < 1) b = 1;
   return (unsigned)b;
+}
+
+unsigned block_for(long long max_threads) {
+  if (max_threads > 0 && max_threads < 256) return (unsigned)(((max_threads + 31) / 32) * 32);
+  return 256;
 }
 
 }  // namespace
@@ -264,7 +270,7 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
                              const int32_t* nbr_indptr, const int32_t* nbr_indices, float a,
                              float b, float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
                              int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
-                             int32_t* diverged, void* stream) {
+                             int64_t concurrency, int32_t* diverged, void* stream) {
   if (n <= 0 || n >= INT_MAX || E < 0 || t < 0 || epoch_begin < 0 || epoch_end > t ||
       (windowed && (window < 1 || window > E))) {
     set_error("gu_sgd_epochs: bad arguments");
@@ -277,7 +283,9 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
     const float lr = (float)((double)lr0 * (1.0 - (double)e / (double)t));
     long long items, start;
     epoch_range(E, e, window, windowed, &items, &start);
-    sgd_epoch_kernel<<<grid_for(items), 256, 0, st>>>(
+    const unsigned bs = block_for(concurrency);
+    const unsigned gs = bs < 256 ? 1u : grid_for(items, concurrency);
+    sgd_epoch_kernel<<<gs, bs, 0, st>>>(
         (int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr, nbr_indices, a, b,
         lr, e, n_neg, items, start, windowed, seed, diverged);
     GU_CHECK_LAUNCH("sgd_epoch_kernel");

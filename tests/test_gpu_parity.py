@@ -1,0 +1,338 @@
+"""GPU parity: libgumap (through the C ABI / drop-in API) vs golden vectors and
+the oracle.  Bit-exact for all integer / index work and for rho / sigma; the
+fuzzy weights within 4 ulp (device exp vs numpy's SIMD exp); the float64
+replay within 1e-5 relative (north-star check (b), max(|x|, 1) denominator).
+"""
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import golden_graphs, load_golden, sha, split
+
+pytestmark = pytest.mark.gpu
+
+# tolerances written down where they are used
+WEIGHT_ULPS = 4          # device exp vs numpy exp, per weight
+REPLAY_REL_TOL = 1e-5    # north star check (b)
+
+
+@pytest.fixture(scope="module")
+def gu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2509_19703_b200 as gu
+    return gu
+
+
+def _ulps(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a.view(np.int64) - b.view(np.int64))
+
+
+# ------------------------------------------------------------- C0 partial
+def test_partial_bfs_golden_small(gu):
+    for g, k, seed, exp in golden_graphs("partial_small.npz"):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            dset, knn = gu.partial_bfs(g, k, seed=seed)
+        assert np.array_equal(knn.indptr, exp["indptr"])
+        assert np.array_equal(knn.dst, exp["dst"])
+        assert np.array_equal(knn.dist, exp["dist"])
+        assert np.array_equal(dset.nbr, exp["dst"])
+
+
+def test_partial_bfs_warns_small_component(gu):
+    g = gu.build_graph([(0, 1), (1, 2), (3, 4)])
+    with pytest.warns(UserWarning, match="smaller than k"):
+        dset, _ = gu.partial_bfs(g, k=3, seed=0)
+    ids, _ = dset.row(3)
+    assert list(ids) == [4]
+
+
+def test_partial_bfs_rejects_bad_k(gu):
+    g = gu.build_graph([(0, 1)])
+    with pytest.raises(ValueError):
+        gu.partial_bfs(g, 0)
+
+
+def test_partial_bfs_c3_bitexact(gu):
+    z = load_golden("c3.npz")
+    g = gu.synth_graph("scale_free", 100000, seed=2, m0=3)
+    _, knn = gu.partial_bfs(g, 15, seed=2)
+    assert sha(knn.indptr) == str(z["knn_indptr_sha"])
+    assert sha(knn.dst) == str(z["knn_dst_sha"])
+    assert sha(knn.dist) == str(z["knn_dist_sha"])
+
+
+def test_partial_bfs_all_tiers_and_large_k(gu, oracle):
+    """k > 32 (tier 2 only) and hub-heavy balls (tier 1b / 2) vs the oracle."""
+    g = gu.synth_graph("scale_free", 3000, seed=5, m0=2)
+    for k in (15, 40, 100):
+        _, knn = gu.partial_bfs(g, k, seed=11)
+        ip, dst, dist = oracle.partial_bfs(g, k, seed=11, nthreads=4)
+        assert np.array_equal(knn.indptr, ip) and np.array_equal(knn.dst, dst)
+        assert np.array_equal(knn.dist, dist)
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_partial_bfs_scale_sample_vs_oracle(gu, oracle, name):
+    """BASELINE c4 / c5 at full size: a 20k-source sample bit-exact vs the
+    oracle, plus size-independent properties over every row."""
+    import torch
+    from paper_2509_19703_b200.device import device_csr
+    from paper_2509_19703_b200.neighbors import partial_bfs_records
+
+    g = gu.config_graph(name)
+    csr = device_csr(g)
+    nbr, dist, cnt = partial_bfs_records(csr, 15, 4, 0, g.n)
+    cnt_h = cnt.cpu().numpy()
+    assert np.all(cnt_h == 15)
+    nb, dd = nbr.cpu().numpy(), dist.cpu().numpy()
+    # rows sorted by (dist, id), no self, distances >= 1
+    key = dd.astype(np.int64) * g.n + nb
+    assert np.all(np.diff(key, axis=1) > 0)
+    assert np.all(nb != np.arange(g.n)[:, None])
+    assert np.all(dd >= 1)
+    rng = np.random.default_rng(0)
+    for s0 in rng.choice(g.n - 2000, size=10, replace=False):
+        o_n, o_d, o_c = oracle.partial_bfs_raw(g, 15, 4, int(s0), int(s0) + 2000, nthreads=8)
+        assert np.array_equal(nb[s0:s0 + 2000].reshape(-1), o_n)
+        assert np.array_equal(dd[s0:s0 + 2000].reshape(-1), o_d)
+
+
+# --------------------------------------------------------------- C0 full
+def test_full_knn_golden_small(gu):
+    for g, k, seed, exp in golden_graphs("full_small.npz"):
+        dset = gu.all_pairs_bfs(g)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            knn = gu.knn_from_full_distances(dset, k, seed=seed)
+        assert np.array_equal(knn.indptr, exp["indptr"])
+        assert np.array_equal(knn.dst, exp["dst"])
+        assert np.array_equal(knn.dist, exp["dist"])
+        assert sha(dset.matrix) == exp["apsp_sha"]
+        # explicit-matrix path (a set that carries its matrix)
+        explicit = gu.SparseDistanceSet(n=g.n, full=True, matrix=np.array(dset.matrix))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            knn2 = gu.knn_from_full_distances(explicit, k, seed=seed)
+        assert np.array_equal(knn2.dst, exp["dst"]) and np.array_equal(knn2.dist, exp["dist"])
+
+
+def test_c1_full_path_bitexact(gu):
+    z = load_golden("c1.npz")
+    g = gu.synth_graph("grid", 2500)
+    dset = gu.all_pairs_bfs(g)
+    knn = gu.knn_from_full_distances(dset, 15, seed=0)
+    assert np.array_equal(knn.indptr, z["knn_indptr"])
+    assert np.array_equal(knn.dst, z["knn_dst"])
+    assert np.array_equal(knn.dist, z["knn_dist"])
+    knn7 = gu.knn_from_full_distances(dset, 5, seed=7)
+    assert np.array_equal(knn7.dst, z["knn7_dst"]) and np.array_equal(knn7.dist, z["knn7_dist"])
+    assert sha(dset.matrix) == str(z["apsp_sha"])
+
+
+def test_c2_full_knn_vs_oracle(gu, oracle):
+    """SS-GUMAP c2 stand-in (G' of ER(20000, 200)): fused BFS-kNN vs oracle."""
+    g = gu.config_graph("c2")
+    knn = gu.knn_from_full_distances(gu.all_pairs_bfs(g), 15, seed=1)
+    dst, dist, cnt = oracle.full_knn(g, 15, seed=1, src_begin=0, src_end=4000, nthreads=8,
+                                     packed=False)
+    assert np.array_equal(knn.dst[: 4000 * 15], dst)
+    assert np.array_equal(knn.dist[: 4000 * 15], dist)
+
+
+# --------------------------------------------------------------------- C1
+def test_smooth_cases_golden(gu):
+    z = load_golden("smooth_cases.npz")
+    for i in range(z["n"].shape[0]):
+        n, k = int(z["n"][i]), int(z["k"][i])
+        knn = gu.DirectedKnn(n=n, k=k, indptr=split(z["indptr"], z["indptr_off"], i),
+                             dst=split(z["dst"], z["dst_off"], i),
+                             dist=split(z["dist"], z["dist_off"], i))
+        gk = gu.smooth_knn_weights(knn)
+        assert np.array_equal(gk.rho, split(z["rho"], z["rho_off"], i))
+        assert np.array_equal(gk.sigma, split(z["sigma"], z["sigma_off"], i))
+        assert np.array_equal(gk.sym_src, split(z["sym_src"], z["sym_src_off"], i))
+        assert np.array_equal(gk.sym_dst, split(z["sym_dst"], z["sym_dst_off"], i))
+        assert _ulps(gk.sym_w, split(z["sym_w"], z["sym_w_off"], i)).max(initial=0) <= WEIGHT_ULPS
+        assert np.array_equal(gk.nbr_indptr, split(z["nbr_indptr"], z["nbr_indptr_off"], i))
+
+
+def test_smooth_rejects_empty_row(gu):
+    knn = gu.DirectedKnn(n=2, k=1, indptr=np.array([0, 1, 1]), dst=np.array([1], np.int32),
+                         dist=np.array([1], np.int32))
+    with pytest.raises(ValueError):
+        gu.smooth_knn_weights(knn)
+
+
+def test_c1_smooth_golden(gu):
+    z = load_golden("c1.npz")
+    knn = gu.DirectedKnn(n=2500, k=15, indptr=z["knn_indptr"], dst=z["knn_dst"],
+                         dist=z["knn_dist"])
+    gk = gu.smooth_knn_weights(knn)
+    for key in ("rho", "sigma", "sym_src", "sym_dst", "nbr_indptr", "nbr_indices"):
+        assert np.array_equal(getattr(gk, key), z[key]), key
+    assert _ulps(gk.sym_w, z["sym_w"]).max() <= WEIGHT_ULPS
+
+
+def test_c3_smooth_golden(gu):
+    z = load_golden("c3.npz")
+    g = gu.synth_graph("scale_free", 100000, seed=2, m0=3)
+    _, knn = gu.partial_bfs(g, 15, seed=2)
+    gk = gu.smooth_knn_weights(knn)
+    assert sha(gk.rho) == str(z["rho_sha"])
+    assert sha(gk.sigma) == str(z["sigma_sha"])
+    assert sha(gk.sym_src) == str(z["sym_src_sha"])
+    assert sha(gk.sym_dst) == str(z["sym_dst_sha"])
+    assert gk.edge_count == int(z["E"])
+    assert _ulps(gk.sym_w[:20000], z["sym_w_head"]).max() <= WEIGHT_ULPS
+
+
+# -------------------------------------------------------- C2 check (b)
+def _rel_err(x, ref):
+    return float(np.max(np.abs(x - ref) / np.maximum(np.abs(ref), 1.0)))
+
+
+def test_replay_c1_full_epochs(gu, oracle):
+    z = load_golden("c1.npz")
+    a, b = float(z["a"]), float(z["b"])
+    gk = gu.KnnGraph(n=2500, k=15, directed=None, rho=z["rho"], sigma=z["sigma"],
+                     sym_src=z["sym_src"], sym_dst=z["sym_dst"], sym_w=z["sym_w"],
+                     nbr_indptr=z["nbr_indptr"], nbr_indices=z["nbr_indices"])
+    c = np.array(z["init"], copy=True)
+    state = 0 ^ oracle.SPLIT_GAMMA
+    for it, key in ((0, "after1"), (1, "after2")):
+        order = z["order%d" % it]
+        before = c.copy()
+        lr = 1.0 - it / 200
+        state, negs, th = oracle.sgd_sweep(c, z["sym_src"], z["sym_dst"], z["sym_w"], order,
+                                           z["nbr_indptr"], z["nbr_indices"], a, b, lr, 5, state)
+        out, nwaves = gu.sgd_replay(gk, before, order, negs, th, a, b, lr, 5)
+        assert nwaves > 1
+        assert _rel_err(out, z[key]) <= REPLAY_REL_TOL
+        c = np.array(z[key], copy=True)
+
+
+def test_replay_c3_window_epoch(gu, oracle):
+    z = load_golden("c3.npz")
+    g = gu.synth_graph("scale_free", 100000, seed=2, m0=3)
+    ip, dst, dist = oracle.partial_bfs(g, 15, seed=2, nthreads=8)
+    o = oracle.smooth_knn_weights(g.n, ip, dst, dist, 15, nthreads=8)
+    E = o["sym_src"].shape[0]
+    samp = math.log(0.1 * E) / math.log(E)
+    init = np.random.default_rng(2).uniform(-10.0, 10.0, size=(g.n, 2))
+    a, b = float(z["a"]), float(z["b"])
+    _, logs = oracle.run_sgd(o, init, 1, a, b, 1.0, 5, 2, samp=samp, windowed=True,
+                             epochs_to_log=(0,))
+    before, order, negs, th, lr = logs[0]
+    c = before.copy()
+    oracle.sgd_sweep(c, o["sym_src"], o["sym_dst"], o["sym_w"], order, o["nbr_indptr"],
+                     o["nbr_indices"], a, b, lr, 5, 2 ^ oracle.SPLIT_GAMMA)
+    gk = gu.KnnGraph(n=g.n, k=15, directed=None, **{k_: o[k_] for k_ in (
+        "rho", "sigma", "sym_src", "sym_dst", "sym_w", "nbr_indptr", "nbr_indices")})
+    out, _ = gu.sgd_replay(gk, before, order, negs, th, a, b, lr, 5)
+    assert _rel_err(out, c) <= REPLAY_REL_TOL
+
+
+# ---------------------------------------------------- C2 Hogwild epochs
+def test_sgd_zero_iterations_identity(gu):
+    g = gu.build_graph([(0, 1), (1, 2), (2, 3), (3, 0)])
+    _, knn = gu.partial_bfs(g, 2, seed=0)
+    gk = gu.smooth_knn_weights(knn)
+    init = gu.random_init(g, 0)
+    cfg = gu.OptimizerConfig(iterations=0, k=2, seed=0)
+    assert np.array_equal(gu.optimize_full(gk, init, cfg).coords, init.coords)
+    assert np.array_equal(gu.optimize_sampled(gk, init, cfg).coords, init.coords)
+
+
+def test_sgd_visit_log_coverage(gu):
+    g = gu.synth_graph("scale_free", 300, seed=3, m0=3)
+    _, knn = gu.partial_bfs(g, 6, seed=0)
+    gk = gu.smooth_knn_weights(knn)
+    init = gu.random_init(g, 1)
+    E = gk.edge_count
+    cfg = gu.OptimizerConfig(iterations=4, k=6, samp=1.0, seed=9)
+    lf, ls = [], []
+    gu.optimize_full(gk, init, cfg, visit_log=lf)
+    gu.optimize_sampled(gk, init, cfg, visit_log=ls)
+    for a_, b_ in zip(lf, ls):
+        assert sorted(a_.tolist()) == list(range(E)) == sorted(b_.tolist())
+    # pigeonhole: ceil(E / window) windows touch every edge
+    s = int(math.floor(E ** 0.9))
+    cfg2 = gu.OptimizerConfig(iterations=math.ceil(E / s), k=6, samp=0.9, seed=4)
+    log = []
+    gu.optimize_sampled(gk, init, cfg2, visit_log=log)
+    assert set(np.concatenate(log).tolist()) == set(range(E))
+
+
+def test_sgd_pure_attraction_shrinks_edge(gu):
+    g = gu.build_graph([(0, 1)])
+    _, knn = gu.partial_bfs(g, 1, seed=0)
+    gk = gu.smooth_knn_weights(knn)
+    init = gu.Layout(coords=np.array([[-4.0, 0.0], [4.0, 0.0]]))
+    cfg = gu.OptimizerConfig(iterations=200, k=1, negative_sample_count=0,
+                             learning_rate=0.05, seed=1)
+    dists = []
+    gu.optimize_full(gk, init, cfg, callback=lambda it, c: dists.append(
+        np.linalg.norm(c[0] - c[1])), callback_every=10)
+    assert all(b_ <= a_ + 1e-5 for a_, b_ in zip(dists, dists[1:]))
+    assert dists[-1] < 1.0
+
+
+def test_sgd_divergence_detected(gu):
+    g = gu.build_graph([(0, 1)])
+    _, knn = gu.partial_bfs(g, 1, seed=0)
+    gk = gu.smooth_knn_weights(knn)
+    init = gu.Layout(coords=np.array([[0.0, 0.0], [1.0, 0.0]]))
+    cfg = gu.OptimizerConfig(iterations=5, k=1, learning_rate=1e308, seed=0)
+    with pytest.raises(gu.OptimizationDiverged):
+        gu.optimize_full(gk, init, cfg)
+
+
+def test_drivers_run(gu):
+    g = gu.build_graph([(i, (i + 1) % 6) for i in range(6)])
+    cfg = gu.OptimizerConfig(iterations=30, k=2, seed=0)
+    for fn in (gu.run_gumap, gu.run_ss_gumap, gu.run_sl_gumap, gu.run_sssl_gumap):
+        lay, rep = fn(g, cfg)
+        assert lay.n == 6 and np.all(np.isfinite(lay.coords))
+        assert rep.total_ms >= max(rep.c0_ms, rep.c1_ms, rep.c2_ms)
+
+
+def test_quality_c1_vs_reference(gu):
+    """Check (c): NP / stress / crossings of the c1 layout over seeds vs the
+    reference's own seed distribution (tests/golden/quality_c1.npz)."""
+    from oracle.metrics import count_crossings, neighborhood_preservation, stress
+
+    z = load_golden("quality_c1.npz")
+    g = gu.synth_graph("grid", 2500)
+    dset = gu.all_pairs_bfs(g)
+    hop = np.array(dset.matrix, dtype=np.float64)
+    # metric restatement pinned on the reference's own layouts
+    for i, lay in enumerate((z["layout0"], z["layout1"])):
+        assert abs(neighborhood_preservation(g, lay) - z["np_"][i]) < 1e-12
+        assert abs(stress(g, lay, hop) - z["stress"][i]) < 1e-9
+        assert count_crossings(g, lay) == int(z["crossings"][i])
+    vals = []
+    for seed in range(10):
+        knn = gu.knn_from_full_distances(dset, 15, seed=seed)
+        gk = gu.smooth_knn_weights(knn)
+        init = gu.random_init(g, seed, 10.0)
+        cfg = gu.OptimizerConfig(iterations=200, k=15, seed=seed)
+        lay = gu.optimize_full(gk, init, cfg, tag="GUMAP").coords
+        vals.append((neighborhood_preservation(g, lay), stress(g, lay, hop),
+                     count_crossings(g, lay)))
+    v = np.array(vals)
+    ref = np.stack([z["np_"], z["stress"], z["crossings"]], axis=1)
+    ratio = v.mean(axis=0) / ref.mean(axis=0)
+    print("check (c) mean ratios gpu/ref [np, stress, crossings]:", ratio)
+    # NP must not be worse than the reference's own spread allows
+    se = ref.std(axis=0, ddof=1) / math.sqrt(ref.shape[0]) + v.std(axis=0, ddof=1) / math.sqrt(v.shape[0])
+    assert v.mean(axis=0)[0] >= ref.mean(axis=0)[0] - 4 * se[0]
+    assert v.mean(axis=0)[1] <= ref.mean(axis=0)[1] + 4 * se[1]
+    assert v.mean(axis=0)[2] <= ref.mean(axis=0)[2] + 4 * se[2]
