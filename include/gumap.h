@@ -53,8 +53,9 @@ int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_t* indices,
                        int32_t* out_nbr, int32_t* out_dist, int32_t* out_count,
                        uint64_t* work_counters, void* workspace, size_t ws_bytes,
                        int32_t tier2_warps, void* stream);
-/* synchronous: how many sources fell to tier 1b / tier 2 in the last call */
-int gu_partial_bfs_overflow_counts(void* workspace, int64_t nsrc, int32_t* host_out2);
+/* synchronous: sources that fell from tier 0 (thread per source) to tier 1a,
+ * to tier 1b and to tier 2 in the last call on this workspace (3 ints) */
+int gu_partial_bfs_overflow_counts(void* workspace, int64_t nsrc, int32_t* host_out3);
 
 /* ----------------------------------------------- C0 full BFS (bitset)
  * Replaces _kernels.py:33-57 apsp_rows via neighbors.py:120 all_pairs_bfs:

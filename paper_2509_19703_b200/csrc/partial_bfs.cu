@@ -8,12 +8,12 @@
 //
 // The Fisher-Yates indexes the crossing level in the reference's FIFO
 // *discovery order*.  A level-synchronous warp reproduces it without a queue:
-// level L+1 in discovery order == its vertices sorted by (min rank of a parent
-// in level L, vertex id).  Each warp expands a whole level
-// at once (flattened adjacency of the frontier, 32 entries per step), inserts
-// the neighbours into a shared-memory hash keyed by vertex id whose value is
-// atomicMin((level << 20) | parent_rank), then sorts the new level by
-// (rank, id) with a warp bitonic sort.
+// level L+1 in discovery order == the frontier's adjacency lists concatenated
+// in queue order, each vertex kept at its first occurrence (equivalently: its
+// vertices sorted by (min rank of a parent in level L, vertex id), SURVEY.md
+// 8(a) A5).  Each warp expands a whole level at once (flattened adjacency of
+// the frontier, 32 entries per step) against a shared-memory hash of the
+// vertices already discovered, compacting first occurrences in order.
 //
 // Tiers (no host sync between them; counts live in device memory):
 //   tier 1a  shared hash, CAP=128 discovered vertices per source, 8 warps/CTA
@@ -22,6 +22,8 @@
 //            sequentially in queue order (any level size, any k)
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "gumap.h"
@@ -33,53 +35,43 @@ constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ unsigned hash_id(int w) { return (unsigned)w * 0x9E3779B1u; }
 
-// warp bitonic sort of P (power of two, >= 32) 64-bit keys in shared memory
-__device__ __forceinline__ void warp_bitonic_sort(long long* key, int P) {
-  const int lane = lane_id();
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = lane; t < (P >> 1); t += 32) {
-        int i = 2 * t - (t & (stride - 1));
-        int j = i + stride;
-        bool up = (i & size) == 0;
-        long long a = key[i], b = key[j];
-        if ((a > b) == up) {
-          key[i] = b;
-          key[j] = a;
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
-
-// Sort `count` (<= 32) entries held one per lane by (dist, id) and store.
-__device__ __forceinline__ void store_sorted_row(int count, int my_v, int my_d,
-                                                 int* out_nbr, int* out_dist) {
-  const int lane = lane_id();
-  int pos = 0;
-  for (int j = 0; j < count; j++) {
-    int vj = __shfl_sync(FULL, my_v, j);
-    int dj = __shfl_sync(FULL, my_d, j);
-    if (dj < my_d || (dj == my_d && vj < my_v)) pos++;
-  }
-  if (lane < count) {
-    out_nbr[pos] = my_v;
-    out_dist[pos] = my_d;
-  }
-}
-
-template <int CAP>
+// Tier-1 geometry: G lanes per source (32 / G sources per warp), at most CAP
+// vertices discovered (hash of 2*CAP slots), PCAP frontier parents and TCAP
+// flattened frontier adjacency entries per level.
+template <int G, int CAP, int PCAP, int TCAP>
 struct Tier1 {
   static constexpr int HC = 2 * CAP;
-  // per-warp shared layout (ints): disc[CAP] stage[CAP] key64[CAP](=2*CAP ints)
-  //                                hkey[HC] hval[HC]
-  // pre/beg of the frontier alias the key64 region (used before the sort).
-  static constexpr int WORDS = CAP + CAP + 2 * CAP + 2 * HC + 4;
-  static constexpr size_t BYTES = WORDS * sizeof(int);
+  static constexpr int TW = TCAP / 32;
+  // per-group shared layout (ints): hkey[HC] disc[CAP] ppre[PCAP] pbeg[PCAP] bmap[TW]
+  static constexpr int WORDS = HC + CAP + 2 * PCAP + TW;
+  static constexpr int NG = 32 / G;
+  static_assert(HC % 4 == 0 && (WORDS % 4) == 0, "int4 alignment");
 };
 
-template <int CAP, int WARPS>
+// (i+1)-th output of the splitmix64 stream whose state starts at `base`
+// (_kernels.py:18-25): draws are independent of each other, so the lanes of a
+// group compute the crossing level's Fisher-Yates indices in parallel.
+__device__ __forceinline__ unsigned long long splitmix_at(unsigned long long base, int i) {
+  unsigned long long z = base + SPLIT_GAMMA * (unsigned long long)(i + 1);
+  z = (z ^ (z >> 30)) * SPLIT_MUL1;
+  z = (z ^ (z >> 27)) * SPLIT_MUL2;
+  return z ^ (z >> 31);
+}
+
+// Discovery order without sorting: the reference appends a vertex the first
+// time it is met while scanning the frontier in queue order, each parent's
+// sorted adjacency in turn.  Concatenating the frontier's adjacency lists in
+// that order (the "flattened" index t) and keeping each vertex at its first
+// occurrence t -- and only if no earlier level holds it -- therefore yields
+// the next level in exactly the reference's order.  A group of G lanes walks
+// t in chunks of G: the parent of t is found from a per-level bitmap of
+// adjacency-start positions (popc), __match_any_sync elects the lowest lane of
+// equal ids inside a chunk, and that lane's atomicCAS into the per-source hash
+// succeeds iff the id was never seen in an earlier chunk or level.
+// ballot/popc compacts the winners in t order.  All warp-collective calls use
+// the full mask with loops bounded by the warp-wide maximum, so the 32/G
+// sources of a warp advance in lockstep.
+template <int G, int CAP, int PCAP, int TCAP, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     pbfs_tier1(const int* __restrict__ indptr, const int* __restrict__ indices,
                int K, unsigned long long seed, long long src_begin, long long nsrc,
@@ -87,82 +79,114 @@ __global__ void __launch_bounds__(WARPS * 32)
                int* __restrict__ out_nbr, int* __restrict__ out_dist,
                int* __restrict__ out_cnt, int* __restrict__ ovf_list,
                int* __restrict__ ovf_count, unsigned long long* __restrict__ work) {
-  constexpr int HC = Tier1<CAP>::HC;
+  using L = Tier1<G, CAP, PCAP, TCAP>;
+  constexpr int HC = L::HC, TW = L::TW, NG = L::NG;
+  constexpr unsigned GM = G == 32 ? FULL : ((1u << G) - 1u);
   extern __shared__ __align__(16) int smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int* base = smem + warp * Tier1<CAP>::WORDS;
-  int* disc = base;
-  int* stage = disc + CAP;
-  long long* key64 = reinterpret_cast<long long*>(stage + CAP);  // 2*CAP ints
-  int* pre = reinterpret_cast<int*>(key64);                       // CAP+1 ints
-  int* beg = pre + CAP + 1;                                       // CAP-1 .. ints
-  int* hkey = stage + 3 * CAP;
-  int* hval = hkey + HC;
+  const int gid = lane / G, gl = lane % G, gbase = gid * G;
+  const unsigned lt_g = (1u << gl) - 1u;  // lanes below me inside the group
+  int* hkey = smem + (warp * NG + gid) * L::WORDS;
+  int* disc = hkey + HC;
+  int* ppre = disc + CAP;
+  int* pbeg = ppre + PCAP;
+  unsigned* bmap = reinterpret_cast<unsigned*>(pbeg + PCAP);
 
   unsigned long long w_scanned = 0, w_expanded = 0;
   const long long total = list ? (long long)(*list_count) : nsrc;
-  for (long long item = (long long)blockIdx.x * WARPS + warp; item < total;
-       item += (long long)gridDim.x * WARPS) {
-    const int s = list ? list[item] : (int)(src_begin + item);
-    for (int i = lane; i < HC; i += 32) {
-      hkey[i] = -1;
-      hval[i] = INT_MAX;
+  const long long stride = (long long)gridDim.x * WARPS * NG;
+  for (long long item = ((long long)blockIdx.x * WARPS + warp) * NG + gid;; item += stride) {
+    const bool has = item < total;
+    if (!__any_sync(FULL, has)) break;
+    const int s = has ? (list ? list[item] : (int)(src_begin + item)) : 0;
+    {
+      int4* h4 = reinterpret_cast<int4*>(hkey);
+#pragma unroll
+      for (int i = gl; i < HC / 4; i += G) h4[i] = make_int4(-1, -1, -1, -1);
     }
     __syncwarp();
-    if (lane == 0) {
-      unsigned h = hash_id(s) & (HC - 1);
-      hkey[h] = s;
-      hval[h] = 0;
+    if (has && gl == 0) {
+      hkey[hash_id(s) & (HC - 1)] = s;
       disc[0] = s;
     }
     __syncwarp();
     int lb = 0, le = 1, count = 0, depth = 0;
-    bool ovf = false;
-    int my_v = 0, my_d = 0;
+    bool live = has, ovf = false, l1_sorted = false;
+    int my_v = 0, my_d = 0, my_lvl0 = 0, my_lvln = 0;  // my entry, its level's [start, end)
     unsigned long long scanned = 0, expanded = 0;
-    while (count < K) {
-      const int f = le - lb;
-      // ---- frontier degrees, exclusive prefix (pre), adjacency starts (beg)
-      // beg aliases pre[CAP+1..]; frontier sizes f <= CAP-1 keep them apart.
-      int carry = 0;
-      for (int i0 = 0; i0 < f; i0 += 32) {
-        int i = i0 + lane, d = 0, b = 0;
+    while (__any_sync(FULL, live)) {
+      int f = live ? le - lb : 0;
+      if (f > PCAP) {
+        ovf = true;
+        live = false;
+        f = 0;
+      }
+      // ---- frontier: degrees, prefix, non-empty parents compacted, bitmap
+      for (int w = gl; w < TW; w += G) bmap[w] = 0u;
+      __syncwarp();
+      int carry = 0, nne = 0;
+      for (int i0 = 0; __any_sync(FULL, i0 < f); i0 += G) {
+        const int i = i0 + gl;
+        int d = 0, b = 0;
         if (i < f) {
-          int u = disc[lb + i];
+          const int u = disc[lb + i];
           b = __ldg(indptr + u);
           d = __ldg(indptr + u + 1) - b;
         }
-        int inc = warp_incl_scan(d);
-        if (i < f) {
-          pre[i] = carry + inc - d;
-          beg[i] = b;
+        int inc = d;
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+          const int tt = __shfl_up_sync(FULL, inc, o, G);
+          if (gl >= o) inc += tt;
         }
-        carry += __shfl_sync(FULL, inc, 31);
+        const unsigned ne = (__ballot_sync(FULL, d > 0) >> gbase) & GM;
+        if (d > 0) {
+          const int r = nne + __popc(ne & lt_g);
+          const int p0 = carry + inc - d;
+          ppre[r] = p0;
+          pbeg[r] = b;
+          if (p0 < TCAP) atomicOr(&bmap[p0 >> 5], 1u << (p0 & 31));
+        }
+        carry += __shfl_sync(FULL, inc, G - 1, G);
+        nne += __popc(ne);
+      }
+      const int T = live ? carry : 0;
+      if (T > TCAP) {
+        ovf = true;
+        live = false;
       }
       __syncwarp();
-      const int T = carry;
-      scanned += T;
-      expanded += f;
+      if (live) {
+        scanned += T;
+        expanded += f;
+      }
       depth++;
-      const int tag = depth << 20;
-      // ---- expand: flattened adjacency of the frontier, 32 entries per step
-      int nst = 0;
+      // ---- expansion of the flattened frontier adjacency
+      const int room = CAP - le;
+      int nst = 0, pb = -1;
       bool fail = false;
-      for (int t0 = 0; t0 < T; t0 += 32) {
-        const int t = t0 + lane;
-        bool isnew = false;
+      const int Tl = live ? T : 0;
+      for (int t0 = 0; __any_sync(FULL, t0 < Tl); t0 += G) {
+        const bool act = gl + t0 < Tl;
+        unsigned m = 0u;
+        if (t0 < Tl) {
+          m = bmap[t0 >> 5];
+          if (G < 32) m = (m >> (t0 & 31)) & GM;
+        }
         int w = -1;
-        if (t < T) {
-          int lo = 0, hi = f - 1;  // largest p with pre[p] <= t
-          while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (pre[mid] <= t) lo = mid; else hi = mid - 1;
-          }
-          w = __ldg(indices + beg[lo] + (t - pre[lo]));
+        if (act) {
+          const int p = pb + __popc(m & ((2u << gl) - 1u));
+          w = __ldg(indices + pbeg[p] + (t0 + gl - ppre[p]));
+        }
+        pb += __popc(m);
+        const unsigned long long key = ((unsigned long long)gid << 32) | (unsigned)w;
+        const unsigned grp = __match_any_sync(FULL, key);
+        bool isnew = false;
+        if (act && lane == __ffs(grp) - 1) {
           unsigned h = hash_id(w) & (HC - 1);
           int probe = 0;
           for (; probe < HC; probe++) {
-            int old = atomicCAS(&hkey[h], -1, w);
+            const int old = atomicCAS(&hkey[h], -1, w);
             if (old == -1) {
               isnew = true;
               break;
@@ -171,49 +195,272 @@ __global__ void __launch_bounds__(WARPS * 32)
             h = (h + 1) & (HC - 1);
           }
           if (probe == HC) fail = true;
-          else atomicMin(&hval[h], tag | lo);
         }
-        unsigned bal = __ballot_sync(FULL, isnew);
+        const unsigned bal = (__ballot_sync(FULL, isnew) >> gbase) & GM;
         if (isnew) {
-          int pos = nst + __popc(bal & lanemask_lt());
-          if (pos < CAP) stage[pos] = w;
+          const int pos = nst + __popc(bal & lt_g);
+          if (pos < room) disc[le + pos] = w;
         }
         nst += __popc(bal);
       }
+      if ((__ballot_sync(FULL, fail) >> gbase) & GM) fail = true;
+      if (live && (fail || nst > room - 1)) {
+        ovf = true;
+        live = false;
+      }
+      if (live && nst == 0) live = false;  // component exhausted
       __syncwarp();
-      if (__any_sync(FULL, fail) || le + nst > CAP - 1) {
+      const int remaining = K - count;
+      const bool cross = live && nst > remaining;
+      // ---- crossing level: random subset (_kernels.py:98-105)
+      int j = 0;
+      if (cross && gl < remaining)
+        j = gl + (int)(splitmix_at(seed + SPLIT_GAMMA * (unsigned long long)(s + 1), gl) %
+                       (unsigned long long)(nst - gl));
+      const int rem_c = cross ? remaining : 0;
+      for (int i = 0; __any_sync(FULL, i < rem_c); i++) {
+        const int ji = __shfl_sync(FULL, j, i, G);
+        if (gl == 0 && i < rem_c) {
+          const int a = disc[le + i];
+          disc[le + i] = disc[le + ji];
+          disc[le + ji] = a;
+        }
+      }
+      __syncwarp();
+      if (live) {
+        const int take = cross ? remaining : nst;
+        if (depth == 1 && !cross) l1_sorted = true;  // level 1 == sorted adjacency of s
+        if (gl >= count && gl < count + take) {
+          my_v = disc[le + gl - count];
+          my_d = depth;
+          my_lvl0 = count;
+          my_lvln = count + take;
+        }
+        count += take;
+        lb = le;
+        le += nst;
+        if (count >= K) live = false;
+      }
+    }
+    // ---- output: (dist, id) order; levels are already in dist order, so
+    //      only ids inside a level need ranking (level 1 comes sorted)
+    const bool emit = has && !ovf;
+    const bool mine = emit && gl < count;
+    int pos = gl;
+    int seg = (mine && !(my_d == 1 && l1_sorted)) ? my_lvln - my_lvl0 : 0;
+    if (seg) pos = my_lvl0;
+    for (int k2 = 0; __any_sync(FULL, k2 < seg); k2++) {
+      const int src = gbase + (k2 < seg ? my_lvl0 + k2 : gl);
+      const int vj = __shfl_sync(FULL, my_v, src);
+      if (k2 < seg && vj < my_v) pos++;
+    }
+    if (mine) {
+      const long long row = (long long)s - src_begin;
+      out_nbr[row * K + pos] = my_v;
+      out_dist[row * K + pos] = my_d;
+    }
+    if (emit && gl == 0) out_cnt[(long long)s - src_begin] = count;
+    if (has && ovf && gl == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+    if (emit) {
+      w_scanned += scanned;
+      w_expanded += expanded;
+    }
+  }
+  if (work && gl == 0) {
+    atomicAdd(work, w_scanned);
+    atomicAdd(work + 1, w_expanded);
+  }
+}
+
+// Lean warp-per-source variant of tier 1 (G = 32): level 0 is the sorted
+// adjacency of s itself (no dedupe needed beyond the hash insert), deeper
+// levels use the bitmap parent lookup with the next chunk's candidate load
+// issued before the current chunk's hash work (two loads in flight per lane).
+template <int CAP, int PCAP, int TCAP, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
+    pbfs_warp(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
+              unsigned long long seed, long long src_begin, long long nsrc,
+              int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
+              int* __restrict__ ovf_list, int* __restrict__ ovf_count,
+              unsigned long long* __restrict__ work) {
+  using L = Tier1<32, CAP, PCAP, TCAP>;
+  constexpr int HC = L::HC, TW = L::TW;
+  extern __shared__ __align__(16) int smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
+  int* hkey = smem + warp * L::WORDS;
+  int* disc = hkey + HC;
+  int* ppre = disc + CAP;
+  int* pbeg = ppre + PCAP;
+  unsigned* bmap = reinterpret_cast<unsigned*>(pbeg + PCAP);
+  unsigned long long w_scanned = 0, w_expanded = 0;
+
+  for (long long item = (long long)blockIdx.x * WARPS + warp; item < nsrc;
+       item += (long long)gridDim.x * WARPS) {
+    const int s = (int)(src_begin + item);
+    {
+      int4* h4 = reinterpret_cast<int4*>(hkey);
+#pragma unroll
+      for (int i = lane; i < HC / 4; i += 32) h4[i] = make_int4(-1, -1, -1, -1);
+    }
+    const int b0 = __ldg(indptr + s);
+    const int T0 = __ldg(indptr + s + 1) - b0;
+    __syncwarp();
+    bool ovf = T0 > CAP - 2;
+    int count = 0, nst = 0, lb = 1, le = 1, depth = 1;
+    int my_v = 0, my_d = 0, my_lvl0 = 0, my_lvln = 0;
+    bool l1_sorted = false;
+    unsigned long long scanned = T0, expanded = 1;
+    if (!ovf) {
+      // ---- level 1: adjacency of s, already in discovery (= id) order
+      if (lane == 0) hkey[hash_id(s) & (HC - 1)] = s;
+      __syncwarp();
+      for (int t0 = 0; t0 < T0; t0 += 32) {
+        const int t = t0 + lane;
+        if (t < T0) {
+          const int w = __ldg(indices + b0 + t);
+          unsigned h = hash_id(w) & (HC - 1);
+          while (atomicCAS(&hkey[h], -1, w) != -1) h = (h + 1) & (HC - 1);
+          disc[1 + t] = w;
+        }
+      }
+      __syncwarp();
+      nst = T0;
+      le = 1 + T0;
+      const int take = nst < K ? nst : K;
+      if (nst > K) {
+        // crossing at level 1
+        int j = 0;
+        if (lane < K)
+          j = lane + (int)(splitmix_at(seed + SPLIT_GAMMA * (unsigned long long)(s + 1), lane) %
+                           (unsigned long long)(nst - lane));
+        for (int i = 0; i < K; i++) {
+          const int ji = __shfl_sync(FULL, j, i);
+          if (lane == 0) {
+            const int a = disc[1 + i];
+            disc[1 + i] = disc[1 + ji];
+            disc[1 + ji] = a;
+          }
+        }
+        __syncwarp();
+      } else {
+        l1_sorted = true;
+      }
+      if (lane < take) {
+        my_v = disc[1 + lane];
+        my_d = 1;
+        my_lvl0 = 0;
+        my_lvln = take;
+      }
+      count = take;
+    }
+    // ---- deeper levels
+    while (!ovf && count < K && nst > 0) {
+      const int f = nst;  // frontier = last level, disc[lb, le)
+      if (f > PCAP) {
         ovf = true;
         break;
       }
-      if (nst == 0) break;  // component exhausted
-      // ---- order the new level by (min parent rank, id) == discovery order
-      int P = 32;
-      while (P < nst) P <<= 1;
-      for (int i = lane; i < P; i += 32) {
-        long long key = LLONG_MAX;
-        if (i < nst) {
-          int w = stage[i];
-          unsigned h = hash_id(w) & (HC - 1);
-          while (hkey[h] != w) h = (h + 1) & (HC - 1);
-          key = ((long long)(hval[h] & 0xFFFFF) << 32) | (unsigned)w;
+      for (int w = lane; w < TW; w += 32) bmap[w] = 0u;
+      __syncwarp();
+      int carry = 0, nne = 0;
+      for (int i0 = 0; i0 < f; i0 += 32) {
+        const int i = i0 + lane;
+        int d = 0, b = 0;
+        if (i < f) {
+          const int u = disc[lb + i];
+          b = __ldg(indptr + u);
+          d = __ldg(indptr + u + 1) - b;
         }
-        key64[i] = key;
+        const int inc = warp_incl_scan(d);
+        const unsigned ne = __ballot_sync(FULL, d > 0);
+        if (d > 0) {
+          const int r = nne + __popc(ne & lt);
+          const int p0 = carry + inc - d;
+          ppre[r] = p0;
+          pbeg[r] = b;
+          if (p0 < TCAP) atomicOr(&bmap[p0 >> 5], 1u << (p0 & 31));
+        }
+        carry += __shfl_sync(FULL, inc, 31);
+        nne += __popc(ne);
+      }
+      const int T = carry;
+      if (T > TCAP) {
+        ovf = true;
+        break;
       }
       __syncwarp();
-      warp_bitonic_sort(key64, P);
-      for (int i = lane; i < nst; i += 32) disc[le + i] = (int)(key64[i] & 0xffffffffLL);
+      scanned += T;
+      expanded += f;
+      depth++;
+      const int room = CAP - le;
+      nst = 0;
+      int pb = -1;
+      bool fail = false;
+      // chunk 0 load
+      unsigned m = T > 0 ? bmap[0] : 0u;
+      int w = -1;
+      if (lane < T) {
+        const int p = pb + __popc(m & le_mask);
+        w = __ldg(indices + pbeg[p] + (lane - ppre[p]));
+      }
+      pb += __popc(m);
+      for (int t0 = 0; t0 < T; t0 += 32) {
+        // prefetch next chunk
+        int wn = -1;
+        const int t1 = t0 + 32;
+        if (t1 < T) {
+          const unsigned m1 = bmap[t1 >> 5];
+          if (t1 + lane < T) {
+            const int p = pb + __popc(m1 & le_mask);
+            wn = __ldg(indices + pbeg[p] + (t1 + lane - ppre[p]));
+          }
+          pb += __popc(m1);
+        }
+        const bool act = t0 + lane < T;
+        const unsigned grp = __match_any_sync(FULL, w);
+        bool isnew = false;
+        if (act && lane == __ffs(grp) - 1) {
+          unsigned h = hash_id(w) & (HC - 1);
+          int probe = 0;
+          for (; probe < HC; probe++) {
+            const int old = atomicCAS(&hkey[h], -1, w);
+            if (old == -1) {
+              isnew = true;
+              break;
+            }
+            if (old == w) break;
+            h = (h + 1) & (HC - 1);
+          }
+          fail |= probe == HC;
+        }
+        const unsigned bal = __ballot_sync(FULL, isnew);
+        if (isnew) {
+          const int pos = nst + __popc(bal & lt);
+          if (pos < room) disc[le + pos] = w;
+        }
+        nst += __popc(bal);
+        w = wn;
+      }
+      if (__any_sync(FULL, fail) || nst > room - 1) {
+        ovf = true;
+        break;
+      }
       __syncwarp();
+      if (nst == 0) break;
       const int remaining = K - count;
       int take = nst;
       if (nst > remaining) {
-        // random subset of the crossing level (_kernels.py:98-105)
-        if (lane == 0) {
-          unsigned long long st = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
-          for (int i = 0; i < remaining; i++) {
-            int j = i + (int)(splitmix_next(st) % (unsigned long long)(nst - i));
-            int a = disc[le + i];
-            disc[le + i] = disc[le + j];
-            disc[le + j] = a;
+        int j = 0;
+        if (lane < remaining)
+          j = lane + (int)(splitmix_at(seed + SPLIT_GAMMA * (unsigned long long)(s + 1), lane) %
+                           (unsigned long long)(nst - lane));
+        for (int i = 0; i < remaining; i++) {
+          const int ji = __shfl_sync(FULL, j, i);
+          if (lane == 0) {
+            const int a = disc[le + i];
+            disc[le + i] = disc[le + ji];
+            disc[le + ji] = a;
           }
         }
         __syncwarp();
@@ -222,6 +469,8 @@ __global__ void __launch_bounds__(WARPS * 32)
       if (lane >= count && lane < count + take) {
         my_v = disc[le + lane - count];
         my_d = depth;
+        my_lvl0 = count;
+        my_lvln = count + take;
       }
       count += take;
       lb = le;
@@ -231,8 +480,20 @@ __global__ void __launch_bounds__(WARPS * 32)
       if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
       continue;
     }
+    // ---- output in (dist, id) order: rank ids inside each level
+    int pos = lane;
+    const int seg = (lane < count && !(my_d == 1 && l1_sorted)) ? my_lvln - my_lvl0 : 0;
+    if (seg) pos = my_lvl0;
+    const int segmax = __reduce_max_sync(FULL, seg);
+    for (int k2 = 0; k2 < segmax; k2++) {
+      const int vj = __shfl_sync(FULL, my_v, k2 < seg ? my_lvl0 + k2 : lane);
+      if (k2 < seg && vj < my_v) pos++;
+    }
     const long long row = (long long)s - src_begin;
-    store_sorted_row(count, my_v, my_d, out_nbr + row * K, out_dist + row * K);
+    if (lane < count) {
+      out_nbr[row * K + pos] = my_v;
+      out_dist[row * K + pos] = my_d;
+    }
     if (lane == 0) out_cnt[row] = count;
     w_scanned += scanned;
     w_expanded += expanded;
@@ -240,6 +501,200 @@ __global__ void __launch_bounds__(WARPS * 32)
   if (work && lane == 0) {
     atomicAdd(work, w_scanned);
     atomicAdd(work + 1, w_expanded);
+  }
+}
+
+// ------------------------------------------------------------- tier 0
+// Thread per source: each thread runs the reference's sequential FIFO BFS
+// (_kernels.py:76-131) for its own source -- no warp collectives at all; the
+// 4M independent sources supply the parallelism.  Per-thread state lives in
+// shared memory laid out slot-major ([slot][thread]), so the random hash slots
+// of the 32 lanes of a warp always fall into 32 different banks.
+//   hash   HC slots of vertex ids (linear probing, cleared per source)
+//   list   LCAP discovered vertices of levels >= 2 in discovery order; level 1
+//          is the sorted adjacency of s itself, read straight from the CSR
+// Sources whose ball does not fit (discovered > HLIM, a level > LCAP, or a
+// level-1 crossing with deg(s) > LCAP) are pushed to the warp tiers.
+template <int HC, int LCAP, int TPB>
+struct Tier0 {
+  static constexpr int HLIM = HC * 3 / 4;
+  static constexpr size_t BYTES = sizeof(int) * (size_t)(HC + LCAP) * TPB;
+};
+
+// x % d for d < 2^31 without the 64-bit division routine: a double-precision
+// quotient estimate (error < 2^14) corrected once in exact integer arithmetic.
+__device__ __forceinline__ int umod64_small(unsigned long long x, int d) {
+  const double dd = (double)d;
+  unsigned long long q = (unsigned long long)__ddiv_rz(__ull2double_rz(x), dd);
+  long long r = (long long)(x - q * (unsigned long long)d);  // |r| < 2^14 * d < 2^45
+  long long q2 = (long long)floor((double)r / dd);
+  r -= q2 * (long long)d;
+  if (r < 0) r += d;
+  if (r >= d) r -= d;
+  return (int)r;
+}
+
+template <int HC, int LCAP, int TPB>
+__global__ void __launch_bounds__(TPB)
+    pbfs_thread(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
+                unsigned long long seed, long long src_begin, long long nsrc,
+                int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
+                int* __restrict__ ovf_list, int* __restrict__ ovf_count,
+                unsigned long long* __restrict__ work) {
+  constexpr int HLIM = Tier0<HC, LCAP, TPB>::HLIM;
+  extern __shared__ __align__(16) int smem[];
+  int* hk = smem + threadIdx.x;                     // hk[i * TPB]
+  int* dl = smem + HC * TPB + threadIdx.x;          // dl[i * TPB]
+  unsigned long long w_scanned = 0, w_expanded = 0;
+  for (long long item = (long long)blockIdx.x * TPB + threadIdx.x; item < nsrc;
+       item += (long long)gridDim.x * TPB) {
+    const int s = (int)(src_begin + item);
+    const long long row = item;
+    int* rn = out_nbr + row * K;
+    int* rd = out_dist + row * K;
+#pragma unroll
+    for (int i = 0; i < HC; i++) hk[i * TPB] = -1;
+    int nins = 0;
+    bool ovf = false;
+    // insert w; returns true if it was not present
+    auto insert = [&](int w) -> bool {
+      unsigned h = hash_id(w) & (HC - 1);
+      for (;;) {
+        const int k = hk[h * TPB];
+        if (k == w) return false;
+        if (k == -1) {
+          hk[h * TPB] = w;
+          nins++;
+          return true;
+        }
+        h = (h + 1) & (HC - 1);
+      }
+    };
+    insert(s);
+    const int b0 = __ldg(indptr + s), e0 = __ldg(indptr + s + 1);
+    const int deg = e0 - b0;
+    unsigned long long scanned = deg, expanded = 1;
+    int count = 0;
+    const unsigned long long fy_base = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
+    if (deg + 1 > HLIM || (deg > K && deg > LCAP)) {
+      ovf = true;
+    } else {
+      // ---- level 1: the sorted adjacency of s
+      int p = b0;
+      for (; p + 4 <= e0; p += 4) {
+        const int w0 = __ldg(indices + p), w1 = __ldg(indices + p + 1);
+        const int w2 = __ldg(indices + p + 2), w3 = __ldg(indices + p + 3);
+        insert(w0);
+        insert(w1);
+        insert(w2);
+        insert(w3);
+      }
+      for (; p < e0; p++) insert(__ldg(indices + p));
+      if (deg > K) {
+        // level 1 crosses the budget: Fisher-Yates on a copy of adj(s)
+        for (int i = 0; i < deg; i++) dl[i * TPB] = __ldg(indices + b0 + i);
+        unsigned long long st = fy_base;
+        for (int i = 0; i < K; i++) {
+          const int j = i + umod64_small(splitmix_next(st), deg - i);
+          const int a = dl[i * TPB];
+          dl[i * TPB] = dl[j * TPB];
+          dl[j * TPB] = a;
+        }
+        for (int i = 0; i < K; i++) {  // picks sorted by id (insertion into the row)
+          const int v = dl[i * TPB];
+          int q = i - 1;
+          while (q >= 0 && rn[q] > v) {
+            rn[q + 1] = rn[q];
+            q--;
+          }
+          rn[q + 1] = v;
+        }
+        for (int i = 0; i < K; i++) rd[i] = 1;
+        count = K;
+      } else {
+        for (int i = 0; i < deg; i++) {
+          rn[i] = __ldg(indices + b0 + i);
+          rd[i] = 1;
+        }
+        count = deg;
+        // ---- levels >= 2; frontier of level 1 is adj(s) in global memory
+        int lb = 0, le = 0;  // frontier = dl[lb, le) once past level 1
+        bool from_adj = true;
+        int cur_n = deg, depth = 1;
+        while (count < K && cur_n > 0) {
+          int nst = 0;
+          depth++;
+          for (int ci = 0; ci < cur_n && !ovf; ci++) {
+            const int u = from_adj ? __ldg(indices + b0 + ci) : dl[(lb + ci) * TPB];
+            const int ub = __ldg(indptr + u), ue = __ldg(indptr + u + 1);
+            scanned += ue - ub;
+            expanded++;
+            int q = ub;
+            for (; q + 4 <= ue; q += 4) {
+              const int w0 = __ldg(indices + q), w1 = __ldg(indices + q + 1);
+              const int w2 = __ldg(indices + q + 2), w3 = __ldg(indices + q + 3);
+              if (insert(w0)) { if (le + nst < LCAP) dl[(le + nst) * TPB] = w0; nst++; }
+              if (insert(w1)) { if (le + nst < LCAP) dl[(le + nst) * TPB] = w1; nst++; }
+              if (insert(w2)) { if (le + nst < LCAP) dl[(le + nst) * TPB] = w2; nst++; }
+              if (insert(w3)) { if (le + nst < LCAP) dl[(le + nst) * TPB] = w3; nst++; }
+              if (nins > HLIM) break;
+            }
+            for (; q < ue && nins <= HLIM; q++) {
+              const int w = __ldg(indices + q);
+              if (insert(w)) {
+                if (le + nst < LCAP) dl[(le + nst) * TPB] = w;
+                nst++;
+              }
+            }
+            if (nins > HLIM || le + nst > LCAP) ovf = true;
+          }
+          if (ovf || nst == 0) break;
+          const int remaining = K - count;
+          int take = nst;
+          if (nst > remaining) {
+            unsigned long long st = fy_base;
+            for (int i = 0; i < remaining; i++) {
+              const int j = i + umod64_small(splitmix_next(st), nst - i);
+              const int a = dl[(le + i) * TPB];
+              dl[(le + i) * TPB] = dl[(le + j) * TPB];
+              dl[(le + j) * TPB] = a;
+            }
+            take = remaining;
+          }
+          // append this level's picks to the row, sorted by id within the level
+          for (int i = 0; i < take; i++) {
+            const int v = dl[(le + i) * TPB];
+            int q = count + i - 1;
+            while (q >= count && rn[q] > v) {
+              rn[q + 1] = rn[q];
+              q--;
+            }
+            rn[q + 1] = v;
+            rd[count + i] = depth;
+          }
+          count += take;
+          from_adj = false;
+          lb = le;
+          le += nst;
+          cur_n = nst;
+        }
+      }
+    }
+    if (ovf) {
+      ovf_list[atomicAdd(ovf_count, 1)] = s;
+      continue;
+    }
+    out_cnt[row] = count;
+    w_scanned += scanned;
+    w_expanded += expanded;
+  }
+  if (work) {
+    w_scanned = warp_sum(w_scanned);
+    w_expanded = warp_sum(w_expanded);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(work, w_scanned);
+      atomicAdd(work + 1, w_expanded);
+    }
   }
 }
 
@@ -360,13 +815,14 @@ __global__ void clear_slots_if_needed(int* slots, size_t words, const int* count
     slots[i] = 0;
 }
 
-constexpr int T1A_CAP = 128, T1A_WARPS = 8;
-constexpr int T1B_CAP = 1024, T1B_WARPS = 2;
+constexpr int T1A_CAP = 128, T1A_PCAP = 64, T1A_TCAP = 512, T1A_WARPS = 8;
+constexpr int T1B_CAP = 1024, T1B_PCAP = 512, T1B_TCAP = 4096, T1B_WARPS = 2;
 
 struct PbfsWs {
   int* ovfA;
   int* ovfB;
-  int* counts;  // [0]=ovfA count, [1]=ovfB count
+  int* ovf0;
+  int* counts;  // [0]=ovfA count, [1]=ovfB count, [2]=ovf0 count
   unsigned long long* work;
   int* slots;
 };
@@ -382,17 +838,85 @@ size_t pbfs_ws_layout(long long n, long long nsrc, int slots, char* base, PbfsWs
   };
   size_t oA = take(sizeof(int) * (size_t)(nsrc + 1));
   size_t oB = take(sizeof(int) * (size_t)(nsrc + 1));
+  size_t o0 = take(sizeof(int) * (size_t)(nsrc + 1));
   size_t oC = take(sizeof(int) * 4);
   size_t oW = take(sizeof(unsigned long long) * 2);
   size_t oS = take(sizeof(int) * 2 * (size_t)n * (size_t)slots);
   if (ws && base) {
     ws->ovfA = (int*)(base + oA);
     ws->ovfB = (int*)(base + oB);
+    ws->ovf0 = (int*)(base + o0);
     ws->counts = (int*)(base + oC);
     ws->work = (unsigned long long*)(base + oW);
     ws->slots = (int*)(base + oS);
   }
   return off;
+}
+
+template <int G>
+cudaError_t launch_tier1a(int sms, const int* indptr, const int* indices, int k,
+                          unsigned long long seed, long long src_begin, long long nsrc,
+                          const int* list, const int* list_count, int* out_nbr, int* out_dist,
+                          int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
+                          cudaStream_t st) {
+  using LA = Tier1<G, T1A_CAP, T1A_PCAP, T1A_TCAP>;
+  constexpr size_t smem = sizeof(int) * LA::WORDS * LA::NG * T1A_WARPS;
+  auto kern = pbfs_tier1<G, T1A_CAP, T1A_PCAP, T1A_TCAP, T1A_WARPS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T1A_WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  const long long per_block = (long long)T1A_WARPS * LA::NG;
+  long long blocks = (nsrc + per_block - 1) / per_block;
+  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * (list ? 1 : 8);
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, T1A_WARPS * 32, smem, st>>>(indptr, indices, k, seed, src_begin, nsrc,
+                                                        list, list_count, out_nbr, out_dist,
+                                                        out_count, ovf_out, ovf_cnt, work);
+  return cudaGetLastError();
+}
+
+constexpr int T0_HC = 128, T0_LCAP = 64, T0_TPB = 64;
+
+cudaError_t launch_thread(int sms, const int* indptr, const int* indices, int k,
+                          unsigned long long seed, long long src_begin, long long nsrc,
+                          int* out_nbr, int* out_dist, int* out_count, int* ovf_out, int* ovf_cnt,
+                          unsigned long long* work, cudaStream_t st) {
+  constexpr size_t smem = Tier0<T0_HC, T0_LCAP, T0_TPB>::BYTES;
+  auto kern = pbfs_thread<T0_HC, T0_LCAP, T0_TPB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T0_TPB, smem);
+  if (e != cudaSuccess) return e;
+  long long blocks = (nsrc + T0_TPB - 1) / T0_TPB;
+  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * 16;
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, T0_TPB, smem, st>>>(indptr, indices, k, seed, src_begin, nsrc, out_nbr,
+                                               out_dist, out_count, ovf_out, ovf_cnt, work);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lean(int sms, const int* indptr, const int* indices, int k,
+                        unsigned long long seed, long long src_begin, long long nsrc,
+                        int* out_nbr, int* out_dist, int* out_count, const PbfsWs& ws,
+                        unsigned long long* work, cudaStream_t st) {
+  using LA = Tier1<32, T1A_CAP, T1A_PCAP, T1A_TCAP>;
+  constexpr int W = 8;
+  constexpr size_t smem = sizeof(int) * LA::WORDS * W;
+  auto kern = pbfs_warp<T1A_CAP, T1A_PCAP, T1A_TCAP, W, 8>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
+  if (e != cudaSuccess) return e;
+  long long blocks = (nsrc + W - 1) / W;
+  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * 8;
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, W * 32, smem, st>>>(indptr, indices, k, seed, src_begin, nsrc, out_nbr,
+                                                out_dist, out_count, ws.ovfA, ws.counts + 0, work);
+  return cudaGetLastError();
 }
 
 int sm_count() {
@@ -444,23 +968,31 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
   }
   const int sms = sm_count();
   if (k <= 32) {
-    {
-      constexpr size_t smem = Tier1<T1A_CAP>::BYTES * T1A_WARPS;
-      auto kern = pbfs_tier1<T1A_CAP, T1A_WARPS>;
-      GU_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int per_sm = 0;
-      GU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T1A_WARPS * 32, smem));
-      long long blocks = (nsrc + T1A_WARPS - 1) / T1A_WARPS;
-      long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * 8;
-      if (blocks > cap) blocks = cap;
-      kern<<<(unsigned)blocks, T1A_WARPS * 32, smem, st>>>(
-          indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr, out_nbr, out_dist,
-          out_count, ws.ovfA, ws.counts + 0, work);
-      GU_CHECK_LAUNCH("pbfs_tier1<128>");
+    // tier 1a (lean warp per source, CAP 128) -> tier 1b (CAP 1024) -> tier 2.
+    // GU_PBFS_MODE = lean (default) | thread | g16 | g32 selects the first tier
+    // (tuning / comparison only; every mode is exact).
+    static const char* env_mode = getenv("GU_PBFS_MODE");
+    const char* mode = env_mode ? env_mode : "lean";
+    if (!strcmp(mode, "thread")) {
+      GU_CHECK(launch_thread(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
+                             out_count, ws.ovf0, ws.counts + 2, work, st));
+      GU_CHECK(launch_tier1a<32>(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0,
+                                 ws.counts + 2, out_nbr, out_dist, out_count, ws.ovfA,
+                                 ws.counts + 0, work, st));
+    } else if (!strcmp(mode, "lean")) {
+      GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
+                           out_count, ws, work, st));
+    } else if (k <= 16 && !strcmp(mode, "g16")) {
+      GU_CHECK(launch_tier1a<16>(sms, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
+                                 out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
+    } else {
+      GU_CHECK(launch_tier1a<32>(sms, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
+                                 out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
     }
     {
-      constexpr size_t smem = Tier1<T1B_CAP>::BYTES * T1B_WARPS;
-      auto kern = pbfs_tier1<T1B_CAP, T1B_WARPS>;
+      using LB = Tier1<32, T1B_CAP, T1B_PCAP, T1B_TCAP>;
+      constexpr size_t smem = sizeof(int) * LB::WORDS * LB::NG * T1B_WARPS;
+      auto kern = pbfs_tier1<32, T1B_CAP, T1B_PCAP, T1B_TCAP, T1B_WARPS>;
       GU_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0;
       GU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T1B_WARPS * 32, smem));
@@ -468,10 +1000,10 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
       kern<<<(unsigned)blocks, T1B_WARPS * 32, smem, st>>>(
           indptr, indices, k, seed, src_begin, nsrc, ws.ovfA, ws.counts + 0, out_nbr, out_dist,
           out_count, ws.ovfB, ws.counts + 1, work);
-      GU_CHECK_LAUNCH("pbfs_tier1<1024>");
+      GU_CHECK_LAUNCH("pbfs_tier1 (b)");
     }
   } else {
-    // k > 32: every source goes straight to the exact tier-2 path
+    // k > group size: every source goes straight to the exact tier-2 path
     fill_range_list<<<(unsigned)((nsrc + 255) / 256), 256, 0, st>>>(ws.ovfB, ws.counts + 1,
                                                                    src_begin, nsrc);
     GU_CHECK_LAUNCH("fill_range_list");
@@ -489,9 +1021,13 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
   return GU_OK;
 }
 
-extern "C" int gu_partial_bfs_overflow_counts(void* workspace, int64_t nsrc, int32_t* host_out2) {
+extern "C" int gu_partial_bfs_overflow_counts(void* workspace, int64_t nsrc, int32_t* host_out3) {
   PbfsWs ws;
   pbfs_ws_layout(1, nsrc, 1, (char*)workspace, &ws);
-  GU_CHECK(cudaMemcpy(host_out2, ws.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+  int c[3];
+  GU_CHECK(cudaMemcpy(c, ws.counts, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  host_out3[0] = c[2];  // fell from tier 0 to tier 1a
+  host_out3[1] = c[0];  // fell to tier 1b
+  host_out3[2] = c[1];  // fell to tier 2
   return GU_OK;
 }
