@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libgumap.so")
+LIB_PATH = os.environ.get("GU_LIB_PATH") or os.path.join(_HERE, "_build", "libgumap.so")
 
 ABI_VERSION = 1
 

@@ -58,6 +58,20 @@ __device__ __forceinline__ unsigned long long splitmix_at(unsigned long long bas
   return z ^ (z >> 31);
 }
 
+// x % d for d < 2^31 without the 64-bit division routine: a double-precision
+// quotient estimate (never above the true quotient, error < 2^14) corrected
+// in exact integer arithmetic.
+__device__ __forceinline__ int umod64_small(unsigned long long x, int d) {
+  const double dd = (double)d;
+  const unsigned long long q = (unsigned long long)__ddiv_rz(__ull2double_rz(x), dd);
+  long long r = (long long)(x - q * (unsigned long long)d);  // 0 <= r < 2^14 * d
+  const long long q2 = (long long)((double)r / dd);
+  r -= q2 * (long long)d;
+  while (r < 0) r += d;
+  while (r >= d) r -= d;
+  return (int)r;
+}
+
 // Discovery order without sorting: the reference appends a vertex the first
 // time it is met while scanning the frontier in queue order, each parent's
 // sorted adjacency in turn.  Concatenating the frontier's adjacency lists in
@@ -272,10 +286,15 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
 }
 
-// Lean warp-per-source variant of tier 1 (G = 32): level 0 is the sorted
-// adjacency of s itself (no dedupe needed beyond the hash insert), deeper
-// levels use the bitmap parent lookup with the next chunk's candidate load
-// issued before the current chunk's hash work (two loads in flight per lane).
+// Lean warp-per-source variant of tier 1 (the default first tier).
+//   * level 1 is the sorted adjacency of s itself: no dedupe beyond the hash
+//     insert, and (when not crossing) already in output order;
+//   * deeper levels: parent of a flattened index from a per-level bitmap of
+//     adjacency starts (popc), the next chunk's candidate load issued before
+//     the current chunk's hash work;
+//   * a level's entries are written to the output row as soon as the level is
+//     settled (rank by id inside the level; levels are in distance order);
+//   * overflow is detected before the hash can fill, so probing is unbounded.
 template <int CAP, int PCAP, int TCAP, int WARPS, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     pbfs_warp(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
@@ -288,16 +307,30 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   extern __shared__ __align__(16) int smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
-  int* hkey = smem + warp * L::WORDS;
-  int* disc = hkey + HC;
-  int* ppre = disc + CAP;
-  int* pbeg = ppre + PCAP;
-  unsigned* bmap = reinterpret_cast<unsigned*>(pbeg + PCAP);
+  int* const hkey = smem + warp * L::WORDS;
+  int* const disc = hkey + HC;
+  int* const ppre = disc + CAP;
+  int* const pbeg = ppre + PCAP;
+  unsigned* const bmap = reinterpret_cast<unsigned*>(pbeg + PCAP);
   unsigned long long w_scanned = 0, w_expanded = 0;
+
+  // claim w in the hash; true iff it was not there (table never fills: the
+  // callers stop inserting once a source is known to overflow CAP)
+  auto claim = [&](int w) -> bool {
+    unsigned h = hash_id(w) & (HC - 1);
+    for (;;) {
+      const int old = atomicCAS(&hkey[h], -1, w);
+      if (old == -1) return true;
+      if (old == w) return false;
+      h = (h + 1) & (HC - 1);
+    }
+  };
 
   for (long long item = (long long)blockIdx.x * WARPS + warp; item < nsrc;
        item += (long long)gridDim.x * WARPS) {
     const int s = (int)(src_begin + item);
+    int* const rn = out_nbr + item * K;
+    int* const rd = out_dist + item * K;
     {
       int4* h4 = reinterpret_cast<int4*>(hkey);
 #pragma unroll
@@ -306,10 +339,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     const int b0 = __ldg(indptr + s);
     const int T0 = __ldg(indptr + s + 1) - b0;
     __syncwarp();
+    const unsigned long long fy_base = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
     bool ovf = T0 > CAP - 2;
     int count = 0, nst = 0, lb = 1, le = 1, depth = 1;
-    int my_v = 0, my_d = 0, my_lvl0 = 0, my_lvln = 0;
-    bool l1_sorted = false;
     unsigned long long scanned = T0, expanded = 1;
     if (!ovf) {
       // ---- level 1: adjacency of s, already in discovery (= id) order
@@ -319,21 +351,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         const int t = t0 + lane;
         if (t < T0) {
           const int w = __ldg(indices + b0 + t);
-          unsigned h = hash_id(w) & (HC - 1);
-          while (atomicCAS(&hkey[h], -1, w) != -1) h = (h + 1) & (HC - 1);
+          claim(w);
           disc[1 + t] = w;
         }
       }
       __syncwarp();
       nst = T0;
       le = 1 + T0;
-      const int take = nst < K ? nst : K;
       if (nst > K) {
-        // crossing at level 1
+        // level 1 crosses the budget: partial Fisher-Yates, picks ranked by id
         int j = 0;
-        if (lane < K)
-          j = lane + (int)(splitmix_at(seed + SPLIT_GAMMA * (unsigned long long)(s + 1), lane) %
-                           (unsigned long long)(nst - lane));
+        if (lane < K) j = lane + umod64_small(splitmix_at(fy_base, lane), nst - lane);
         for (int i = 0; i < K; i++) {
           const int ji = __shfl_sync(FULL, j, i);
           if (lane == 0) {
@@ -343,16 +371,21 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
           }
         }
         __syncwarp();
+        if (lane < K) {
+          const int v = disc[1 + lane];
+          int r = 0;
+          for (int q = 0; q < K; q++) r += disc[1 + q] < v;
+          rn[r] = v;
+          rd[r] = 1;
+        }
+        count = K;
       } else {
-        l1_sorted = true;
+        if (lane < nst) {
+          rn[lane] = disc[1 + lane];
+          rd[lane] = 1;
+        }
+        count = nst;
       }
-      if (lane < take) {
-        my_v = disc[1 + lane];
-        my_d = 1;
-        my_lvl0 = 0;
-        my_lvln = take;
-      }
-      count = take;
     }
     // ---- deeper levels
     while (!ovf && count < K && nst > 0) {
@@ -396,8 +429,6 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       const int room = CAP - le;
       nst = 0;
       int pb = -1;
-      bool fail = false;
-      // chunk 0 load
       unsigned m = T > 0 ? bmap[0] : 0u;
       int w = -1;
       if (lane < T) {
@@ -406,7 +437,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       }
       pb += __popc(m);
       for (int t0 = 0; t0 < T; t0 += 32) {
-        // prefetch next chunk
+        if (nst >= room) {  // the level cannot fit: stop inserting, overflow
+          ovf = true;
+          break;
+        }
         int wn = -1;
         const int t1 = t0 + 32;
         if (t1 < T) {
@@ -417,23 +451,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
           }
           pb += __popc(m1);
         }
-        const bool act = t0 + lane < T;
         const unsigned grp = __match_any_sync(FULL, w);
-        bool isnew = false;
-        if (act && lane == __ffs(grp) - 1) {
-          unsigned h = hash_id(w) & (HC - 1);
-          int probe = 0;
-          for (; probe < HC; probe++) {
-            const int old = atomicCAS(&hkey[h], -1, w);
-            if (old == -1) {
-              isnew = true;
-              break;
-            }
-            if (old == w) break;
-            h = (h + 1) & (HC - 1);
-          }
-          fail |= probe == HC;
-        }
+        const bool isnew = t0 + lane < T && lane == __ffs(grp) - 1 && claim(w);
         const unsigned bal = __ballot_sync(FULL, isnew);
         if (isnew) {
           const int pos = nst + __popc(bal & lt);
@@ -442,7 +461,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         nst += __popc(bal);
         w = wn;
       }
-      if (__any_sync(FULL, fail) || nst > room - 1) {
+      if (ovf || nst > room - 1) {
         ovf = true;
         break;
       }
@@ -452,9 +471,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       int take = nst;
       if (nst > remaining) {
         int j = 0;
-        if (lane < remaining)
-          j = lane + (int)(splitmix_at(seed + SPLIT_GAMMA * (unsigned long long)(s + 1), lane) %
-                           (unsigned long long)(nst - lane));
+        if (lane < remaining) j = lane + umod64_small(splitmix_at(fy_base, lane), nst - lane);
         for (int i = 0; i < remaining; i++) {
           const int ji = __shfl_sync(FULL, j, i);
           if (lane == 0) {
@@ -466,11 +483,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         __syncwarp();
         take = remaining;
       }
-      if (lane >= count && lane < count + take) {
-        my_v = disc[le + lane - count];
-        my_d = depth;
-        my_lvl0 = count;
-        my_lvln = count + take;
+      for (int i0 = 0; i0 < take; i0 += 32) {
+        const int i = i0 + lane;
+        if (i < take) {
+          const int v = disc[le + i];
+          int r = 0;
+          for (int q = 0; q < take; q++) r += disc[le + q] < v;
+          rn[count + r] = v;
+          rd[count + r] = depth;
+        }
       }
       count += take;
       lb = le;
@@ -480,21 +501,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
       continue;
     }
-    // ---- output in (dist, id) order: rank ids inside each level
-    int pos = lane;
-    const int seg = (lane < count && !(my_d == 1 && l1_sorted)) ? my_lvln - my_lvl0 : 0;
-    if (seg) pos = my_lvl0;
-    const int segmax = __reduce_max_sync(FULL, seg);
-    for (int k2 = 0; k2 < segmax; k2++) {
-      const int vj = __shfl_sync(FULL, my_v, k2 < seg ? my_lvl0 + k2 : lane);
-      if (k2 < seg && vj < my_v) pos++;
-    }
-    const long long row = (long long)s - src_begin;
-    if (lane < count) {
-      out_nbr[row * K + pos] = my_v;
-      out_dist[row * K + pos] = my_d;
-    }
-    if (lane == 0) out_cnt[row] = count;
+    if (lane == 0) out_cnt[item] = count;
     w_scanned += scanned;
     w_expanded += expanded;
   }
@@ -506,33 +513,27 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 
 // ------------------------------------------------------------- tier 0
 // Thread per source: each thread runs the reference's sequential FIFO BFS
-// (_kernels.py:76-131) for its own source -- no warp collectives at all; the
-// 4M independent sources supply the parallelism.  Per-thread state lives in
-// shared memory laid out slot-major ([slot][thread]), so the random hash slots
-// of the 32 lanes of a warp always fall into 32 different banks.
-//   hash   HC slots of vertex ids (linear probing, cleared per source)
-//   list   LCAP discovered vertices of levels >= 2 in discovery order; level 1
-//          is the sorted adjacency of s itself, read straight from the CSR
-// Sources whose ball does not fit (discovered > HLIM, a level > LCAP, or a
-// level-1 crossing with deg(s) > LCAP) are pushed to the warp tiers.
+// (_kernels.py:76-131) for its own source; the 4M independent sources supply
+// the parallelism and no warp collective is needed.  Divergence is kept low
+// by structure: a parent's adjacency (<= 16 entries, the common case) is
+// loaded as one unrolled burst of independent predicated loads into
+// registers, and the next parent's burst is issued before the current one is
+// hashed (software pipeline, ~2 parents of loads in flight per thread), so
+// all lanes walk their frontiers in near-lockstep.
+// Per-thread state lives in shared memory laid out slot-major
+// ([slot][thread]), so random hash slots of the 32 lanes hit 32 distinct
+// banks:
+//   hash   HC slots of vertex ids (linear probing; cleared per source)
+//   list   LCAP discovered vertices of levels >= 1 in discovery order
+// Sources whose ball does not fit (more than HLIM discovered, or a level
+// beyond LCAP) are pushed to the warp tiers, which handle any size.
 template <int HC, int LCAP, int TPB>
 struct Tier0 {
   static constexpr int HLIM = HC * 3 / 4;
   static constexpr size_t BYTES = sizeof(int) * (size_t)(HC + LCAP) * TPB;
 };
 
-// x % d for d < 2^31 without the 64-bit division routine: a double-precision
-// quotient estimate (error < 2^14) corrected once in exact integer arithmetic.
-__device__ __forceinline__ int umod64_small(unsigned long long x, int d) {
-  const double dd = (double)d;
-  unsigned long long q = (unsigned long long)__ddiv_rz(__ull2double_rz(x), dd);
-  long long r = (long long)(x - q * (unsigned long long)d);  // |r| < 2^14 * d < 2^45
-  long long q2 = (long long)floor((double)r / dd);
-  r -= q2 * (long long)d;
-  if (r < 0) r += d;
-  if (r >= d) r -= d;
-  return (int)r;
-}
+constexpr int T0_BURST = 16;
 
 template <int HC, int LCAP, int TPB>
 __global__ void __launch_bounds__(TPB)
@@ -543,20 +544,16 @@ __global__ void __launch_bounds__(TPB)
                 unsigned long long* __restrict__ work) {
   constexpr int HLIM = Tier0<HC, LCAP, TPB>::HLIM;
   extern __shared__ __align__(16) int smem[];
-  int* hk = smem + threadIdx.x;                     // hk[i * TPB]
-  int* dl = smem + HC * TPB + threadIdx.x;          // dl[i * TPB]
+  int* hk = smem + threadIdx.x;             // hk[i * TPB]
+  int* dl = smem + HC * TPB + threadIdx.x;  // dl[i * TPB]
   unsigned long long w_scanned = 0, w_expanded = 0;
   for (long long item = (long long)blockIdx.x * TPB + threadIdx.x; item < nsrc;
        item += (long long)gridDim.x * TPB) {
     const int s = (int)(src_begin + item);
-    const long long row = item;
-    int* rn = out_nbr + row * K;
-    int* rd = out_dist + row * K;
 #pragma unroll
     for (int i = 0; i < HC; i++) hk[i * TPB] = -1;
     int nins = 0;
-    bool ovf = false;
-    // insert w; returns true if it was not present
+    // insert w; true iff it was not present
     auto insert = [&](int w) -> bool {
       unsigned h = hash_id(w) & (HC - 1);
       for (;;) {
@@ -571,120 +568,110 @@ __global__ void __launch_bounds__(TPB)
       }
     };
     insert(s);
-    const int b0 = __ldg(indptr + s), e0 = __ldg(indptr + s + 1);
-    const int deg = e0 - b0;
-    unsigned long long scanned = deg, expanded = 1;
-    int count = 0;
-    const unsigned long long fy_base = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
-    if (deg + 1 > HLIM || (deg > K && deg > LCAP)) {
-      ovf = true;
-    } else {
-      // ---- level 1: the sorted adjacency of s
-      int p = b0;
-      for (; p + 4 <= e0; p += 4) {
-        const int w0 = __ldg(indices + p), w1 = __ldg(indices + p + 1);
-        const int w2 = __ldg(indices + p + 2), w3 = __ldg(indices + p + 3);
-        insert(w0);
-        insert(w1);
-        insert(w2);
-        insert(w3);
+    // level 0 -> 1: the frontier is [s]; afterwards the frontier is dl[lb, le)
+    int lb = 0, le = 0, count = 0, depth = 0;
+    bool ovf = false;
+    unsigned long long scanned = 0, expanded = 0;
+    int* rn = out_nbr + item * K;
+    int* rd = out_dist + item * K;
+    int f = 1;  // frontier size
+    while (count < K && f > 0) {
+      depth++;
+      int nst = 0;
+      // ---- expand the frontier in queue order, two parents of loads in flight
+      auto parent = [&](int i) -> int { return depth == 1 ? s : dl[(lb + i) * TPB]; };
+      int cb = 0, ce = 0, nb = 0, ne = 0;
+      {
+        const int u0 = parent(0);
+        cb = __ldg(indptr + u0);
+        ce = __ldg(indptr + u0 + 1);
+        if (f > 1) {
+          const int u1 = parent(1);
+          nb = __ldg(indptr + u1);
+          ne = __ldg(indptr + u1 + 1);
+        }
       }
-      for (; p < e0; p++) insert(__ldg(indices + p));
-      if (deg > K) {
-        // level 1 crosses the budget: Fisher-Yates on a copy of adj(s)
-        for (int i = 0; i < deg; i++) dl[i * TPB] = __ldg(indices + b0 + i);
-        unsigned long long st = fy_base;
-        for (int i = 0; i < K; i++) {
-          const int j = i + umod64_small(splitmix_next(st), deg - i);
-          const int a = dl[i * TPB];
-          dl[i * TPB] = dl[j * TPB];
-          dl[j * TPB] = a;
+      int cur[T0_BURST];
+#pragma unroll
+      for (int q = 0; q < T0_BURST; q++) cur[q] = cb + q < ce ? __ldg(indices + cb + q) : -1;
+      for (int i = 0; i < f; i++) {
+        int nxt[T0_BURST];
+#pragma unroll
+        for (int q = 0; q < T0_BURST; q++) nxt[q] = nb + q < ne ? __ldg(indices + nb + q) : -1;
+        int nb2 = 0, ne2 = 0;
+        if (i + 2 < f) {
+          const int u2 = parent(i + 2);
+          nb2 = __ldg(indptr + u2);
+          ne2 = __ldg(indptr + u2 + 1);
         }
-        for (int i = 0; i < K; i++) {  // picks sorted by id (insertion into the row)
-          const int v = dl[i * TPB];
-          int q = i - 1;
-          while (q >= 0 && rn[q] > v) {
-            rn[q + 1] = rn[q];
-            q--;
+        scanned += ce - cb;
+        expanded++;
+#pragma unroll
+        for (int q = 0; q < T0_BURST; q++) {
+          if (cur[q] >= 0 && insert(cur[q])) {
+            if (le + nst < LCAP) dl[(le + nst) * TPB] = cur[q];
+            nst++;
           }
-          rn[q + 1] = v;
         }
-        for (int i = 0; i < K; i++) rd[i] = 1;
-        count = K;
+        for (int p = cb + T0_BURST; p < ce; p++) {  // tail of a long adjacency
+          const int w = __ldg(indices + p);
+          if (insert(w)) {
+            if (le + nst < LCAP) dl[(le + nst) * TPB] = w;
+            nst++;
+          }
+          if (nins > HLIM) break;
+        }
+        if (nins > HLIM || le + nst > LCAP) {
+          ovf = true;
+          break;
+        }
+#pragma unroll
+        for (int q = 0; q < T0_BURST; q++) cur[q] = nxt[q];
+        cb = nb;
+        ce = ne;
+        nb = nb2;
+        ne = ne2;
+      }
+      if (ovf || nst == 0) break;
+      const int remaining = K - count;
+      int take = nst;
+      if (nst > remaining) {
+        // random subset of the crossing level (_kernels.py:98-105)
+        unsigned long long st = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
+        for (int i = 0; i < remaining; i++) {
+          const int j = i + umod64_small(splitmix_next(st), nst - i);
+          const int a = dl[(le + i) * TPB];
+          dl[(le + i) * TPB] = dl[(le + j) * TPB];
+          dl[(le + j) * TPB] = a;
+        }
+        take = remaining;
+      }
+      // this level's entries in id order (level 1 of a full take is the sorted
+      // adjacency of s already); rank each entry inside the level
+      if (depth == 1 && take == nst) {
+        for (int i = 0; i < take; i++) {
+          rn[count + i] = dl[(le + i) * TPB];
+          rd[count + i] = 1;
+        }
       } else {
-        for (int i = 0; i < deg; i++) {
-          rn[i] = __ldg(indices + b0 + i);
-          rd[i] = 1;
-        }
-        count = deg;
-        // ---- levels >= 2; frontier of level 1 is adj(s) in global memory
-        int lb = 0, le = 0;  // frontier = dl[lb, le) once past level 1
-        bool from_adj = true;
-        int cur_n = deg, depth = 1;
-        while (count < K && cur_n > 0) {
-          int nst = 0;
-          depth++;
-          for (int ci = 0; ci < cur_n && !ovf; ci++) {
-            const int u = from_adj ? __ldg(indices + b0 + ci) : dl[(lb + ci) * TPB];
-            const int ub = __ldg(indptr + u), ue = __ldg(indptr + u + 1);
-            scanned += ue - ub;
-            expanded++;
-            int q = ub;
-            for (; q + 4 <= ue; q += 4) {
-              const int w0 = __ldg(indices + q), w1 = __ldg(indices + q + 1);
-              const int w2 = __ldg(indices + q + 2), w3 = __ldg(indices + q + 3);
-              if (insert(w0)) { if (le + nst < LCAP) dl[(le + nst) * TPB] = w0; nst++; }
-              if (insert(w1)) { if (le + nst < LCAP) dl[(le + nst) * TPB] = w1; nst++; }
-              if (insert(w2)) { if (le + nst < LCAP) dl[(le + nst) * TPB] = w2; nst++; }
-              if (insert(w3)) { if (le + nst < LCAP) dl[(le + nst) * TPB] = w3; nst++; }
-              if (nins > HLIM) break;
-            }
-            for (; q < ue && nins <= HLIM; q++) {
-              const int w = __ldg(indices + q);
-              if (insert(w)) {
-                if (le + nst < LCAP) dl[(le + nst) * TPB] = w;
-                nst++;
-              }
-            }
-            if (nins > HLIM || le + nst > LCAP) ovf = true;
-          }
-          if (ovf || nst == 0) break;
-          const int remaining = K - count;
-          int take = nst;
-          if (nst > remaining) {
-            unsigned long long st = fy_base;
-            for (int i = 0; i < remaining; i++) {
-              const int j = i + umod64_small(splitmix_next(st), nst - i);
-              const int a = dl[(le + i) * TPB];
-              dl[(le + i) * TPB] = dl[(le + j) * TPB];
-              dl[(le + j) * TPB] = a;
-            }
-            take = remaining;
-          }
-          // append this level's picks to the row, sorted by id within the level
-          for (int i = 0; i < take; i++) {
-            const int v = dl[(le + i) * TPB];
-            int q = count + i - 1;
-            while (q >= count && rn[q] > v) {
-              rn[q + 1] = rn[q];
-              q--;
-            }
-            rn[q + 1] = v;
-            rd[count + i] = depth;
-          }
-          count += take;
-          from_adj = false;
-          lb = le;
-          le += nst;
-          cur_n = nst;
+        for (int i = 0; i < take; i++) {
+          const int v = dl[(le + i) * TPB];
+          int r = 0;
+          for (int j = 0; j < take; j++) r += dl[(le + j) * TPB] < v;
+          rn[count + r] = v;
+          rd[count + r] = depth;
         }
       }
+      count += take;
+      lb = le;
+      le += nst;
+      f = nst;
     }
     if (ovf) {
       ovf_list[atomicAdd(ovf_count, 1)] = s;
       continue;
     }
-    out_cnt[row] = count;
+    out_cnt[item] = count;
     w_scanned += scanned;
     w_expanded += expanded;
   }
@@ -815,6 +802,9 @@ __global__ void clear_slots_if_needed(int* slots, size_t words, const int* count
     slots[i] = 0;
 }
 
+#ifndef GU_LEAN_MINB
+#define GU_LEAN_MINB 8
+#endif
 constexpr int T1A_CAP = 128, T1A_PCAP = 64, T1A_TCAP = 512, T1A_WARPS = 8;
 constexpr int T1B_CAP = 1024, T1B_PCAP = 512, T1B_TCAP = 4096, T1B_WARPS = 2;
 
@@ -877,7 +867,7 @@ cudaError_t launch_tier1a(int sms, const int* indptr, const int* indices, int k,
   return cudaGetLastError();
 }
 
-constexpr int T0_HC = 128, T0_LCAP = 64, T0_TPB = 64;
+constexpr int T0_HC = 128, T0_LCAP = 96, T0_TPB = 128;
 
 cudaError_t launch_thread(int sms, const int* indptr, const int* indices, int k,
                           unsigned long long seed, long long src_begin, long long nsrc,
@@ -905,7 +895,7 @@ cudaError_t launch_lean(int sms, const int* indptr, const int* indices, int k,
   using LA = Tier1<32, T1A_CAP, T1A_PCAP, T1A_TCAP>;
   constexpr int W = 8;
   constexpr size_t smem = sizeof(int) * LA::WORDS * W;
-  auto kern = pbfs_warp<T1A_CAP, T1A_PCAP, T1A_TCAP, W, 8>;
+  auto kern = pbfs_warp<T1A_CAP, T1A_PCAP, T1A_TCAP, W, GU_LEAN_MINB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;

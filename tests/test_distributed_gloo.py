@@ -1,0 +1,75 @@
+"""world_size-2 gloo test of the source-sharded record exchange (CPU).
+
+Each rank produces the fixed-size kNN records of its source shard (here with
+the oracle, the checker; on B200s the records come from the GPU kernels),
+packs them, all-gathers them through paper_2509_19703_b200.distributed and
+unpacks.  The gathered records must equal the single-process result
+bit for bit (per-source RNG streams make sharding exact).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, mode, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    from paper_2509_19703_b200 import fixtures as F
+    from paper_2509_19703_b200.distributed import (gather_records, pack_records, shard_range,
+                                                   unpack_records)
+
+    g = F.scale_free(3000, seed=7, m0=2) if mode == "partial" else F.grid(900)
+    k = 15
+    align = 1 if mode == "partial" else 64
+    b, e, per = shard_range(g.n, rank, world, align)
+    if mode == "partial":
+        nbr, dd, cnt = O.partial_bfs_raw(g, k, seed=3, src_begin=b, src_end=e, nthreads=2)
+    else:
+        nbr, dd, cnt = O.full_knn(g, k, seed=3, src_begin=b, src_end=e, nthreads=2, packed=False)
+    rec = pack_records(torch.from_numpy(nbr.reshape(-1, k)), torch.from_numpy(dd.reshape(-1, k)),
+                       torch.from_numpy(cnt), per)
+    allrec = gather_records(rec)
+    n2, d2, c2 = unpack_records(allrec, g.n, k)
+    np.savez(os.path.join(out_dir, f"{mode}_{rank}.npz"), nbr=n2.numpy(), dist=d2.numpy(),
+             cnt=c2.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["partial", "full"])
+def test_sharded_records_match_single_process(tmp_path, mode):
+    from oracle import oracle as O
+    from paper_2509_19703_b200 import fixtures as F
+
+    O.build()
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), mode, str(tmp_path)), nprocs=world, join=True)
+    g = F.scale_free(3000, seed=7, m0=2) if mode == "partial" else F.grid(900)
+    if mode == "partial":
+        nbr, dd, cnt = O.partial_bfs_raw(g, 15, seed=3, nthreads=2)
+    else:
+        nbr, dd, cnt = O.full_knn(g, 15, seed=3, nthreads=2, packed=False)
+    for r in range(world):
+        z = np.load(tmp_path / f"{mode}_{r}.npz")
+        assert np.array_equal(z["nbr"].reshape(-1), nbr)
+        assert np.array_equal(z["dist"].reshape(-1), dd)
+        assert np.array_equal(z["cnt"], cnt)
