@@ -511,6 +511,364 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   }
 }
 
+// ------------------------------------------------------------- tier B
+// CTA batch: S sources per CTA processed level-synchronously; every phase is
+// flattened across the batch so that threads, not warps, carry the per-item
+// work and per-source overheads are amortised:
+//   1  thread per source: frontier size f; block scan -> parent bases
+//   2  thread per parent: adjacency start and degree; block scan over the
+//      degrees -> each parent's first flattened candidate slot (sources'
+//      candidates are contiguous, in queue order); owner of every slot
+//   3  thread per candidate slot: load the neighbour id (several independent
+//      loads in flight per thread), insert it into its source's hash: key by
+//      atomicCAS, first flattened index by atomicMin of (level << 22 | t).  An
+//      id is first met at t iff the hash holds t afterwards -- the reference's
+//      FIFO discovery order (see the top of this file).
+//   4  first-occurrence flags, block exclusive scan, compaction into each
+//      source's level list in t order
+//   5  thread per source: crossing-level partial Fisher-Yates (exact 64-bit
+//      remainder by table), level entries written ranked by id.
+// Sources whose ball or level does not fit the per-source budget are pushed
+// to the warp tiers.
+constexpr int TB_THREADS = 256;
+constexpr int TB_WARPS = TB_THREADS / 32;
+
+template <int S, int HC, int LC, int GC, int PC>
+struct TierB {
+  // shared layout, in ints:
+  //   key[S][HC] val[S][HC] disc[S][LC] scan[GC + 1] pbeg[PC] ppre[PC]
+  //   cand/owner as uint16 pairs [GC]  psrc/pidx as uint8 pairs [PC] (PC/2 ints)
+  //   per-source scalars [16][S], block-scan scratch [TB_WARPS + 8]
+  static constexpr int WORDS = 2 * S * HC + S * LC + (GC + 4) + 2 * PC + GC + PC / 2 +
+                               16 * S + TB_WARPS + 8;
+  static constexpr size_t BYTES = sizeof(int) * (size_t)((WORDS + 3) & ~3);
+  static_assert(HC <= 65535 && PC <= 65535 && S <= 255 && LC <= 255, "packed index widths");
+};
+
+// 64-bit remainder by a small divisor (1 <= d <= 4096): q = mulhi(x, M_d) with
+// M_d = ceil(2^64 / d) is floor(x / d) or one more (Granlund-Montgomery), so a
+// single conditional correction gives the exact x % d.
+__device__ unsigned long long g_magic[4097];
+
+__device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
+  if (d == 1) return 0;
+  const unsigned long long q = __umul64hi(x, g_magic[d]);
+  unsigned long long r = x - q * (unsigned long long)d;
+  if (r > x) r += (unsigned long long)d;  // q was one too large
+  return (int)r;
+}
+
+// block-wide exclusive scan of one int per thread (TB_THREADS threads)
+__device__ __forceinline__ int block_scan(int v, int* scratch, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int inc = warp_incl_scan(v);
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const int x = lane < TB_WARPS ? scratch[lane] : 0;
+    const int xi = warp_incl_scan(x);
+    if (lane < TB_WARPS) scratch[lane] = xi - x;
+    if (lane == TB_WARPS - 1) scratch[TB_WARPS] = xi;
+  }
+  __syncthreads();
+  const int r = scratch[warp] + inc - v;
+  *total = scratch[TB_WARPS];
+  __syncthreads();
+  return r;
+}
+
+template <int S, int HC, int LC, int GC, int PC>
+__global__ void __launch_bounds__(TB_THREADS)
+    pbfs_batch(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
+               unsigned long long seed, long long src_begin, long long nsrc,
+               int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
+               int* __restrict__ ovf_list, int* __restrict__ ovf_count,
+               unsigned long long* __restrict__ work) {
+  extern __shared__ __align__(16) int smem[];
+  int* const key = smem;                                   // [S][HC]
+  int* const val = key + S * HC;                           // [S][HC]
+  int* const disc = val + S * HC;                          // [S][LC]
+  int* const scan = disc + S * LC;                         // [GC + 1]
+  int* const pbeg = scan + GC + 4;                         // [PC] (keeps 8-byte alignment)
+  int* const ppre = pbeg + PC;                             // [PC]
+  unsigned short* const cand = reinterpret_cast<unsigned short*>(ppre + PC);   // [GC]
+  unsigned short* const owner = cand + GC;                                     // [GC]
+  unsigned char* const psrc = reinterpret_cast<unsigned char*>(owner + GC);    // [PC]
+  unsigned char* const pidx = psrc + PC;                                       // [PC]
+  int* const sc = reinterpret_cast<int*>(pidx + PC);
+  int* const s_src = sc;
+  int* const s_lb = sc + S;
+  int* const s_le = sc + 2 * S;
+  int* const s_cnt = sc + 3 * S;
+  int* const s_live = sc + 4 * S;  // 1 live, 0 done, 2 overflow
+  int* const s_pb = sc + 5 * S;    // first parent
+  int* const s_f = sc + 6 * S;     // frontier size
+  int* const s_tb = sc + 7 * S;    // first candidate slot
+  int* const s_T = sc + 8 * S;     // candidates this level
+  int* const s_nins = sc + 9 * S;  // ids in the hash
+  int* const s_nst = sc + 10 * S;  // new ids this level
+  int* const s_exp = sc + 11 * S;  // vertices expanded
+  unsigned long long* const s_scn = reinterpret_cast<unsigned long long*>(sc + 12 * S);
+  int* const scr = sc + 16 * S;    // block-scan scratch
+  const int tid = threadIdx.x;
+  unsigned long long w_scanned = 0, w_expanded = 0;
+  const long long nbatch = (nsrc + S - 1) / S;
+
+  for (long long bi = blockIdx.x; bi < nbatch; bi += gridDim.x) {
+    // ---- init
+    for (int i = tid; i < S * HC; i += TB_THREADS) {
+      key[i] = -1;
+      val[i] = INT_MAX;
+    }
+    __syncthreads();
+    if (tid < S) {
+      const long long item = bi * S + tid;
+      const int s = item < nsrc ? (int)(src_begin + item) : -1;
+      s_src[tid] = s;
+      s_lb[tid] = 0;
+      s_le[tid] = 1;
+      s_cnt[tid] = 0;
+      s_live[tid] = s >= 0 ? 1 : 0;
+      s_nins[tid] = 1;
+      s_exp[tid] = 0;
+      s_scn[tid] = 0ull;
+      if (s >= 0) {
+        disc[tid * LC] = s;
+        const unsigned h = hash_id(s) & (HC - 1);
+        key[tid * HC + h] = s;
+        val[tid * HC + h] = 0;
+      }
+    }
+    int depth = 0;
+    for (;;) {
+      __syncthreads();
+      // ---- 1: frontier sizes -> parent bases
+      int f = 0;
+      if (tid < S && s_live[tid] == 1) f = s_le[tid] - s_lb[tid];
+      int P;
+      const int pb = block_scan(f, scr, &P);
+      if (tid < S) {
+        if (f > 0 && pb + f > PC) {
+          s_live[tid] = 2;
+          f = 0;
+        }
+        s_pb[tid] = pb;
+        s_f[tid] = f;
+        for (int i = 0; i < f; i++) {
+          psrc[pb + i] = (unsigned char)tid;
+          pidx[pb + i] = (unsigned char)(s_lb[tid] + i);
+        }
+      }
+      if (P > PC) P = PC;
+      __syncthreads();
+      // ---- 2: parents (blocked: thread owns PPT consecutive parents)
+      constexpr int PPT = (PC + TB_THREADS - 1) / TB_THREADS;
+      int pd[PPT];
+      int dsum = 0;
+#pragma unroll
+      for (int u = 0; u < PPT; u++) {
+        const int p = tid * PPT + u;
+        pd[u] = 0;
+        if (p < P && s_live[psrc[p]] == 1) {
+          const int q = psrc[p];
+          const int v = disc[q * LC + pidx[p]];
+          const int b = __ldg(indptr + v);
+          pd[u] = __ldg(indptr + v + 1) - b;
+          pbeg[p] = b;
+        }
+        dsum += pd[u];
+      }
+      int G;
+      int run = block_scan(dsum, scr, &G);
+#pragma unroll
+      for (int u = 0; u < PPT; u++) {
+        const int p = tid * PPT + u;
+        if (p < P) ppre[p] = run;
+        run += pd[u];
+      }
+      __syncthreads();
+      // per-source candidate ranges + budget checks
+      if (tid < S) {
+        const int ff = s_f[tid];
+        int tb = 0, T = 0;
+        if (ff > 0 && s_live[tid] == 1) {
+          const int p0 = s_pb[tid];
+          tb = ppre[p0];
+          const int last = p0 + ff - 1;
+          T = ppre[last] - tb + (last + 1 < P ? ppre[last + 1] - ppre[last] : G - ppre[last]);
+          s_exp[tid] += ff;
+          s_scn[tid] += (unsigned long long)T;
+          // the hash can never fill and the slots must fit the batch buffer
+          if (s_nins[tid] + T > HC - 1 || tb + T > GC) s_live[tid] = 2;
+        }
+        s_tb[tid] = tb;
+        s_T[tid] = T;
+      }
+      __syncthreads();
+      // owners of the candidate slots (thread per parent)
+#pragma unroll
+      for (int u = 0; u < PPT; u++) {
+        const int p = tid * PPT + u;
+        if (p < P && pd[u] > 0) {  // every slot gets an owner, even of overflowed sources
+          const int o = ppre[p];
+          const int e = o + pd[u] < GC ? o + pd[u] : GC;
+          for (int j = o; j < e; j++) owner[j] = (unsigned short)p;
+        }
+      }
+      // any live source?
+      int anyl = (tid < S && s_live[tid] == 1 && s_f[tid] > 0) ? 1 : 0;
+      anyl = __syncthreads_or(anyl);
+      if (!anyl) break;
+      depth++;
+      if (G > GC) G = GC;
+      const int tag = depth << 22;
+      // ---- 3: candidates -> hash
+      constexpr int U = 8;
+      for (int g0 = tid; g0 < G; g0 += TB_THREADS * U) {
+        int w[U], q[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int g = g0 + u * TB_THREADS;
+          w[u] = -1;
+          q[u] = -1;
+          if (g < G) {
+            const int p = owner[g];
+            const int qq = psrc[p];
+            if (s_live[qq] == 1) {
+              q[u] = qq;
+              w[u] = __ldg(indices + pbeg[p] + (g - ppre[p]));
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          if (q[u] >= 0) {
+            const int g = g0 + u * TB_THREADS;
+            int* kq = key + q[u] * HC;
+            unsigned h = hash_id(w[u]) & (HC - 1);
+            for (;;) {
+              const int old = atomicCAS(&kq[h], -1, w[u]);
+              if (old == -1) {
+                atomicAdd(&s_nins[q[u]], 1);
+                break;
+              }
+              if (old == w[u]) break;
+              h = (h + 1) & (HC - 1);
+            }
+            atomicMin(&val[q[u] * HC + h], tag | (g - s_tb[q[u]]));
+            cand[g] = (unsigned short)h;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- 4: first-occurrence flags -> block scan -> level lists
+      {
+        constexpr int PER = (GC + TB_THREADS - 1) / TB_THREADS;
+        unsigned fl = 0;  // bit u = candidate tid*PER+u is a first occurrence
+        int sum = 0;
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+          const int g = tid * PER + u;
+          if (g < G) {
+            const int qq = psrc[owner[g]];
+            if (s_live[qq] == 1 && val[qq * HC + cand[g]] == (tag | (g - s_tb[qq]))) {
+              fl |= 1u << u;
+              sum++;
+            }
+          }
+        }
+        int tot;
+        int run2 = block_scan(sum, scr, &tot);
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+          const int g = tid * PER + u;
+          if (g < GC) scan[g] = run2;
+          run2 += (fl >> u) & 1u;
+        }
+        if (tid == TB_THREADS - 1) scan[GC] = run2;
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+          if ((fl >> u) & 1u) {
+            const int g = tid * PER + u;
+            const int qq = psrc[owner[g]];
+            const int pos = s_le[qq] + scan[g] - scan[s_tb[qq]];
+            if (pos < LC) disc[qq * LC + pos] = key[qq * HC + cand[g]];
+          }
+        }
+        if (tid < S) s_nst[tid] = s_live[tid] == 1 ? scan[s_tb[tid] + s_T[tid]] - scan[s_tb[tid]] : 0;
+      }
+      __syncthreads();
+      // ---- 5: level finalize (thread per source)
+      if (tid < S && s_live[tid] == 1) {
+        const int q = tid;
+        const int le = s_le[q], nst = s_nst[q];
+        if (le + nst > LC) {
+          s_live[q] = 2;
+        } else if (nst == 0) {
+          s_live[q] = 0;
+        } else {
+          int* dq = disc + q * LC;
+          const int count = s_cnt[q];
+          const int remaining = K - count;
+          int take = nst;
+          if (nst > remaining) {
+            unsigned long long st = seed + SPLIT_GAMMA * (unsigned long long)(s_src[q] + 1);
+            for (int i = 0; i < remaining; i++) {
+              const int j = i + umod64_tab(splitmix_next(st), nst - i);
+              const int a = dq[le + i];
+              dq[le + i] = dq[le + j];
+              dq[le + j] = a;
+            }
+            take = remaining;
+          }
+          const long long row = (long long)s_src[q] - src_begin;
+          int* rn = out_nbr + row * K + count;
+          int* rd = out_dist + row * K + count;
+          if (depth == 1 && take == nst) {
+            for (int i = 0; i < take; i++) {  // level 1 in full: sorted adjacency of s
+              rn[i] = dq[le + i];
+              rd[i] = 1;
+            }
+          } else {
+            for (int i = 0; i < take; i++) {
+              const int v = dq[le + i];
+              int r = 0;
+              for (int x = 0; x < take; x++) r += dq[le + x] < v;
+              rn[r] = v;
+              rd[r] = depth;
+            }
+          }
+          s_cnt[q] = count + take;
+          s_lb[q] = le;
+          s_le[q] = le + nst;
+          if (count + take >= K) s_live[q] = 0;
+        }
+      }
+    }
+    // ---- batch outputs
+    __syncthreads();
+    if (tid < S && s_src[tid] >= 0) {
+      const int s = s_src[tid];
+      if (s_live[tid] == 2) {
+        ovf_list[atomicAdd(ovf_count, 1)] = s;
+      } else {
+        out_cnt[(long long)s - src_begin] = s_cnt[tid];
+        w_scanned += s_scn[tid];
+        w_expanded += (unsigned long long)s_exp[tid];
+      }
+    }
+  }
+  if (work) {
+    w_scanned = warp_sum(w_scanned);
+    w_expanded = warp_sum(w_expanded);
+    if ((tid & 31) == 0 && (w_scanned | w_expanded)) {
+      atomicAdd(work, w_scanned);
+      atomicAdd(work + 1, w_expanded);
+    }
+  }
+}
+
 // ------------------------------------------------------------- tier 0
 // Thread per source: each thread runs the reference's sequential FIFO BFS
 // (_kernels.py:76-131) for its own source; the 4M independent sources supply
@@ -888,6 +1246,38 @@ cudaError_t launch_thread(int sms, const int* indptr, const int* indices, int k,
   return cudaGetLastError();
 }
 
+constexpr int TBS = 32, TB_HC = 128, TB_LC = 96, TB_GC = 4096, TB_PC = 1024;
+
+cudaError_t launch_batch(int sms, const int* indptr, const int* indices, int k,
+                         unsigned long long seed, long long src_begin, long long nsrc,
+                         int* out_nbr, int* out_dist, int* out_count, int* ovf_out, int* ovf_cnt,
+                         unsigned long long* work, cudaStream_t st) {
+  static bool magic_ready = false;
+  if (!magic_ready) {
+    static unsigned long long host_magic[4097];
+    host_magic[0] = host_magic[1] = 0;
+    for (int d = 2; d <= 4096; d++) host_magic[d] = ~0ull / (unsigned long long)d + 1ull;
+    cudaError_t e = cudaMemcpyToSymbol(g_magic, host_magic, sizeof(host_magic));
+    if (e != cudaSuccess) return e;
+    magic_ready = true;
+  }
+  using LB = TierB<TBS, TB_HC, TB_LC, TB_GC, TB_PC>;
+  constexpr size_t smem = LB::BYTES;
+  auto kern = pbfs_batch<TBS, TB_HC, TB_LC, TB_GC, TB_PC>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TB_THREADS, smem);
+  if (e != cudaSuccess) return e;
+  long long blocks = (nsrc + TBS - 1) / TBS;
+  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1);
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, TB_THREADS, smem, st>>>(indptr, indices, k, seed, src_begin, nsrc,
+                                                    out_nbr, out_dist, out_count, ovf_out, ovf_cnt,
+                                                    work);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_lean(int sms, const int* indptr, const int* indices, int k,
                         unsigned long long seed, long long src_begin, long long nsrc,
                         int* out_nbr, int* out_dist, int* out_count, const PbfsWs& ws,
@@ -963,7 +1353,13 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
     // (tuning / comparison only; every mode is exact).
     static const char* env_mode = getenv("GU_PBFS_MODE");
     const char* mode = env_mode ? env_mode : "lean";
-    if (!strcmp(mode, "thread")) {
+    if (!strcmp(mode, "batch")) {
+      GU_CHECK(launch_batch(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
+                            out_count, ws.ovf0, ws.counts + 2, work, st));
+      GU_CHECK(launch_tier1a<32>(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0,
+                                 ws.counts + 2, out_nbr, out_dist, out_count, ws.ovfA,
+                                 ws.counts + 0, work, st));
+    } else if (!strcmp(mode, "thread")) {
       GU_CHECK(launch_thread(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
                              out_count, ws.ovf0, ws.counts + 2, work, st));
       GU_CHECK(launch_tier1a<32>(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0,

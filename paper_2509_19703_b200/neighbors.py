@@ -238,13 +238,18 @@ def all_pairs_bfs(g, chunk=1024):
 
 
 # --------------------------------------------------------------- records
-def _pack(n_rows, k, rec_nbr, rec_dist, rec_cnt, dev):
-    """Fixed-stride records -> (indptr int64, dst int32, dist int32) on device."""
+def _pack(n_rows, k, rec_nbr, rec_dist, rec_cnt, dev, host_indptr=None):
+    """Fixed-stride records -> (indptr int64, dst int32, dist int32) on device.
+
+    When every row is full the records already are the packed CSR and the
+    indptr is k * arange (also handed back on the host through
+    ``host_indptr``, a dict, so it never crosses the link)."""
     indptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
     total_max = n_rows * k
     if total_max and bool((rec_cnt == k).all()):
-        # every row full: the records already are the packed CSR
         torch.arange(0, (n_rows + 1) * k, k, dtype=torch.int64, device=dev, out=indptr)
+        if host_indptr is not None:
+            host_indptr["indptr"] = np.arange(0, (n_rows + 1) * k, k, dtype=np.int64)
         return indptr, rec_nbr.reshape(-1)[:total_max], rec_dist.reshape(-1)[:total_max]
     ws = workspace(_lib.load().gu_pack_records_workspace_size(n_rows), dev)
     dst = torch.empty(max(total_max, 1), dtype=torch.int32, device=dev)
@@ -329,10 +334,11 @@ def partial_bfs(g, k, seed=0):
     nbr, dist, cnt = partial_bfs_records(csr, k_eff, seed, 0, n)
     short = int((cnt < k_eff).sum().item()) if n else 0
     _warn_short(short)
-    indptr, dst, dd = _pack(n, k_eff, nbr, dist, cnt, dev)
+    hp = {}
+    indptr, dst, dd = _pack(n, k_eff, nbr, dist, cnt, dev, hp)
     devd = dict(indptr=indptr, nbr=dst, dist=dd)
-    dset = SparseDistanceSet(n=n, full=False, _dev=devd)
-    knn = DirectedKnn(n=n, k=k, _dev=dict(indptr=indptr, dst=dst, dist=dd))
+    dset = SparseDistanceSet(n=n, full=False, indptr=hp.get("indptr"), _dev=devd)
+    knn = DirectedKnn(n=n, k=k, indptr=hp.get("indptr"), _dev=dict(indptr=indptr, dst=dst, dist=dd))
     return dset, knn
 
 
@@ -359,8 +365,9 @@ def knn_from_full_distances(dist_set, k, seed=0):
         nbr, dist, cnt = _knn_from_matrix(np.asarray(dist_set.matrix), k, seed, dev)
     short = int((cnt < k).sum().item()) if n else 0
     _warn_short(short)
-    indptr, dst, dd = _pack(n, k, nbr, dist, cnt, dev)
-    return DirectedKnn(n=n, k=k, _dev=dict(indptr=indptr, dst=dst, dist=dd))
+    hp = {}
+    indptr, dst, dd = _pack(n, k, nbr, dist, cnt, dev, hp)
+    return DirectedKnn(n=n, k=k, indptr=hp.get("indptr"), _dev=dict(indptr=indptr, dst=dst, dist=dd))
 
 
 def _knn_from_matrix(matrix, k, seed, dev, chunk_bytes=256 << 20):
