@@ -299,6 +299,7 @@ template <int CAP, int PCAP, int TCAP, int WARPS, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     pbfs_warp(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
               unsigned long long seed, long long src_begin, long long nsrc,
+              const int* __restrict__ list, const int* __restrict__ list_count,
               int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
               int* __restrict__ ovf_list, int* __restrict__ ovf_count,
               unsigned long long* __restrict__ work) {
@@ -326,9 +327,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     }
   };
 
-  for (long long item = (long long)blockIdx.x * WARPS + warp; item < nsrc;
-       item += (long long)gridDim.x * WARPS) {
-    const int s = (int)(src_begin + item);
+  const long long total = list ? (long long)(*list_count) : nsrc;
+  for (long long it = (long long)blockIdx.x * WARPS + warp; it < total;
+       it += (long long)gridDim.x * WARPS) {
+    const int s = list ? list[it] : (int)(src_begin + it);
+    const long long item = (long long)s - src_begin;  // output row
     int* const rn = out_nbr + item * K;
     int* const rd = out_dist + item * K;
     {
@@ -511,6 +514,214 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   }
 }
 
+// ---------------------------------------------------------- tier F (fast)
+// The dominant shape of a k-ball on the BASELINE graphs: level 1 (the sorted
+// adjacency of s, <= 32 ids) and level 2 crossing the budget.  Everything is
+// kept in registers: lane i holds parent i of level 2 (= the i-th neighbour of
+// s); zero-degree parents are compacted away by ballot; the parent of a
+// flattened index t is the number of adjacency starts <= t inside the chunk
+// (__reduce_or_sync of per-parent bits) plus the starts of earlier chunks,
+// fetched by shuffle; the next chunk's loads are issued before the current
+// chunk's hash work.  Sources of any other shape (deg(s) > 32, a level 2 that
+// does not reach k, a ball above the budget) go to the generic tiers.
+constexpr int TF_CAP2 = 160;  // level-2 ids kept per source
+
+__device__ unsigned long long g_magic[4097];
+
+// 64-bit remainder by a small divisor (1 <= d <= 4096): q = mulhi(x, M_d) with
+// M_d = ceil(2^64 / d) is floor(x / d) or one more (Granlund-Montgomery), so a
+// single conditional correction gives the exact x % d.
+__device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
+  if (d == 1) return 0;
+  const unsigned long long q = __umul64hi(x, g_magic[d]);
+  unsigned long long r = x - q * (unsigned long long)d;
+  if (r > x) r += (unsigned long long)d;  // q was one too large
+  return (int)r;
+}
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    pbfs_fast(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
+              unsigned long long seed, long long src_begin, long long nsrc,
+              int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
+              int* __restrict__ ovf_list, int* __restrict__ ovf_count,
+              unsigned long long* __restrict__ work) {
+  constexpr int HC = 512;
+  __shared__ __align__(16) int sm_hash[WARPS][HC];
+  __shared__ int sm_list[WARPS][TF_CAP2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
+  int* const hkey = sm_hash[warp];
+  int* const lst = sm_list[warp];
+  unsigned long long w_scanned = 0, w_expanded = 0;
+  auto claim = [&](int w) -> bool {
+    unsigned h = hash_id(w) & (HC - 1);
+    for (;;) {
+      const int old = atomicCAS(&hkey[h], -1, w);
+      if (old == -1) return true;
+      if (old == w) return false;
+      h = (h + 1) & (HC - 1);
+    }
+  };
+  for (long long item = (long long)blockIdx.x * WARPS + warp; item < nsrc;
+       item += (long long)gridDim.x * WARPS) {
+    const int s = (int)(src_begin + item);
+    int* const rn = out_nbr + item * K;
+    int* const rd = out_dist + item * K;
+    const int b0 = __ldg(indptr + s);
+    const int T0 = __ldg(indptr + s + 1) - b0;
+    if (T0 > 32) {
+      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+      continue;
+    }
+#pragma unroll
+    for (int i = 0; i < HC / 128; i++) reinterpret_cast<int4*>(hkey)[lane + 32 * i] = make_int4(-1, -1, -1, -1);
+    const int w1 = lane < T0 ? __ldg(indices + b0 + lane) : -1;
+    // level-2 parent ranges issued right away (needed unless level 1 crosses)
+    int pb = 0, pd = 0;
+    if (T0 < K && lane < T0) {
+      pb = __ldg(indptr + w1);
+      pd = __ldg(indptr + w1 + 1) - pb;
+    }
+    __syncwarp();
+    if (lane == 0) hkey[hash_id(s) & (HC - 1)] = s;
+    __syncwarp();
+    if (lane < T0) claim(w1);
+    const unsigned long long fy_base = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
+    if (T0 >= K) {
+      // ---- level 1 reaches the budget: sorted adjacency, or a random subset
+      if (T0 == K) {
+        if (lane < K) {
+          rn[lane] = w1;
+          rd[lane] = 1;
+        }
+      } else {
+        if (lane < T0) lst[lane] = w1;
+        int j = 0;
+        if (lane < K) j = lane + umod64_tab(splitmix_at(fy_base, lane), T0 - lane);
+        __syncwarp();
+        for (int i = 0; i < K; i++) {
+          const int ji = __shfl_sync(FULL, j, i);
+          if (lane == 0) {
+            const int a = lst[i];
+            lst[i] = lst[ji];
+            lst[ji] = a;
+          }
+        }
+        __syncwarp();
+        if (lane < K) {
+          const int v = lst[lane];
+          int r = 0;
+          for (int q = 0; q < K; q++) r += lst[q] < v;
+          rn[r] = v;
+          rd[r] = 1;
+        }
+      }
+      if (lane == 0) out_cnt[item] = T0 < K ? T0 : K;
+      w_scanned += T0;
+      w_expanded += 1;
+      __syncwarp();
+      continue;
+    }
+    if (T0 == 0) {  // isolated vertex: nothing reachable
+      if (lane == 0) out_cnt[item] = 0;
+      w_expanded += 1;
+      continue;
+    }
+    // ---- level 1 in full
+    if (lane < T0) {
+      rn[lane] = w1;
+      rd[lane] = 1;
+    }
+    // ---- level 2: compact non-empty parents, prefix of their degrees
+    const unsigned nem = __ballot_sync(FULL, pd > 0);
+    const int nne = __popc(nem);
+    // compaction through the (still unused) list buffer: lane r gets the r-th
+    // non-empty parent
+    if (pd > 0) {
+      const int r = __popc(nem & lt);
+      lst[r] = pb;
+      lst[32 + r] = pd;
+    }
+    __syncwarp();
+    const int cb = lane < nne ? lst[lane] : 0;
+    const int cdv = lane < nne ? lst[32 + lane] : 0;
+    __syncwarp();
+    const int inc = warp_incl_scan(cdv);
+    const int cpre = inc - cdv;
+    const int T = __shfl_sync(FULL, inc, 31);
+    int nst = 0, pcount = 0;
+    // candidate of chunk t0 for this lane (parent count of earlier chunks: pc)
+    auto load_chunk = [&](int t0, int pc, int& w, unsigned& m) {
+      const bool mine = lane < nne && cpre >= t0 && cpre < t0 + 32;
+      m = __reduce_or_sync(FULL, mine ? 1u << (cpre - t0) : 0u);
+      const int p = pc + __popc(m & le_mask) - 1;
+      const int ppre = __shfl_sync(FULL, cpre, p & 31);
+      const int pbb = __shfl_sync(FULL, cb, p & 31);
+      w = t0 + lane < T ? __ldg(indices + pbb + (t0 + lane - ppre)) : -1;
+    };
+    int w;
+    unsigned m;
+    load_chunk(0, 0, w, m);
+    bool ovf = false;
+    for (int t0 = 0; t0 < T; t0 += 32) {
+      pcount += __popc(m);
+      int wn = -1;
+      unsigned mn = 0;
+      if (t0 + 32 < T) load_chunk(t0 + 32, pcount, wn, mn);
+      const unsigned grp = __match_any_sync(FULL, w);
+      const bool isnew = t0 + lane < T && lane == __ffs(grp) - 1 && claim(w);
+      const unsigned bal = __ballot_sync(FULL, isnew);
+      if (isnew) {
+        const int pos = nst + __popc(bal & lt);
+        if (pos < TF_CAP2) lst[pos] = w;
+      }
+      nst += __popc(bal);
+      w = wn;
+      m = mn;
+      if (nst > TF_CAP2 || nst + T0 + 1 > (HC * 3) / 4) {  // ball above the budget
+        ovf = true;
+        break;
+      }
+    }
+    const int remaining = K - T0;
+    if (ovf || nst < remaining) {  // level 2 does not reach k (or too big): generic path
+      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    if (nst > remaining) {
+      int j = 0;
+      if (lane < remaining) j = lane + umod64_tab(splitmix_at(fy_base, lane), nst - lane);
+      for (int i = 0; i < remaining; i++) {
+        const int ji = __shfl_sync(FULL, j, i);
+        if (lane == 0) {
+          const int a = lst[i];
+          lst[i] = lst[ji];
+          lst[ji] = a;
+        }
+      }
+      __syncwarp();
+    }
+    if (lane < remaining) {
+      const int v = lst[lane];
+      int r = 0;
+      for (int q = 0; q < remaining; q++) r += lst[q] < v;
+      rn[T0 + r] = v;
+      rd[T0 + r] = 2;
+    }
+    if (lane == 0) out_cnt[item] = K;
+    w_scanned += (unsigned long long)(T0 + T);
+    w_expanded += (unsigned long long)(1 + T0);
+    __syncwarp();
+  }
+  if (work && lane == 0) {
+    atomicAdd(work, w_scanned);
+    atomicAdd(work + 1, w_expanded);
+  }
+}
+
 // ------------------------------------------------------------- tier B
 // CTA batch: S sources per CTA processed level-synchronously; every phase is
 // flattened across the batch so that threads, not warps, carry the per-item
@@ -544,19 +755,6 @@ struct TierB {
   static constexpr size_t BYTES = sizeof(int) * (size_t)((WORDS + 3) & ~3);
   static_assert(HC <= 65535 && PC <= 65535 && S <= 255 && LC <= 255, "packed index widths");
 };
-
-// 64-bit remainder by a small divisor (1 <= d <= 4096): q = mulhi(x, M_d) with
-// M_d = ceil(2^64 / d) is floor(x / d) or one more (Granlund-Montgomery), so a
-// single conditional correction gives the exact x % d.
-__device__ unsigned long long g_magic[4097];
-
-__device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
-  if (d == 1) return 0;
-  const unsigned long long q = __umul64hi(x, g_magic[d]);
-  unsigned long long r = x - q * (unsigned long long)d;
-  if (r > x) r += (unsigned long long)d;  // q was one too large
-  return (int)r;
-}
 
 // block-wide exclusive scan of one int per thread (TB_THREADS threads)
 __device__ __forceinline__ int block_scan(int v, int* scratch, int* total) {
@@ -1248,18 +1446,48 @@ cudaError_t launch_thread(int sms, const int* indptr, const int* indices, int k,
 
 constexpr int TBS = 32, TB_HC = 128, TB_LC = 96, TB_GC = 4096, TB_PC = 1024;
 
+// M_d = ceil(2^64 / d) for the table remainder (uploaded once per device)
+cudaError_t ensure_magic() {
+  static int ready_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (ready_dev == dev) return cudaSuccess;
+  static unsigned long long host_magic[4097];
+  host_magic[0] = host_magic[1] = 0;
+  for (int d = 2; d <= 4096; d++) host_magic[d] = ~0ull / (unsigned long long)d + 1ull;
+  cudaError_t e = cudaMemcpyToSymbol(g_magic, host_magic, sizeof(host_magic));
+  if (e == cudaSuccess) ready_dev = dev;
+  return e;
+}
+
+constexpr int TF_WARPS = 8;
+
+cudaError_t launch_fast(int sms, const int* indptr, const int* indices, int k,
+                        unsigned long long seed, long long src_begin, long long nsrc,
+                        int* out_nbr, int* out_dist, int* out_count, int* ovf_out, int* ovf_cnt,
+                        unsigned long long* work, cudaStream_t st) {
+  cudaError_t e = ensure_magic();
+  if (e != cudaSuccess) return e;
+  auto kern = pbfs_fast<TF_WARPS>;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TF_WARPS * 32, 0);
+  if (e != cudaSuccess) return e;
+  long long blocks = (nsrc + TF_WARPS - 1) / TF_WARPS;
+  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * 8;
+  if (blocks > cap) blocks = cap;
+  kern<<<(unsigned)blocks, TF_WARPS * 32, 0, st>>>(indptr, indices, k, seed, src_begin, nsrc,
+                                                   out_nbr, out_dist, out_count, ovf_out, ovf_cnt,
+                                                   work);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_batch(int sms, const int* indptr, const int* indices, int k,
                          unsigned long long seed, long long src_begin, long long nsrc,
                          int* out_nbr, int* out_dist, int* out_count, int* ovf_out, int* ovf_cnt,
                          unsigned long long* work, cudaStream_t st) {
-  static bool magic_ready = false;
-  if (!magic_ready) {
-    static unsigned long long host_magic[4097];
-    host_magic[0] = host_magic[1] = 0;
-    for (int d = 2; d <= 4096; d++) host_magic[d] = ~0ull / (unsigned long long)d + 1ull;
-    cudaError_t e = cudaMemcpyToSymbol(g_magic, host_magic, sizeof(host_magic));
-    if (e != cudaSuccess) return e;
-    magic_ready = true;
+  {
+    cudaError_t e0 = ensure_magic();
+    if (e0 != cudaSuccess) return e0;
   }
   using LB = TierB<TBS, TB_HC, TB_LC, TB_GC, TB_PC>;
   constexpr size_t smem = LB::BYTES;
@@ -1280,8 +1508,9 @@ cudaError_t launch_batch(int sms, const int* indptr, const int* indices, int k,
 
 cudaError_t launch_lean(int sms, const int* indptr, const int* indices, int k,
                         unsigned long long seed, long long src_begin, long long nsrc,
-                        int* out_nbr, int* out_dist, int* out_count, const PbfsWs& ws,
-                        unsigned long long* work, cudaStream_t st) {
+                        const int* list, const int* list_count, int* out_nbr, int* out_dist,
+                        int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
+                        cudaStream_t st) {
   using LA = Tier1<32, T1A_CAP, T1A_PCAP, T1A_TCAP>;
   constexpr int W = 8;
   constexpr size_t smem = sizeof(int) * LA::WORDS * W;
@@ -1292,10 +1521,11 @@ cudaError_t launch_lean(int sms, const int* indptr, const int* indices, int k,
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   if (e != cudaSuccess) return e;
   long long blocks = (nsrc + W - 1) / W;
-  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * 8;
+  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * (list ? 1 : 8);
   if (blocks > cap) blocks = cap;
-  kern<<<(unsigned)blocks, W * 32, smem, st>>>(indptr, indices, k, seed, src_begin, nsrc, out_nbr,
-                                                out_dist, out_count, ws.ovfA, ws.counts + 0, work);
+  kern<<<(unsigned)blocks, W * 32, smem, st>>>(indptr, indices, k, seed, src_begin, nsrc, list,
+                                                list_count, out_nbr, out_dist, out_count, ovf_out,
+                                                ovf_cnt, work);
   return cudaGetLastError();
 }
 
@@ -1352,8 +1582,13 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
     // GU_PBFS_MODE = lean (default) | thread | g16 | g32 selects the first tier
     // (tuning / comparison only; every mode is exact).
     static const char* env_mode = getenv("GU_PBFS_MODE");
-    const char* mode = env_mode ? env_mode : "lean";
-    if (!strcmp(mode, "batch")) {
+    const char* mode = env_mode ? env_mode : "fast";
+    if (!strcmp(mode, "fast")) {
+      GU_CHECK(launch_fast(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
+                           out_count, ws.ovf0, ws.counts + 2, work, st));
+      GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0, ws.counts + 2,
+                           out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
+    } else if (!strcmp(mode, "batch")) {
       GU_CHECK(launch_batch(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
                             out_count, ws.ovf0, ws.counts + 2, work, st));
       GU_CHECK(launch_tier1a<32>(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0,
@@ -1366,8 +1601,8 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
                                  ws.counts + 2, out_nbr, out_dist, out_count, ws.ovfA,
                                  ws.counts + 0, work, st));
     } else if (!strcmp(mode, "lean")) {
-      GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
-                           out_count, ws, work, st));
+      GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
+                           out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
     } else if (k <= 16 && !strcmp(mode, "g16")) {
       GU_CHECK(launch_tier1a<16>(sms, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
                                  out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
