@@ -31,6 +31,7 @@ namespace gu {
 namespace {
 
 constexpr int TILE = 1024;
+constexpr int SGD_NEG_BLOCK = 5;  // negatives handled in lockstep per block
 
 // Feistel bijection on [0, 2^bits) with cycle walking into [0, m)
 __device__ __host__ __forceinline__ unsigned long long mix64(unsigned long long x) {
@@ -139,61 +140,94 @@ __global__ void __launch_bounds__(256)
         if (!isfinite(xv.x - gx) || !isfinite(xv.y - gy)) bad = true;
       }
     }
-    // repulsions: candidates from Philox(position, epoch, draw-block)
-    unsigned rnd[4];
-    int have = 0, blk = 0;
-    for (int q = 0; q < n_neg; q++) {
-      int c = -1;
-      for (int t = 0; t < 8; t++) {
-        if (have == 0) {
-          uint4 r4 = Philox::gen(make_uint4((unsigned)p, (unsigned)(p >> 32), (unsigned)epoch,
-                                            (unsigned)blk++),
-                                 key);
-          rnd[0] = r4.x;
-          rnd[1] = r4.y;
-          rnd[2] = r4.z;
-          rnd[3] = r4.w;
-          have = 4;
-        }
-        const int cand = (int)__umulhi(rnd[--have], (unsigned)n);
-        if (cand == u) continue;
-        if (!is_neighbor(nip, nix, u, cand)) {
-          c = cand;
-          break;
-        }
+    // repulsions.  Draw d of slot q comes from Philox(p, epoch, q, d) (four
+    // 32-bit draws per call: one candidate try or one theta each).  The
+    // first tries of all slots are known up front, so their neighbour tests
+    // run as lockstep binary searches over the head's sorted row (bounds
+    // loaded once), and their coordinate loads are issued together; a
+    // rejected try (c == u or a neighbour: probability ~deg/n) takes the
+    // sequential retry path.  The repulsion math itself stays sequential in
+    // slot order on the register copy of x_u, as in the reference sweep.
+    const int rb = __ldg(nip + u), re = __ldg(nip + u + 1);
+    for (int q0 = 0; q0 < n_neg; q0 += SGD_NEG_BLOCK) {
+      const int nq = min(SGD_NEG_BLOCK, n_neg - q0);
+      int cand[SGD_NEG_BLOCK], lo[SGD_NEG_BLOCK], len[SGD_NEG_BLOCK];
+      uint4 r4[SGD_NEG_BLOCK];
+#pragma unroll
+      for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+        r4[q] = Philox::gen(make_uint4((unsigned)p, (unsigned)(p >> 32), (unsigned)epoch,
+                                       (unsigned)((q0 + q) << 8)), key);
+        cand[q] = (int)__umulhi(r4[q].x, (unsigned)n);
+        lo[q] = rb;
+        len[q] = q < nq ? re - rb : 0;
       }
-      if (c < 0) continue;
-      const float2 xc = xy[c];
-      const float dx = xu.x - xc.x, dy = xu.y - xc.y;
-      const float d2 = dx * dx + dy * dy;
-      float gx, gy;
-      if (d2 > 0.f) {
-        const float g = 2.0f * b / ((0.001f + d2) * (a * __powf(d2, b) + 1.0f));
-        gx = clip4(g * dx);
-        gy = clip4(g * dy);
-      } else {
-        if (have == 0) {
-          uint4 r4 = Philox::gen(make_uint4((unsigned)p, (unsigned)(p >> 32), (unsigned)epoch,
-                                            (unsigned)blk++),
-                                 key);
-          rnd[0] = r4.x;
-          rnd[1] = r4.y;
-          rnd[2] = r4.z;
-          rnd[3] = r4.w;
-          have = 4;
+      // lockstep lower_bound of every candidate in the row
+      for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+          if (len[q] > 0) {
+            const int half = len[q] >> 1;
+            const int x = __ldg(nix + lo[q] + half);
+            if (x < cand[q]) {
+              lo[q] += half + 1;
+              len[q] -= half + 1;
+            } else {
+              len[q] = half;
+            }
+            any = true;
+          }
         }
-        const float th = (float)rnd[--have] * (6.283185307179586f / 4294967296.0f);
-        float sn, cs;
-        __sincosf(th, &sn, &cs);
-        gx = 4.0f * cs;
-        gy = 4.0f * sn;
+        if (!any) break;
       }
-      gx *= lr;
-      gy *= lr;
-      dux += gx;
-      duy += gy;
-      xu.x += gx;
-      xu.y += gy;
+      float2 xc[SGD_NEG_BLOCK];
+      bool ok[SGD_NEG_BLOCK];
+#pragma unroll
+      for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+        ok[q] = q < nq && cand[q] != u && !(lo[q] < re && __ldg(nix + lo[q]) == cand[q]);
+        if (ok[q]) xc[q] = xy[cand[q]];
+      }
+#pragma unroll
+      for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+        if (q >= nq) break;
+        int c = ok[q] ? cand[q] : -1;
+        unsigned spare = r4[q].y;  // theta draw of this slot
+        if (!ok[q]) {
+          // retries 2..8 of this slot (rare)
+          for (int t = 1; t < 8; t++) {
+            const uint4 rr = Philox::gen(make_uint4((unsigned)p, (unsigned)(p >> 32),
+                                                    (unsigned)epoch,
+                                                    (unsigned)(((q0 + q) << 8) | t)), key);
+            const int cc = (int)__umulhi(rr.x, (unsigned)n);
+            if (cc == u || is_neighbor(nip, nix, u, cc)) continue;
+            c = cc;
+            spare = rr.y;
+            break;
+          }
+          if (c < 0) continue;
+          xc[q] = xy[c];
+        }
+        const float dx = xu.x - xc[q].x, dy = xu.y - xc[q].y;
+        const float d2 = dx * dx + dy * dy;
+        float gx, gy;
+        if (d2 > 0.f) {
+          const float g = 2.0f * b / ((0.001f + d2) * (a * __powf(d2, b) + 1.0f));
+          gx = clip4(g * dx);
+          gy = clip4(g * dy);
+        } else {
+          const float th = (float)spare * (6.283185307179586f / 4294967296.0f);
+          float sn, cs;
+          __sincosf(th, &sn, &cs);
+          gx = 4.0f * cs;
+          gy = 4.0f * sn;
+        }
+        gx *= lr;
+        gy *= lr;
+        dux += gx;
+        duy += gy;
+        xu.x += gx;
+        xu.y += gy;
+      }
     }
     if (dux != 0.f || duy != 0.f) atomicAdd(&xy[u], make_float2(dux, duy));
     if (!isfinite(xu.x) || !isfinite(xu.y)) bad = true;
