@@ -68,32 +68,48 @@ def _profile_traffic(kernel):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML every ~2 ms during
+    the timed region (nvidia-smi is too slow for a ~20 ms region); falls back
+    to nvidia-smi when NVML is unavailable."""
 
-    def __init__(self, index=0):
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index=0, period=0.002):
         self.index = index
+        self.period = period
         self.samples = []
         self._stop = threading.Event()
         self._th = None
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, mx, rs))
+                self._stop.wait(self.period)
+            pynvml.nvmlShutdown()
+        except Exception:
+            q = "clocks.sm,clocks.max.sm"
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip().split(",")
+                    self.samples.append((float(out[0]), float(out[1]), 0))
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
 
     def __enter__(self):
         self._th = threading.Thread(target=self._run, daemon=True)
         self._th.start()
+        time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
@@ -103,18 +119,14 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            for nm, v in zip(names, s[3:7]):
-                if v.strip().lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"],
+                    "samples": 0}
+        sm = [float(x[0]) for x in self.samples]
+        reasons = sorted({name for _, _, r in self.samples for name, bit in self.REASONS.items()
+                          if int(r) & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(float(x[1]) for x in self.samples),
+                "sm_min_mhz": min(sm), "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml"}
 
 
 def _dist_env():
