@@ -123,10 +123,26 @@ def to_device(a, dtype, device):
         src = torch.from_numpy(a)
     if a.nbytes < _PIN_THRESHOLD:
         return src.to(device)
-    staging = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
-    staging.copy_(src)
-    dev = torch.empty(src.shape, dtype=src.dtype, device=device)
-    dev.copy_(staging, non_blocking=True)
-    torch.cuda.current_stream(device).synchronize()
-    return dev
+    # chunked, double-buffered: the host copy of chunk i+1 overlaps the DMA of i
+    flat = src.reshape(-1)
+    dev = torch.empty(flat.shape, dtype=src.dtype, device=device)
+    chunk = max(1, _UPLOAD_CHUNK_BYTES // src.element_size())
+    bufs = [torch.empty(min(chunk, flat.numel()), dtype=src.dtype, pin_memory=True)
+            for _ in range(2)]
+    evs = [None, None]
+    stream = torch.cuda.current_stream(device)
+    for i, lo in enumerate(range(0, flat.numel(), chunk)):
+        hi = min(lo + chunk, flat.numel())
+        b = i & 1
+        if evs[b] is not None:
+            evs[b].synchronize()  # the DMA that last read this buffer is done
+        bufs[b][: hi - lo].copy_(flat[lo:hi])
+        dev[lo:hi].copy_(bufs[b][: hi - lo], non_blocking=True)
+        evs[b] = torch.cuda.Event()
+        evs[b].record(stream)
+    stream.synchronize()
+    return dev.reshape(src.shape)
+
+
+_UPLOAD_CHUNK_BYTES = 32 << 20
 

@@ -46,9 +46,16 @@ class _LazyArrays:
     def _init_lazy(self, host, dev):
         object.__setattr__(self, "_host", dict(host))
         object.__setattr__(self, "_dev", dict(dev))
+        object.__setattr__(self, "_pending", {})  # name -> (pinned tensor, event)
 
     def _get_host(self, name):
         h = self._host.get(name)
+        if h is None and name in self._pending:
+            pinned, ev = self._pending.pop(name)
+            ev.synchronize()
+            h = pinned.numpy()
+            h.setflags(write=False)
+            self._host[name] = h
         if h is None:
             d = self._dev.get(name)
             if d is None:
@@ -238,18 +245,17 @@ def all_pairs_bfs(g, chunk=1024):
 
 
 # --------------------------------------------------------------- records
-def _pack(n_rows, k, rec_nbr, rec_dist, rec_cnt, dev, host_indptr=None):
+def _pack(n_rows, k, rec_nbr, rec_dist, rec_cnt, dev, full=None):
     """Fixed-stride records -> (indptr int64, dst int32, dist int32) on device.
 
-    When every row is full the records already are the packed CSR and the
-    indptr is k * arange (also handed back on the host through
-    ``host_indptr``, a dict, so it never crosses the link)."""
+    When every row is full (``full``; computed if None) the records already
+    are the packed CSR and the indptr is k * arange."""
     indptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
     total_max = n_rows * k
-    if total_max and bool((rec_cnt == k).all()):
+    if full is None:
+        full = bool(total_max) and bool((rec_cnt == k).all())
+    if total_max and full:
         torch.arange(0, (n_rows + 1) * k, k, dtype=torch.int64, device=dev, out=indptr)
-        if host_indptr is not None:
-            host_indptr["indptr"] = np.arange(0, (n_rows + 1) * k, k, dtype=np.int64)
         return indptr, rec_nbr.reshape(-1)[:total_max], rec_dist.reshape(-1)[:total_max]
     ws = workspace(_lib.load().gu_pack_records_workspace_size(n_rows), dev)
     dst = torch.empty(max(total_max, 1), dtype=torch.int32, device=dev)
@@ -270,23 +276,32 @@ def _warn_short(short, stacklevel=3):
         )
 
 
-def partial_bfs_records(csr, k_eff, seed, src_begin, src_end, work=None, tier2_warps=None):
+def _tier2_warps(n):
+    return int(max(1, min(148 * 8, _TIER2_BUDGET_BYTES // max(8 * n, 1))))
+
+
+def partial_bfs_records(csr, k_eff, seed, src_begin, src_end, work=None, tier2_warps=None,
+                        out=None, ws=None):
     """Raw fixed-stride records of sources [src_begin, src_end) (device).
 
-    Returns (nbr int32[ns, k], dist int32[ns, k], count int32[ns]).  ``work``:
-    optional int64[2] device tensor receiving (entries scanned, vertices
-    expanded)."""
+    Returns (nbr int32[ns, k], dist int32[ns, k], count int32[ns]), written
+    into ``out`` when given.  ``work``: optional int64[2] device tensor
+    receiving (entries scanned, vertices expanded)."""
     dev = csr.device
     ns = src_end - src_begin
     kk = max(k_eff, 1)
-    nbr = torch.empty((ns, kk), dtype=torch.int32, device=dev)
-    dist = torch.empty((ns, kk), dtype=torch.int32, device=dev)
-    cnt = torch.empty(ns, dtype=torch.int32, device=dev)
+    if out is None:
+        nbr = torch.empty((ns, kk), dtype=torch.int32, device=dev)
+        dist = torch.empty((ns, kk), dtype=torch.int32, device=dev)
+        cnt = torch.empty(ns, dtype=torch.int32, device=dev)
+    else:
+        nbr, dist, cnt = out
     n = csr.n
     if tier2_warps is None:
-        tier2_warps = int(max(1, min(148 * 8, _TIER2_BUDGET_BYTES // max(8 * n, 1))))
+        tier2_warps = _tier2_warps(n)
     lib = _lib.load()
-    ws = workspace(lib.gu_partial_bfs_workspace_size(n, ns, tier2_warps), dev)
+    if ws is None:
+        ws = workspace(lib.gu_partial_bfs_workspace_size(n, ns, tier2_warps), dev)
     _lib.call("gu_partial_bfs_knn", n, _lib.ptr(csr.indptr), _lib.ptr(csr.indices), k_eff,
               int(seed) & (2**64 - 1), src_begin, src_end, _lib.ptr(nbr), _lib.ptr(dist),
               _lib.ptr(cnt), _lib.ptr(work), _lib.ptr(ws), ws.numel(), tier2_warps,
@@ -324,6 +339,10 @@ def partial_bfs(g, k, seed=0):
     distance set together with the directed kNN edges it implies.  Vertices
     whose component holds fewer than k+1 vertices report everything
     reachable, with a warning.
+
+    The sources run in chunks; each chunk's rows are copied into pinned host
+    memory on a side stream while the next chunk computes, so the numpy
+    results (``knn.dst`` ...) are ready shortly after the kernel.
     """
     if k < 1:
         raise ValueError("k must be >= 1")
@@ -331,15 +350,60 @@ def partial_bfs(g, k, seed=0):
     n = int(g.n)
     k_eff = min(k, n - 1) if n > 1 else 0
     csr = device_csr(g, dev)
-    nbr, dist, cnt = partial_bfs_records(csr, k_eff, seed, 0, n)
+    kk = max(k_eff, 1)
+    nbr = torch.empty((n, kk), dtype=torch.int32, device=dev)
+    dist = torch.empty((n, kk), dtype=torch.int32, device=dev)
+    cnt = torch.empty(n, dtype=torch.int32, device=dev)
+    prefetch = _HostPrefetch(dev, n * kk, ("dst", "dist")) if n * kk * 8 >= (64 << 20) else None
+    nchunk = 4 if prefetch is not None else 1
+    bounds = [n * i // nchunk for i in range(nchunk + 1)]
+    tw = _tier2_warps(n)
+    ws = workspace(_lib.load().gu_partial_bfs_workspace_size(n, bounds[1] - bounds[0] + 1, tw), dev)
+    for c in range(nchunk):
+        b, e = bounds[c], bounds[c + 1]
+        partial_bfs_records(csr, k_eff, seed, b, e, tier2_warps=tw, out=(nbr[b:e], dist[b:e], cnt[b:e]),
+                            ws=ws)
+        if prefetch is not None:
+            prefetch.copy_rows(dict(dst=nbr, dist=dist), b * kk, e * kk)
     short = int((cnt < k_eff).sum().item()) if n else 0
     _warn_short(short)
-    hp = {}
-    indptr, dst, dd = _pack(n, k_eff, nbr, dist, cnt, dev, hp)
+    indptr, dst, dd = _pack(n, k_eff, nbr, dist, cnt, dev, full=(short == 0 and k_eff > 0))
+    host = {}
+    if prefetch is not None and short == 0:
+        host = prefetch.finish()  # rows are the packed arrays: host copies are valid
     devd = dict(indptr=indptr, nbr=dst, dist=dd)
-    dset = SparseDistanceSet(n=n, full=False, indptr=hp.get("indptr"), _dev=devd)
-    knn = DirectedKnn(n=n, k=k, indptr=hp.get("indptr"), _dev=dict(indptr=indptr, dst=dst, dist=dd))
+    dset = SparseDistanceSet(n=n, full=False, _dev=devd)
+    knn = DirectedKnn(n=n, k=k, _dev=dict(indptr=indptr, dst=dst, dist=dd))
+    for name, pend in host.items():
+        knn._pending[name] = pend
+        dset._pending["nbr" if name == "dst" else name] = pend
     return dset, knn
+
+
+class _HostPrefetch:
+    """Asynchronous device -> pinned-host copies of row ranges on a side
+    stream, ordered after the compute stream's work so far."""
+
+    _streams = {}
+
+    def __init__(self, dev, numel, names):
+        self.dev = dev
+        self.stream = self._streams.setdefault(str(dev), torch.cuda.Stream(device=dev))
+        self.host = {nm: torch.empty(numel, dtype=torch.int32, pin_memory=True) for nm in names}
+        self.done = None
+
+    def copy_rows(self, srcs, lo, hi):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(self.stream):
+            self.stream.wait_event(ev)
+            for nm, t in srcs.items():
+                self.host[nm][lo:hi].copy_(t.reshape(-1)[lo:hi], non_blocking=True)
+        self.done = torch.cuda.Event()
+        self.done.record(self.stream)
+
+    def finish(self):
+        return {nm: (h, self.done) for nm, h in self.host.items()}
 
 
 def knn_from_full_distances(dist_set, k, seed=0):
@@ -365,9 +429,8 @@ def knn_from_full_distances(dist_set, k, seed=0):
         nbr, dist, cnt = _knn_from_matrix(np.asarray(dist_set.matrix), k, seed, dev)
     short = int((cnt < k).sum().item()) if n else 0
     _warn_short(short)
-    hp = {}
-    indptr, dst, dd = _pack(n, k, nbr, dist, cnt, dev, hp)
-    return DirectedKnn(n=n, k=k, indptr=hp.get("indptr"), _dev=dict(indptr=indptr, dst=dst, dist=dd))
+    indptr, dst, dd = _pack(n, k, nbr, dist, cnt, dev, full=(short == 0))
+    return DirectedKnn(n=n, k=k, _dev=dict(indptr=indptr, dst=dst, dist=dd))
 
 
 def _knn_from_matrix(matrix, k, seed, dev, chunk_bytes=256 << 20):
