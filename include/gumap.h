@@ -127,8 +127,9 @@ int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* 
  * points), run as a Hogwild epoch over fp32 float2 coordinates.  The epoch
  * schedule (fresh order per epoch, or a sliding window of `window` edges over
  * one shuffled order) and the negatives come from Philox4x32-10 keyed by seed.
- * edges: int4 records {src, dst, float-bits(h), 0} in the caller's order;
- * gu_sgd_prepare_edges builds them shuffled. nbr CSR int32.
+ * edges: int4 records {src, dst, float-bits(h), (row start << 6) | degree or -1},
+ * built in a shuffled order by gu_sgd_prepare_edges (perm_out, nullable,
+ * receives the sym edge id of every record position).  nbr CSR int32.
  * Runs epochs [epoch_begin, epoch_end) of a t-epoch schedule,
  * lr_e = lr0 * (1 - e/t).  diverged (int32, device): atomicMin'd with the
  * first epoch that produced a non-finite coordinate (init to INT32_MAX).
@@ -136,8 +137,8 @@ int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* 
  * the GPU.  Hogwild stays statistically close to the sequential sweep only
  * while concurrency << n, so callers cap it for small graphs. */
 int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
-                         const double* sym_w, uint64_t seed, void* edges_int4,
-                         void* stream);
+                         const double* sym_w, const int32_t* nbr_indptr, uint64_t seed,
+                         void* edges_int4, int32_t* perm_out, void* stream);
 int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4,
                   const int32_t* nbr_indptr, const int32_t* nbr_indices, float a, float b,
                   float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,

@@ -73,14 +73,23 @@ struct Feistel {
   }
 };
 
+// Edge record {src, dst, float(h), row}: row = (start of src's neighbour row
+// << 6) | degree when both fit (start < 2^26, degree < 63), else -1 (the
+// kernel then reads nbr_indptr) -- the first rejection probe can then issue
+// straight after the coalesced record load.
 __global__ void prepare_edges_kernel(long long E, const int* __restrict__ src,
                                      const int* __restrict__ dst, const double* __restrict__ w,
-                                     unsigned long long key, int4* __restrict__ out) {
+                                     const int* __restrict__ nip, unsigned long long key,
+                                     int4* __restrict__ out, int* __restrict__ perm_out) {
   Feistel perm((unsigned long long)E, key);
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E;
        p += (long long)gridDim.x * blockDim.x) {
     const long long e = (long long)perm((unsigned long long)p);
-    out[p] = make_int4(src[e], dst[e], __float_as_int((float)w[e]), (int)e);
+    const int u = src[e];
+    const int rb = nip[u], deg = nip[u + 1] - rb;
+    const int row = (rb < (1 << 26) && deg < 63) ? ((rb << 6) | deg) : -1;
+    out[p] = make_int4(u, dst[e], __float_as_int((float)w[e]), row);
+    if (perm_out) perm_out[p] = (int)e;
   }
 }
 
@@ -148,7 +157,14 @@ __global__ void __launch_bounds__(256)
     // rejected try (c == u or a neighbour: probability ~deg/n) takes the
     // sequential retry path.  The repulsion math itself stays sequential in
     // slot order on the register copy of x_u, as in the reference sweep.
-    const int rb = __ldg(nip + u), re = __ldg(nip + u + 1);
+    int rb, re;
+    if (rec.w >= 0) {
+      rb = rec.w >> 6;
+      re = rb + (rec.w & 63);
+    } else {
+      rb = __ldg(nip + u);
+      re = __ldg(nip + u + 1);
+    }
     for (int q0 = 0; q0 < n_neg; q0 += SGD_NEG_BLOCK) {
       const int nq = min(SGD_NEG_BLOCK, n_neg - q0);
       int cand[SGD_NEG_BLOCK], lo[SGD_NEG_BLOCK], len[SGD_NEG_BLOCK];
@@ -275,15 +291,16 @@ unsigned block_for(long long max_threads) {
 using namespace gu;
 
 extern "C" int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
-                                    const double* sym_w, uint64_t seed, void* edges_int4,
-                                    void* stream) {
+                                    const double* sym_w, const int32_t* nbr_indptr, uint64_t seed,
+                                    void* edges_int4, int32_t* perm_out, void* stream) {
   if (E < 0 || E >= INT_MAX) {
     set_error("gu_sgd_prepare_edges: unsupported E=%lld", (long long)E);
     return GU_ERR_UNSUPPORTED;
   }
   if (E == 0) return GU_OK;
   prepare_edges_kernel<<<grid_for(E), 256, 0, (cudaStream_t)stream>>>(
-      E, sym_src, sym_dst, sym_w, mix64(seed ^ 0xED6E5ull), (int4*)edges_int4);
+      E, sym_src, sym_dst, sym_w, nbr_indptr, mix64(seed ^ 0xED6E5ull), (int4*)edges_int4,
+      perm_out);
   GU_CHECK_LAUNCH("prepare_edges_kernel");
   return GU_OK;
 }
