@@ -22,18 +22,29 @@ size_t scan_workspace(long long nrows);
 
 namespace {
 
+// thread per kNN entry (coalesced writes); the row of entry i is found by a
+// binary search on indptr, or directly as i / kfix when every row holds kfix
 __global__ void build_keys(long long n, long long nrows, const long long* __restrict__ indptr,
-                           const int* __restrict__ dst, long long nnz,
+                           const int* __restrict__ dst, long long nnz, int kfix,
                            unsigned long long* __restrict__ keys, int* __restrict__ vals) {
-  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
-       r += (long long)gridDim.x * blockDim.x) {
-    for (long long i = indptr[r]; i < indptr[r + 1]; i++) {
-      const long long c = dst[i];
-      keys[i] = (unsigned long long)(r * n + c);
-      vals[i] = (int)i;
-      keys[nnz + i] = (unsigned long long)(c * n + r);
-      vals[nnz + i] = (int)(nnz + i);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long r;
+    if (kfix > 0) {
+      r = i / kfix;
+    } else {
+      long long lo = 0, hi = nrows - 1;
+      while (lo < hi) {
+        const long long mid = (lo + hi + 1) >> 1;
+        if (indptr[mid] <= i) lo = mid; else hi = mid - 1;
+      }
+      r = lo;
     }
+    const long long c = dst[i];
+    keys[i] = (unsigned long long)(r * n + c);
+    vals[i] = (int)i;
+    keys[nnz + i] = (unsigned long long)(c * n + r);
+    vals[nnz + i] = (int)(nnz + i);
   }
 }
 
@@ -86,6 +97,25 @@ __global__ void union_write(long long m, long long n, const unsigned long long* 
       atomicAdd(&rowcnt[s], 1);
     }
   }
+}
+
+__global__ void check_rows_fixed(const long long* __restrict__ indptr, long long n, long long kfix,
+                                 int* __restrict__ bad) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x)
+    if (indptr[r + 1] - indptr[r] != kfix) *bad = 1;
+}
+
+unsigned grid_for(long long items);
+
+bool rows_fixed(const int64_t* indptr, long long n, int kfix, long long* scratch, cudaStream_t st) {
+  int* bad = reinterpret_cast<int*>(scratch);
+  if (cudaMemsetAsync(bad, 0, sizeof(int), st) != cudaSuccess) return false;
+  check_rows_fixed<<<grid_for(n), 256, 0, st>>>((const long long*)indptr, n, kfix, bad);
+  int h = 1;
+  if (cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) return false;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return false;
+  return h == 0;
 }
 
 struct SymWs {
@@ -177,7 +207,20 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
   const long long m = 2 * nnz;
   GU_CHECK(cudaMemsetAsync(ws.rowcnt, 0, sizeof(int) * (size_t)(n + 1), st));
   if (m > 0) {
-    build_keys<<<grid_for(n), 256, 0, st>>>(n, n, (const long long*)indptr, dst, nnz, ws.k0, ws.v0);
+    // fixed row length when indptr == kfix * arange (checked on the host side
+    // of the call: nnz == n * kfix and the last offset matches)
+    long long last = 0;
+    GU_CHECK(cudaMemcpyAsync(&last, indptr + n, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    long long first1 = 0;
+    GU_CHECK(cudaMemcpyAsync(&first1, indptr + 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    GU_CHECK(cudaStreamSynchronize(st));
+    int kfix = (n > 0 && first1 > 0 && first1 * n == nnz && last == nnz) ? (int)first1 : 0;
+    if (kfix > 0) {
+      // confirm every row has kfix entries (one pass, flag in the scan workspace)
+      kfix = rows_fixed(indptr, n, kfix, ws.partial, st) ? kfix : 0;
+    }
+    build_keys<<<grid_for(nnz), 256, 0, st>>>(n, n, (const long long*)indptr, dst, nnz, kfix,
+                                              ws.k0, ws.v0);
     GU_CHECK_LAUNCH("build_keys");
     int end_bit = 1;
     while (end_bit < 64 && ((unsigned long long)n * (unsigned long long)n) > (1ull << end_bit))
