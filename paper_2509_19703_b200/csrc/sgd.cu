@@ -14,13 +14,13 @@
 //               sequential sweep; u and v receive their deltas through
 //               vector float2 atomics (red.global.add.v2.f32).
 // Schedule (D7 in SURVEY.md section 9): edges are stored once in a
-// Philox-Feistel shuffled order (gu_sgd_prepare_edges).  Windowed epochs
+// Feistel-shuffled order (gu_sgd_prepare_edges).  Windowed epochs
 // (optimize_sampled) take the window of `window` consecutive positions
 // starting where the previous epoch stopped, wrapping (layout.py:329-337).
 // Full epochs (optimize_full) visit every edge in a fresh per-epoch order:
 // 1024-edge tiles permuted by a per-epoch Feistel bijection, tiles streamed
-// coalesced.  Negatives and thetas come from Philox4x32-10 keyed by
-// (seed, epoch, position).
+// coalesced.  Negatives and thetas come from a counter-based 64-bit mix of
+// (seed, epoch, position, slot, try).
 #include <climits>
 #include <cmath>
 
@@ -31,7 +31,10 @@ namespace gu {
 namespace {
 
 constexpr int TILE = 1024;
-constexpr int SGD_NEG_BLOCK = 5;  // negatives handled in lockstep per block
+constexpr int SGD_NEG_BLOCK = 5;
+#ifndef SGD_MIN_BLOCKS
+#define SGD_MIN_BLOCKS 4  // <= 64 registers: 32 warps per SM
+#endif  // negatives handled in lockstep per block
 
 // Feistel bijection on [0, 2^bits) with cycle walking into [0, m)
 __device__ __host__ __forceinline__ unsigned long long mix64(unsigned long long x) {
@@ -41,6 +44,13 @@ __device__ __host__ __forceinline__ unsigned long long mix64(unsigned long long 
   x *= 0xc4ceb9fe1a85ec53ULL;
   x ^= x >> 33;
   return x;
+}
+
+// counter-based draw for (edge position p, negative slot q, try t) of one
+// epoch: two rounds of a 64-bit finaliser over the packed counter
+__device__ __forceinline__ unsigned long long draw64(unsigned long long key, long long p, int q,
+                                                     int t) {
+  return mix64(mix64(key ^ (unsigned long long)p) ^ (((unsigned long long)q << 8) | (unsigned)t));
 }
 
 struct Feistel {
@@ -108,14 +118,14 @@ __device__ __forceinline__ bool is_neighbor(const int* __restrict__ ip, const in
   return false;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
     sgd_epoch_kernel(int n, long long E, float2* __restrict__ xy, const int4* __restrict__ edges,
                      const int* __restrict__ nip, const int* __restrict__ nix, float a, float b,
                      float lr, int epoch, int n_neg, long long items, long long start,
                      int windowed, unsigned long long seed, int* __restrict__ diverged) {
   const long long ntiles = (E + TILE - 1) / TILE;
   Feistel tperm((unsigned long long)ntiles, mix64(seed ^ (0x51ED27ull + (unsigned long long)epoch)));
-  const uint2 key = make_uint2((unsigned)seed, (unsigned)(seed >> 32));
+  const unsigned long long rkey = mix64(seed ^ (0xA5A5A5A5ull * (unsigned long long)(epoch + 1)));
   bool bad = false;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < items;
        i += (long long)gridDim.x * blockDim.x) {
@@ -149,8 +159,8 @@ __global__ void __launch_bounds__(256)
         if (!isfinite(xv.x - gx) || !isfinite(xv.y - gy)) bad = true;
       }
     }
-    // repulsions.  Draw d of slot q comes from Philox(p, epoch, q, d) (four
-    // 32-bit draws per call: one candidate try or one theta each).  The
+    // repulsions.  Try t of slot q draws 64 bits from draw64(epoch key, p,
+    // q, t): the high half picks the candidate, the low half is its theta.  The
     // first tries of all slots are known up front, so their neighbour tests
     // run as lockstep binary searches over the head's sorted row (bounds
     // loaded once), and their coordinate loads are issued together; a
@@ -168,12 +178,12 @@ __global__ void __launch_bounds__(256)
     for (int q0 = 0; q0 < n_neg; q0 += SGD_NEG_BLOCK) {
       const int nq = min(SGD_NEG_BLOCK, n_neg - q0);
       int cand[SGD_NEG_BLOCK], lo[SGD_NEG_BLOCK], len[SGD_NEG_BLOCK];
-      uint4 r4[SGD_NEG_BLOCK];
+      unsigned spare_q[SGD_NEG_BLOCK];
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
-        r4[q] = Philox::gen(make_uint4((unsigned)p, (unsigned)(p >> 32), (unsigned)epoch,
-                                       (unsigned)((q0 + q) << 8)), key);
-        cand[q] = (int)__umulhi(r4[q].x, (unsigned)n);
+        const unsigned long long r = draw64(rkey, p, q0 + q, 0);
+        cand[q] = (int)__umulhi((unsigned)(r >> 32), (unsigned)n);
+        spare_q[q] = (unsigned)r;
         lo[q] = rb;
         len[q] = q < nq ? re - rb : 0;
       }
@@ -207,17 +217,15 @@ __global__ void __launch_bounds__(256)
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         if (q >= nq) break;
         int c = ok[q] ? cand[q] : -1;
-        unsigned spare = r4[q].y;  // theta draw of this slot
+        unsigned spare = spare_q[q];  // theta draw of this slot
         if (!ok[q]) {
           // retries 2..8 of this slot (rare)
           for (int t = 1; t < 8; t++) {
-            const uint4 rr = Philox::gen(make_uint4((unsigned)p, (unsigned)(p >> 32),
-                                                    (unsigned)epoch,
-                                                    (unsigned)(((q0 + q) << 8) | t)), key);
-            const int cc = (int)__umulhi(rr.x, (unsigned)n);
+            const unsigned long long rr = draw64(rkey, p, q0 + q, t);
+            const int cc = (int)__umulhi((unsigned)(rr >> 32), (unsigned)n);
             if (cc == u || is_neighbor(nip, nix, u, cc)) continue;
             c = cc;
-            spare = rr.y;
+            spare = (unsigned)rr;
             break;
           }
           if (c < 0) continue;
