@@ -525,6 +525,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 // chunk's hash work.  Sources of any other shape (deg(s) > 32, a level 2 that
 // does not reach k, a ball above the budget) go to the generic tiers.
 constexpr int TF_CAP2 = 160;  // level-2 ids kept per source
+#ifndef TF_HC
+#define TF_HC 512  // hash slots per source (ball budget 3/4 of it)
+#endif
 
 __device__ unsigned long long g_magic[4097];
 
@@ -546,7 +549,7 @@ __global__ void __launch_bounds__(WARPS * 32)
               int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
               int* __restrict__ ovf_list, int* __restrict__ ovf_count,
               unsigned long long* __restrict__ work) {
-  constexpr int HC = 512;
+  constexpr int HC = TF_HC;
   __shared__ __align__(16) int sm_hash[WARPS][HC];
   __shared__ int sm_list[WARPS][TF_CAP2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -651,14 +654,17 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int cpre = inc - cdv;
     const int T = __shfl_sync(FULL, inc, 31);
     int nst = 0, pcount = 0;
-    // candidate of chunk t0 for this lane (parent count of earlier chunks: pc)
+    // candidate of chunk t0 for this lane (parent count of earlier chunks: pc);
+    // cbase = adjacency start - flattened start of the lane's parent, so a
+    // candidate address is one shuffle and one add away
+    const int cbase = cb - cpre;
     auto load_chunk = [&](int t0, int pc, int& w, unsigned& m) {
-      const bool mine = lane < nne && cpre >= t0 && cpre < t0 + 32;
-      m = __reduce_or_sync(FULL, mine ? 1u << (cpre - t0) : 0u);
+      const unsigned off = (unsigned)(cpre - t0);
+      m = __reduce_or_sync(FULL, (lane < nne && off < 32u) ? (1u << off) : 0u);
       const int p = pc + __popc(m & le_mask) - 1;
-      const int ppre = __shfl_sync(FULL, cpre, p & 31);
-      const int pbb = __shfl_sync(FULL, cb, p & 31);
-      w = t0 + lane < T ? __ldg(indices + pbb + (t0 + lane - ppre)) : -1;
+      const int base = __shfl_sync(FULL, cbase, p & 31);
+      const int t = t0 + lane;
+      w = t < T ? __ldg(indices + (base + t)) : -1;
     };
     int w;
     unsigned m;
