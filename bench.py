@@ -264,6 +264,7 @@ def run_ours(args):
             result["sgd"] = _sgd_bench(gu, g, args, dev, peak)
         if not args.skip_layout:
             result["layout_e2e"] = _layout_e2e(gu)
+            result["full_path"] = _full_path(gu, peak)
         if not args.skip_cpu:
             result["cpu_baseline"] = _cpu_baseline(g)
         print(json.dumps(result), flush=True)
@@ -347,6 +348,59 @@ def _sgd_bench(gu, g, args, dev, peak):
             "diverged": int(div.item()) != INT32_MAX}
 
 
+def _full_path(gu, peak):
+    """Fused full-BFS kNN (GUMAP / SS-GUMAP C0+C1) on c1 and c2: GTEPS over
+    the adjacency entries the early-exit bitset BFS actually scans."""
+    import torch
+    from paper_2509_19703_b200 import fixtures
+    from paper_2509_19703_b200.device import device_csr
+    from paper_2509_19703_b200.neighbors import full_knn_records
+
+    out = {}
+    for name in ("c1", "c2"):
+        g = fixtures.config_graph(name)
+        csr = device_csr(g)
+        work = torch.zeros(2, dtype=torch.int64, device="cuda")
+        full_knn_records(csr, K_NN, 0, 0, g.n, work=work)
+        torch.cuda.synchronize()
+        te = int(work[0])
+        ts = []
+        for _ in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            full_knn_records(csr, K_NN, 0, 0, g.n)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = sum(ts[1:]) / len(ts[1:])
+        out[name] = {"n": g.n, "m": int(g.m), "ms": round(ms, 4), "te": te,
+                     "gteps": round(te / ms / 1e6, 3)}
+    return {"metric": "BFS-kNN GTEPS, full path (bitset BFS, early exit at the k-th distance, "
+                      "numpy tie-break)", "configs": out}
+
+
+def _layout_gumap_c1(gu):
+    """GUMAP on c1 (BASELINE configs[0]) through the public API: all-pairs
+    BFS kNN -> weights -> 200 full epochs from random init, seconds."""
+    import torch
+    from paper_2509_19703_b200 import fixtures
+
+    g = fixtures.grid(2500)
+
+    def once():
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        knn = gu.knn_from_full_distances(gu.all_pairs_bfs(g), 15, seed=0)
+        gk = gu.smooth_knn_weights(knn)
+        lay = gu.optimize_full(gk, gu.random_init(g, 0, 10.0),
+                               gu.OptimizerConfig(iterations=200, k=15, seed=0), tag="GUMAP")
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0
+
+    once()
+    return round(min(once() for _ in range(3)), 4)
+
+
 def _layout_e2e(gu):
     """SL-GUMAP on c3 through the public API, host arrays in / out."""
     import torch
@@ -373,7 +427,8 @@ def _layout_e2e(gu):
     ts = [once()[0] for _ in range(3)]
     return {"metric": "end-to-end layout seconds", "config": "c3 SL-GUMAP BA(100k, m0=3), "
             "200 epochs, 10% window, random init, host arrays in/out", "value": round(min(ts), 4),
-            "unit": "s", "higher_is_better": False}
+            "unit": "s", "higher_is_better": False,
+            "c1_gumap_seconds": _layout_gumap_c1(gu)}
 
 
 def _cpu_baseline(g, sample=400_000):
