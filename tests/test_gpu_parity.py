@@ -336,3 +336,35 @@ def test_quality_c1_vs_reference(gu):
     assert v.mean(axis=0)[0] >= ref.mean(axis=0)[0] - 4 * se[0]
     assert v.mean(axis=0)[1] <= ref.mean(axis=0)[1] + 4 * se[1]
     assert v.mean(axis=0)[2] <= ref.mean(axis=0)[2] + 4 * se[2]
+
+
+def test_sharded_knn_nccl_single_rank(gu):
+    """The NCCL path of distributed.sharded_knn (all_gather of records) on a
+    one-rank group: identical to the single-GPU kNN (partial and full)."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2509_19703_b200.distributed import sharded_knn
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        g = gu.synth_graph("scale_free", 5000, seed=3, m0=3)
+        knn = sharded_knn(g, 15, seed=7, mode="partial")
+        _, ref = gu.partial_bfs(g, 15, seed=7)
+        assert np.array_equal(knn.dst, ref.dst) and np.array_equal(knn.dist, ref.dist)
+        assert np.array_equal(knn.indptr, ref.indptr)
+        g2 = gu.synth_graph("grid", 900)
+        knn2 = sharded_knn(g2, 15, seed=1, mode="full")
+        ref2 = gu.knn_from_full_distances(gu.all_pairs_bfs(g2), 15, seed=1)
+        assert np.array_equal(knn2.dst, ref2.dst) and np.array_equal(knn2.dist, ref2.dist)
+    finally:
+        dist.destroy_process_group()
