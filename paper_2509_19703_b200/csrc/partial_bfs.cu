@@ -15,9 +15,10 @@
 // the frontier, 32 entries per step) against a shared-memory hash of the
 // vertices already discovered, compacting first occurrences in order.
 //
-// Tiers (no host sync between them; counts live in device memory):
-//   tier 1a  shared hash, CAP=128 discovered vertices per source, 8 warps/CTA
-//   tier 1b  shared hash, CAP=1024 (sources that overflowed 1a)
+// Tiers (no host sync between them; overflow lists live in device memory):
+//   tier F   register fast path: levels 1-2 reach k, deg(s) <= 32 (default)
+//   tier 1a  lean warp per source, shared hash, CAP=128 discovered vertices
+//   tier 1b  grouped warp kernel, shared hash, CAP=1024
 //   tier 2   per-warp global stamp array of n ints, parents expanded
 //            sequentially in queue order (any level size, any k)
 #include <climits>
@@ -728,525 +729,6 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
 }
 
-// ------------------------------------------------------------- tier B
-// CTA batch: S sources per CTA processed level-synchronously; every phase is
-// flattened across the batch so that threads, not warps, carry the per-item
-// work and per-source overheads are amortised:
-//   1  thread per source: frontier size f; block scan -> parent bases
-//   2  thread per parent: adjacency start and degree; block scan over the
-//      degrees -> each parent's first flattened candidate slot (sources'
-//      candidates are contiguous, in queue order); owner of every slot
-//   3  thread per candidate slot: load the neighbour id (several independent
-//      loads in flight per thread), insert it into its source's hash: key by
-//      atomicCAS, first flattened index by atomicMin of (level << 22 | t).  An
-//      id is first met at t iff the hash holds t afterwards -- the reference's
-//      FIFO discovery order (see the top of this file).
-//   4  first-occurrence flags, block exclusive scan, compaction into each
-//      source's level list in t order
-//   5  thread per source: crossing-level partial Fisher-Yates (exact 64-bit
-//      remainder by table), level entries written ranked by id.
-// Sources whose ball or level does not fit the per-source budget are pushed
-// to the warp tiers.
-constexpr int TB_THREADS = 256;
-constexpr int TB_WARPS = TB_THREADS / 32;
-
-template <int S, int HC, int LC, int GC, int PC>
-struct TierB {
-  // shared layout, in ints:
-  //   key[S][HC] val[S][HC] disc[S][LC] scan[GC + 1] pbeg[PC] ppre[PC]
-  //   cand/owner as uint16 pairs [GC]  psrc/pidx as uint8 pairs [PC] (PC/2 ints)
-  //   per-source scalars [16][S], block-scan scratch [TB_WARPS + 8]
-  static constexpr int WORDS = 2 * S * HC + S * LC + (GC + 4) + 2 * PC + GC + PC / 2 +
-                               16 * S + TB_WARPS + 8;
-  static constexpr size_t BYTES = sizeof(int) * (size_t)((WORDS + 3) & ~3);
-  static_assert(HC <= 65535 && PC <= 65535 && S <= 255 && LC <= 255, "packed index widths");
-};
-
-// block-wide exclusive scan of one int per thread (TB_THREADS threads)
-__device__ __forceinline__ int block_scan(int v, int* scratch, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int inc = warp_incl_scan(v);
-  if (lane == 31) scratch[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    const int x = lane < TB_WARPS ? scratch[lane] : 0;
-    const int xi = warp_incl_scan(x);
-    if (lane < TB_WARPS) scratch[lane] = xi - x;
-    if (lane == TB_WARPS - 1) scratch[TB_WARPS] = xi;
-  }
-  __syncthreads();
-  const int r = scratch[warp] + inc - v;
-  *total = scratch[TB_WARPS];
-  __syncthreads();
-  return r;
-}
-
-template <int S, int HC, int LC, int GC, int PC>
-__global__ void __launch_bounds__(TB_THREADS)
-    pbfs_batch(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
-               unsigned long long seed, long long src_begin, long long nsrc,
-               int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
-               int* __restrict__ ovf_list, int* __restrict__ ovf_count,
-               unsigned long long* __restrict__ work) {
-  extern __shared__ __align__(16) int smem[];
-  int* const key = smem;                                   // [S][HC]
-  int* const val = key + S * HC;                           // [S][HC]
-  int* const disc = val + S * HC;                          // [S][LC]
-  int* const scan = disc + S * LC;                         // [GC + 1]
-  int* const pbeg = scan + GC + 4;                         // [PC] (keeps 8-byte alignment)
-  int* const ppre = pbeg + PC;                             // [PC]
-  unsigned short* const cand = reinterpret_cast<unsigned short*>(ppre + PC);   // [GC]
-  unsigned short* const owner = cand + GC;                                     // [GC]
-  unsigned char* const psrc = reinterpret_cast<unsigned char*>(owner + GC);    // [PC]
-  unsigned char* const pidx = psrc + PC;                                       // [PC]
-  int* const sc = reinterpret_cast<int*>(pidx + PC);
-  int* const s_src = sc;
-  int* const s_lb = sc + S;
-  int* const s_le = sc + 2 * S;
-  int* const s_cnt = sc + 3 * S;
-  int* const s_live = sc + 4 * S;  // 1 live, 0 done, 2 overflow
-  int* const s_pb = sc + 5 * S;    // first parent
-  int* const s_f = sc + 6 * S;     // frontier size
-  int* const s_tb = sc + 7 * S;    // first candidate slot
-  int* const s_T = sc + 8 * S;     // candidates this level
-  int* const s_nins = sc + 9 * S;  // ids in the hash
-  int* const s_nst = sc + 10 * S;  // new ids this level
-  int* const s_exp = sc + 11 * S;  // vertices expanded
-  unsigned long long* const s_scn = reinterpret_cast<unsigned long long*>(sc + 12 * S);
-  int* const scr = sc + 16 * S;    // block-scan scratch
-  const int tid = threadIdx.x;
-  unsigned long long w_scanned = 0, w_expanded = 0;
-  const long long nbatch = (nsrc + S - 1) / S;
-
-  for (long long bi = blockIdx.x; bi < nbatch; bi += gridDim.x) {
-    // ---- init
-    for (int i = tid; i < S * HC; i += TB_THREADS) {
-      key[i] = -1;
-      val[i] = INT_MAX;
-    }
-    __syncthreads();
-    if (tid < S) {
-      const long long item = bi * S + tid;
-      const int s = item < nsrc ? (int)(src_begin + item) : -1;
-      s_src[tid] = s;
-      s_lb[tid] = 0;
-      s_le[tid] = 1;
-      s_cnt[tid] = 0;
-      s_live[tid] = s >= 0 ? 1 : 0;
-      s_nins[tid] = 1;
-      s_exp[tid] = 0;
-      s_scn[tid] = 0ull;
-      if (s >= 0) {
-        disc[tid * LC] = s;
-        const unsigned h = hash_id(s) & (HC - 1);
-        key[tid * HC + h] = s;
-        val[tid * HC + h] = 0;
-      }
-    }
-    int depth = 0;
-    for (;;) {
-      __syncthreads();
-      // ---- 1: frontier sizes -> parent bases
-      int f = 0;
-      if (tid < S && s_live[tid] == 1) f = s_le[tid] - s_lb[tid];
-      int P;
-      const int pb = block_scan(f, scr, &P);
-      if (tid < S) {
-        if (f > 0 && pb + f > PC) {
-          s_live[tid] = 2;
-          f = 0;
-        }
-        s_pb[tid] = pb;
-        s_f[tid] = f;
-        for (int i = 0; i < f; i++) {
-          psrc[pb + i] = (unsigned char)tid;
-          pidx[pb + i] = (unsigned char)(s_lb[tid] + i);
-        }
-      }
-      if (P > PC) P = PC;
-      __syncthreads();
-      // ---- 2: parents (blocked: thread owns PPT consecutive parents)
-      constexpr int PPT = (PC + TB_THREADS - 1) / TB_THREADS;
-      int pd[PPT];
-      int dsum = 0;
-#pragma unroll
-      for (int u = 0; u < PPT; u++) {
-        const int p = tid * PPT + u;
-        pd[u] = 0;
-        if (p < P && s_live[psrc[p]] == 1) {
-          const int q = psrc[p];
-          const int v = disc[q * LC + pidx[p]];
-          const int b = __ldg(indptr + v);
-          pd[u] = __ldg(indptr + v + 1) - b;
-          pbeg[p] = b;
-        }
-        dsum += pd[u];
-      }
-      int G;
-      int run = block_scan(dsum, scr, &G);
-#pragma unroll
-      for (int u = 0; u < PPT; u++) {
-        const int p = tid * PPT + u;
-        if (p < P) ppre[p] = run;
-        run += pd[u];
-      }
-      __syncthreads();
-      // per-source candidate ranges + budget checks
-      if (tid < S) {
-        const int ff = s_f[tid];
-        int tb = 0, T = 0;
-        if (ff > 0 && s_live[tid] == 1) {
-          const int p0 = s_pb[tid];
-          tb = ppre[p0];
-          const int last = p0 + ff - 1;
-          T = ppre[last] - tb + (last + 1 < P ? ppre[last + 1] - ppre[last] : G - ppre[last]);
-          s_exp[tid] += ff;
-          s_scn[tid] += (unsigned long long)T;
-          // the hash can never fill and the slots must fit the batch buffer
-          if (s_nins[tid] + T > HC - 1 || tb + T > GC) s_live[tid] = 2;
-        }
-        s_tb[tid] = tb;
-        s_T[tid] = T;
-      }
-      __syncthreads();
-      // owners of the candidate slots (thread per parent)
-#pragma unroll
-      for (int u = 0; u < PPT; u++) {
-        const int p = tid * PPT + u;
-        if (p < P && pd[u] > 0) {  // every slot gets an owner, even of overflowed sources
-          const int o = ppre[p];
-          const int e = o + pd[u] < GC ? o + pd[u] : GC;
-          for (int j = o; j < e; j++) owner[j] = (unsigned short)p;
-        }
-      }
-      // any live source?
-      int anyl = (tid < S && s_live[tid] == 1 && s_f[tid] > 0) ? 1 : 0;
-      anyl = __syncthreads_or(anyl);
-      if (!anyl) break;
-      depth++;
-      if (G > GC) G = GC;
-      const int tag = depth << 22;
-      // ---- 3: candidates -> hash
-      constexpr int U = 8;
-      for (int g0 = tid; g0 < G; g0 += TB_THREADS * U) {
-        int w[U], q[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-          const int g = g0 + u * TB_THREADS;
-          w[u] = -1;
-          q[u] = -1;
-          if (g < G) {
-            const int p = owner[g];
-            const int qq = psrc[p];
-            if (s_live[qq] == 1) {
-              q[u] = qq;
-              w[u] = __ldg(indices + pbeg[p] + (g - ppre[p]));
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-          if (q[u] >= 0) {
-            const int g = g0 + u * TB_THREADS;
-            int* kq = key + q[u] * HC;
-            unsigned h = hash_id(w[u]) & (HC - 1);
-            for (;;) {
-              const int old = atomicCAS(&kq[h], -1, w[u]);
-              if (old == -1) {
-                atomicAdd(&s_nins[q[u]], 1);
-                break;
-              }
-              if (old == w[u]) break;
-              h = (h + 1) & (HC - 1);
-            }
-            atomicMin(&val[q[u] * HC + h], tag | (g - s_tb[q[u]]));
-            cand[g] = (unsigned short)h;
-          }
-        }
-      }
-      __syncthreads();
-      // ---- 4: first-occurrence flags -> block scan -> level lists
-      {
-        constexpr int PER = (GC + TB_THREADS - 1) / TB_THREADS;
-        unsigned fl = 0;  // bit u = candidate tid*PER+u is a first occurrence
-        int sum = 0;
-#pragma unroll
-        for (int u = 0; u < PER; u++) {
-          const int g = tid * PER + u;
-          if (g < G) {
-            const int qq = psrc[owner[g]];
-            if (s_live[qq] == 1 && val[qq * HC + cand[g]] == (tag | (g - s_tb[qq]))) {
-              fl |= 1u << u;
-              sum++;
-            }
-          }
-        }
-        int tot;
-        int run2 = block_scan(sum, scr, &tot);
-#pragma unroll
-        for (int u = 0; u < PER; u++) {
-          const int g = tid * PER + u;
-          if (g < GC) scan[g] = run2;
-          run2 += (fl >> u) & 1u;
-        }
-        if (tid == TB_THREADS - 1) scan[GC] = run2;
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < PER; u++) {
-          if ((fl >> u) & 1u) {
-            const int g = tid * PER + u;
-            const int qq = psrc[owner[g]];
-            const int pos = s_le[qq] + scan[g] - scan[s_tb[qq]];
-            if (pos < LC) disc[qq * LC + pos] = key[qq * HC + cand[g]];
-          }
-        }
-        if (tid < S) s_nst[tid] = s_live[tid] == 1 ? scan[s_tb[tid] + s_T[tid]] - scan[s_tb[tid]] : 0;
-      }
-      __syncthreads();
-      // ---- 5: level finalize (thread per source)
-      if (tid < S && s_live[tid] == 1) {
-        const int q = tid;
-        const int le = s_le[q], nst = s_nst[q];
-        if (le + nst > LC) {
-          s_live[q] = 2;
-        } else if (nst == 0) {
-          s_live[q] = 0;
-        } else {
-          int* dq = disc + q * LC;
-          const int count = s_cnt[q];
-          const int remaining = K - count;
-          int take = nst;
-          if (nst > remaining) {
-            unsigned long long st = seed + SPLIT_GAMMA * (unsigned long long)(s_src[q] + 1);
-            for (int i = 0; i < remaining; i++) {
-              const int j = i + umod64_tab(splitmix_next(st), nst - i);
-              const int a = dq[le + i];
-              dq[le + i] = dq[le + j];
-              dq[le + j] = a;
-            }
-            take = remaining;
-          }
-          const long long row = (long long)s_src[q] - src_begin;
-          int* rn = out_nbr + row * K + count;
-          int* rd = out_dist + row * K + count;
-          if (depth == 1 && take == nst) {
-            for (int i = 0; i < take; i++) {  // level 1 in full: sorted adjacency of s
-              rn[i] = dq[le + i];
-              rd[i] = 1;
-            }
-          } else {
-            for (int i = 0; i < take; i++) {
-              const int v = dq[le + i];
-              int r = 0;
-              for (int x = 0; x < take; x++) r += dq[le + x] < v;
-              rn[r] = v;
-              rd[r] = depth;
-            }
-          }
-          s_cnt[q] = count + take;
-          s_lb[q] = le;
-          s_le[q] = le + nst;
-          if (count + take >= K) s_live[q] = 0;
-        }
-      }
-    }
-    // ---- batch outputs
-    __syncthreads();
-    if (tid < S && s_src[tid] >= 0) {
-      const int s = s_src[tid];
-      if (s_live[tid] == 2) {
-        ovf_list[atomicAdd(ovf_count, 1)] = s;
-      } else {
-        out_cnt[(long long)s - src_begin] = s_cnt[tid];
-        w_scanned += s_scn[tid];
-        w_expanded += (unsigned long long)s_exp[tid];
-      }
-    }
-  }
-  if (work) {
-    w_scanned = warp_sum(w_scanned);
-    w_expanded = warp_sum(w_expanded);
-    if ((tid & 31) == 0 && (w_scanned | w_expanded)) {
-      atomicAdd(work, w_scanned);
-      atomicAdd(work + 1, w_expanded);
-    }
-  }
-}
-
-// ------------------------------------------------------------- tier 0
-// Thread per source: each thread runs the reference's sequential FIFO BFS
-// (_kernels.py:76-131) for its own source; the 4M independent sources supply
-// the parallelism and no warp collective is needed.  Divergence is kept low
-// by structure: a parent's adjacency (<= 16 entries, the common case) is
-// loaded as one unrolled burst of independent predicated loads into
-// registers, and the next parent's burst is issued before the current one is
-// hashed (software pipeline, ~2 parents of loads in flight per thread), so
-// all lanes walk their frontiers in near-lockstep.
-// Per-thread state lives in shared memory laid out slot-major
-// ([slot][thread]), so random hash slots of the 32 lanes hit 32 distinct
-// banks:
-//   hash   HC slots of vertex ids (linear probing; cleared per source)
-//   list   LCAP discovered vertices of levels >= 1 in discovery order
-// Sources whose ball does not fit (more than HLIM discovered, or a level
-// beyond LCAP) are pushed to the warp tiers, which handle any size.
-template <int HC, int LCAP, int TPB>
-struct Tier0 {
-  static constexpr int HLIM = HC * 3 / 4;
-  static constexpr size_t BYTES = sizeof(int) * (size_t)(HC + LCAP) * TPB;
-};
-
-constexpr int T0_BURST = 16;
-
-template <int HC, int LCAP, int TPB>
-__global__ void __launch_bounds__(TPB)
-    pbfs_thread(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
-                unsigned long long seed, long long src_begin, long long nsrc,
-                int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
-                int* __restrict__ ovf_list, int* __restrict__ ovf_count,
-                unsigned long long* __restrict__ work) {
-  constexpr int HLIM = Tier0<HC, LCAP, TPB>::HLIM;
-  extern __shared__ __align__(16) int smem[];
-  int* hk = smem + threadIdx.x;             // hk[i * TPB]
-  int* dl = smem + HC * TPB + threadIdx.x;  // dl[i * TPB]
-  unsigned long long w_scanned = 0, w_expanded = 0;
-  for (long long item = (long long)blockIdx.x * TPB + threadIdx.x; item < nsrc;
-       item += (long long)gridDim.x * TPB) {
-    const int s = (int)(src_begin + item);
-#pragma unroll
-    for (int i = 0; i < HC; i++) hk[i * TPB] = -1;
-    int nins = 0;
-    // insert w; true iff it was not present
-    auto insert = [&](int w) -> bool {
-      unsigned h = hash_id(w) & (HC - 1);
-      for (;;) {
-        const int k = hk[h * TPB];
-        if (k == w) return false;
-        if (k == -1) {
-          hk[h * TPB] = w;
-          nins++;
-          return true;
-        }
-        h = (h + 1) & (HC - 1);
-      }
-    };
-    insert(s);
-    // level 0 -> 1: the frontier is [s]; afterwards the frontier is dl[lb, le)
-    int lb = 0, le = 0, count = 0, depth = 0;
-    bool ovf = false;
-    unsigned long long scanned = 0, expanded = 0;
-    int* rn = out_nbr + item * K;
-    int* rd = out_dist + item * K;
-    int f = 1;  // frontier size
-    while (count < K && f > 0) {
-      depth++;
-      int nst = 0;
-      // ---- expand the frontier in queue order, two parents of loads in flight
-      auto parent = [&](int i) -> int { return depth == 1 ? s : dl[(lb + i) * TPB]; };
-      int cb = 0, ce = 0, nb = 0, ne = 0;
-      {
-        const int u0 = parent(0);
-        cb = __ldg(indptr + u0);
-        ce = __ldg(indptr + u0 + 1);
-        if (f > 1) {
-          const int u1 = parent(1);
-          nb = __ldg(indptr + u1);
-          ne = __ldg(indptr + u1 + 1);
-        }
-      }
-      int cur[T0_BURST];
-#pragma unroll
-      for (int q = 0; q < T0_BURST; q++) cur[q] = cb + q < ce ? __ldg(indices + cb + q) : -1;
-      for (int i = 0; i < f; i++) {
-        int nxt[T0_BURST];
-#pragma unroll
-        for (int q = 0; q < T0_BURST; q++) nxt[q] = nb + q < ne ? __ldg(indices + nb + q) : -1;
-        int nb2 = 0, ne2 = 0;
-        if (i + 2 < f) {
-          const int u2 = parent(i + 2);
-          nb2 = __ldg(indptr + u2);
-          ne2 = __ldg(indptr + u2 + 1);
-        }
-        scanned += ce - cb;
-        expanded++;
-#pragma unroll
-        for (int q = 0; q < T0_BURST; q++) {
-          if (cur[q] >= 0 && insert(cur[q])) {
-            if (le + nst < LCAP) dl[(le + nst) * TPB] = cur[q];
-            nst++;
-          }
-        }
-        for (int p = cb + T0_BURST; p < ce; p++) {  // tail of a long adjacency
-          const int w = __ldg(indices + p);
-          if (insert(w)) {
-            if (le + nst < LCAP) dl[(le + nst) * TPB] = w;
-            nst++;
-          }
-          if (nins > HLIM) break;
-        }
-        if (nins > HLIM || le + nst > LCAP) {
-          ovf = true;
-          break;
-        }
-#pragma unroll
-        for (int q = 0; q < T0_BURST; q++) cur[q] = nxt[q];
-        cb = nb;
-        ce = ne;
-        nb = nb2;
-        ne = ne2;
-      }
-      if (ovf || nst == 0) break;
-      const int remaining = K - count;
-      int take = nst;
-      if (nst > remaining) {
-        // random subset of the crossing level (_kernels.py:98-105)
-        unsigned long long st = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
-        for (int i = 0; i < remaining; i++) {
-          const int j = i + umod64_small(splitmix_next(st), nst - i);
-          const int a = dl[(le + i) * TPB];
-          dl[(le + i) * TPB] = dl[(le + j) * TPB];
-          dl[(le + j) * TPB] = a;
-        }
-        take = remaining;
-      }
-      // this level's entries in id order (level 1 of a full take is the sorted
-      // adjacency of s already); rank each entry inside the level
-      if (depth == 1 && take == nst) {
-        for (int i = 0; i < take; i++) {
-          rn[count + i] = dl[(le + i) * TPB];
-          rd[count + i] = 1;
-        }
-      } else {
-        for (int i = 0; i < take; i++) {
-          const int v = dl[(le + i) * TPB];
-          int r = 0;
-          for (int j = 0; j < take; j++) r += dl[(le + j) * TPB] < v;
-          rn[count + r] = v;
-          rd[count + r] = depth;
-        }
-      }
-      count += take;
-      lb = le;
-      le += nst;
-      f = nst;
-    }
-    if (ovf) {
-      ovf_list[atomicAdd(ovf_count, 1)] = s;
-      continue;
-    }
-    out_cnt[item] = count;
-    w_scanned += scanned;
-    w_expanded += expanded;
-  }
-  if (work) {
-    w_scanned = warp_sum(w_scanned);
-    w_expanded = warp_sum(w_expanded);
-    if ((threadIdx.x & 31) == 0) {
-      atomicAdd(work, w_scanned);
-      atomicAdd(work + 1, w_expanded);
-    }
-  }
-}
-
 // ----------------------------------------------------------------- tier 2
 // Exact FIFO emulation: parents in queue order, each parent's sorted
 // adjacency in 32-entry chunks; per-warp stamp array (value s+1) of n ints.
@@ -1405,53 +887,6 @@ size_t pbfs_ws_layout(long long n, long long nsrc, int slots, char* base, PbfsWs
   return off;
 }
 
-template <int G>
-cudaError_t launch_tier1a(int sms, const int* indptr, const int* indices, int k,
-                          unsigned long long seed, long long src_begin, long long nsrc,
-                          const int* list, const int* list_count, int* out_nbr, int* out_dist,
-                          int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
-                          cudaStream_t st) {
-  using LA = Tier1<G, T1A_CAP, T1A_PCAP, T1A_TCAP>;
-  constexpr size_t smem = sizeof(int) * LA::WORDS * LA::NG * T1A_WARPS;
-  auto kern = pbfs_tier1<G, T1A_CAP, T1A_PCAP, T1A_TCAP, T1A_WARPS>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T1A_WARPS * 32, smem);
-  if (e != cudaSuccess) return e;
-  const long long per_block = (long long)T1A_WARPS * LA::NG;
-  long long blocks = (nsrc + per_block - 1) / per_block;
-  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * (list ? 1 : 8);
-  if (blocks > cap) blocks = cap;
-  kern<<<(unsigned)blocks, T1A_WARPS * 32, smem, st>>>(indptr, indices, k, seed, src_begin, nsrc,
-                                                        list, list_count, out_nbr, out_dist,
-                                                        out_count, ovf_out, ovf_cnt, work);
-  return cudaGetLastError();
-}
-
-constexpr int T0_HC = 128, T0_LCAP = 96, T0_TPB = 128;
-
-cudaError_t launch_thread(int sms, const int* indptr, const int* indices, int k,
-                          unsigned long long seed, long long src_begin, long long nsrc,
-                          int* out_nbr, int* out_dist, int* out_count, int* ovf_out, int* ovf_cnt,
-                          unsigned long long* work, cudaStream_t st) {
-  constexpr size_t smem = Tier0<T0_HC, T0_LCAP, T0_TPB>::BYTES;
-  auto kern = pbfs_thread<T0_HC, T0_LCAP, T0_TPB>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T0_TPB, smem);
-  if (e != cudaSuccess) return e;
-  long long blocks = (nsrc + T0_TPB - 1) / T0_TPB;
-  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * 16;
-  if (blocks > cap) blocks = cap;
-  kern<<<(unsigned)blocks, T0_TPB, smem, st>>>(indptr, indices, k, seed, src_begin, nsrc, out_nbr,
-                                               out_dist, out_count, ovf_out, ovf_cnt, work);
-  return cudaGetLastError();
-}
-
-constexpr int TBS = 32, TB_HC = 128, TB_LC = 96, TB_GC = 4096, TB_PC = 1024;
-
 // M_d = ceil(2^64 / d) for the table remainder (uploaded once per device)
 cudaError_t ensure_magic() {
   static int ready_dev = -1;
@@ -1484,31 +919,6 @@ cudaError_t launch_fast(int sms, const int* indptr, const int* indices, int k,
   kern<<<(unsigned)blocks, TF_WARPS * 32, 0, st>>>(indptr, indices, k, seed, src_begin, nsrc,
                                                    out_nbr, out_dist, out_count, ovf_out, ovf_cnt,
                                                    work);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_batch(int sms, const int* indptr, const int* indices, int k,
-                         unsigned long long seed, long long src_begin, long long nsrc,
-                         int* out_nbr, int* out_dist, int* out_count, int* ovf_out, int* ovf_cnt,
-                         unsigned long long* work, cudaStream_t st) {
-  {
-    cudaError_t e0 = ensure_magic();
-    if (e0 != cudaSuccess) return e0;
-  }
-  using LB = TierB<TBS, TB_HC, TB_LC, TB_GC, TB_PC>;
-  constexpr size_t smem = LB::BYTES;
-  auto kern = pbfs_batch<TBS, TB_HC, TB_LC, TB_GC, TB_PC>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TB_THREADS, smem);
-  if (e != cudaSuccess) return e;
-  long long blocks = (nsrc + TBS - 1) / TBS;
-  long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1);
-  if (blocks > cap) blocks = cap;
-  kern<<<(unsigned)blocks, TB_THREADS, smem, st>>>(indptr, indices, k, seed, src_begin, nsrc,
-                                                    out_nbr, out_dist, out_count, ovf_out, ovf_cnt,
-                                                    work);
   return cudaGetLastError();
 }
 
@@ -1584,37 +994,18 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
   }
   const int sms = sm_count();
   if (k <= 32) {
-    // tier 1a (lean warp per source, CAP 128) -> tier 1b (CAP 1024) -> tier 2.
-    // GU_PBFS_MODE = lean (default) | thread | g16 | g32 selects the first tier
-    // (tuning / comparison only; every mode is exact).
+    // tier F (register fast path) -> tier 1a (lean warp per source, CAP 128)
+    // -> tier 1b (CAP 1024) -> tier 2.  GU_PBFS_MODE=lean skips tier F
+    // (comparison only; every path is exact).
     static const char* env_mode = getenv("GU_PBFS_MODE");
-    const char* mode = env_mode ? env_mode : "fast";
-    if (!strcmp(mode, "fast")) {
+    if (!env_mode || strcmp(env_mode, "lean")) {
       GU_CHECK(launch_fast(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
                            out_count, ws.ovf0, ws.counts + 2, work, st));
       GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0, ws.counts + 2,
                            out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
-    } else if (!strcmp(mode, "batch")) {
-      GU_CHECK(launch_batch(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
-                            out_count, ws.ovf0, ws.counts + 2, work, st));
-      GU_CHECK(launch_tier1a<32>(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0,
-                                 ws.counts + 2, out_nbr, out_dist, out_count, ws.ovfA,
-                                 ws.counts + 0, work, st));
-    } else if (!strcmp(mode, "thread")) {
-      GU_CHECK(launch_thread(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
-                             out_count, ws.ovf0, ws.counts + 2, work, st));
-      GU_CHECK(launch_tier1a<32>(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0,
-                                 ws.counts + 2, out_nbr, out_dist, out_count, ws.ovfA,
-                                 ws.counts + 0, work, st));
-    } else if (!strcmp(mode, "lean")) {
+    } else {
       GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
                            out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
-    } else if (k <= 16 && !strcmp(mode, "g16")) {
-      GU_CHECK(launch_tier1a<16>(sms, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
-                                 out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
-    } else {
-      GU_CHECK(launch_tier1a<32>(sms, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
-                                 out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
     }
     {
       using LB = Tier1<32, T1B_CAP, T1B_PCAP, T1B_TCAP>;
