@@ -18,7 +18,7 @@
 // Tiers (no host sync between them; overflow lists live in device memory):
 //   tier F   register fast path: levels 1-2 reach k, deg(s) <= 32 (default)
 //   tier 1a  lean warp per source, shared hash, CAP=128 discovered vertices
-//   tier 1b  grouped warp kernel, shared hash, CAP=1024
+//   tier 1b  lean warp per source, shared hash, CAP=1024
 //   tier 2   per-warp global stamp array of n ints, parents expanded
 //            sequentially in queue order (any level size, any k)
 #include <climits>
@@ -922,15 +922,15 @@ cudaError_t launch_fast(int sms, const int* indptr, const int* indices, int k,
   return cudaGetLastError();
 }
 
-cudaError_t launch_lean(int sms, const int* indptr, const int* indices, int k,
-                        unsigned long long seed, long long src_begin, long long nsrc,
-                        const int* list, const int* list_count, int* out_nbr, int* out_dist,
-                        int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
-                        cudaStream_t st) {
-  using LA = Tier1<32, T1A_CAP, T1A_PCAP, T1A_TCAP>;
-  constexpr int W = 8;
+template <int CAP, int PCAP, int TCAP, int W, int MINB>
+cudaError_t launch_warp_tier(int sms, const int* indptr, const int* indices, int k,
+                             unsigned long long seed, long long src_begin, long long nsrc,
+                             const int* list, const int* list_count, int* out_nbr, int* out_dist,
+                             int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
+                             cudaStream_t st) {
+  using LA = Tier1<32, CAP, PCAP, TCAP>;
   constexpr size_t smem = sizeof(int) * LA::WORDS * W;
-  auto kern = pbfs_warp<T1A_CAP, T1A_PCAP, T1A_TCAP, W, GU_LEAN_MINB>;
+  auto kern = pbfs_warp<CAP, PCAP, TCAP, W, MINB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -943,6 +943,28 @@ cudaError_t launch_lean(int sms, const int* indptr, const int* indices, int k,
                                                 list_count, out_nbr, out_dist, out_count, ovf_out,
                                                 ovf_cnt, work);
   return cudaGetLastError();
+}
+
+// tier 1a: lean warp, CAP 128
+cudaError_t launch_lean(int sms, const int* indptr, const int* indices, int k,
+                        unsigned long long seed, long long src_begin, long long nsrc,
+                        const int* list, const int* list_count, int* out_nbr, int* out_dist,
+                        int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
+                        cudaStream_t st) {
+  return launch_warp_tier<T1A_CAP, T1A_PCAP, T1A_TCAP, 8, GU_LEAN_MINB>(
+      sms, indptr, indices, k, seed, src_begin, nsrc, list, list_count, out_nbr, out_dist, out_count,
+      ovf_out, ovf_cnt, work, st);
+}
+
+// tier 1b: the same lean warp kernel with CAP 1024 (hub-adjacent balls)
+cudaError_t launch_lean_big(int sms, const int* indptr, const int* indices, int k,
+                            unsigned long long seed, long long src_begin, long long nsrc,
+                            const int* list, const int* list_count, int* out_nbr, int* out_dist,
+                            int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
+                            cudaStream_t st) {
+  return launch_warp_tier<T1B_CAP, T1B_PCAP, T1B_TCAP, 2, 1>(
+      sms, indptr, indices, k, seed, src_begin, nsrc, list, list_count, out_nbr, out_dist, out_count,
+      ovf_out, ovf_cnt, work, st);
 }
 
 int sm_count() {
@@ -1007,19 +1029,8 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
       GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
                            out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
     }
-    {
-      using LB = Tier1<32, T1B_CAP, T1B_PCAP, T1B_TCAP>;
-      constexpr size_t smem = sizeof(int) * LB::WORDS * LB::NG * T1B_WARPS;
-      auto kern = pbfs_tier1<32, T1B_CAP, T1B_PCAP, T1B_TCAP, T1B_WARPS>;
-      GU_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int per_sm = 0;
-      GU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T1B_WARPS * 32, smem));
-      long long blocks = (long long)sms * (per_sm > 0 ? per_sm : 1);
-      kern<<<(unsigned)blocks, T1B_WARPS * 32, smem, st>>>(
-          indptr, indices, k, seed, src_begin, nsrc, ws.ovfA, ws.counts + 0, out_nbr, out_dist,
-          out_count, ws.ovfB, ws.counts + 1, work);
-      GU_CHECK_LAUNCH("pbfs_tier1 (b)");
-    }
+    GU_CHECK(launch_lean_big(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovfA, ws.counts + 0,
+                             out_nbr, out_dist, out_count, ws.ovfB, ws.counts + 1, work, st));
   } else {
     // k > group size: every source goes straight to the exact tier-2 path
     fill_range_list<<<(unsigned)((nsrc + 255) / 256), 256, 0, st>>>(ws.ovfB, ws.counts + 1,
