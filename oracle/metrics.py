@@ -146,3 +146,50 @@ def count_crossings(g, coords, block=256):
         if _cross_exact(P[i], Q[i], P[j], Q[j]):
             extra += 1
     return certain + extra
+
+
+# ----------------------------------------------------------- sampled metrics
+# Exact per-vertex / per-pair terms of the two metrics above, averaged over a
+# fixed sample of source vertices: unbiased estimators used for check (c) on
+# graphs where the all-pairs versions do not fit a CPU (c3 and larger).
+
+def sample_sources(n, size=2000, seed=12345):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(n, size=min(size, n), replace=False))
+
+
+def sampled_neighborhood_preservation(coords, hop_rows, sources, r=2):
+    """Mean over ``sources`` of the metrics.py:41-79 Jaccard term.  hop_rows:
+    int32 BFS rows of the sources (INF32 unreachable)."""
+    coords = np.asarray(coords, np.float64)
+    total = 0.0
+    for i, v in enumerate(sources):
+        hv = hop_rows[i]
+        hood = np.flatnonzero((hv >= 1) & (hv <= r))
+        q = hood.shape[0]
+        if q == 0:
+            total += 1.0
+            continue
+        row = cdist(coords[v:v + 1], coords)[0]
+        row[v] = np.inf
+        nearest = np.argsort(row, kind="stable")[:q]
+        inter = np.intersect1d(hood, nearest, assume_unique=True).shape[0]
+        total += inter / (2 * q - inter)
+    return total / len(sources)
+
+
+def sampled_stress(coords, hop_rows, sources):
+    """metrics.py:90-132 restricted to the rows of ``sources`` (optimal scale
+    fitted on the same pairs)."""
+    coords = np.asarray(coords, np.float64)
+    delta = cdist(coords[sources], coords)
+    d = hop_rows.astype(np.float64)
+    d[np.arange(len(sources)), sources] = np.inf
+    d[d >= 2**31 - 1] = np.inf
+    s_num = float((delta / d).sum())
+    s_den = float((delta * delta / (d * d)).sum())
+    scale = s_num / s_den if s_den > 0 else 1.0
+    term = (1.0 - scale * delta / d) ** 2
+    term[np.arange(len(sources)), sources] = 0.0
+    finite = np.isfinite(d)
+    return float(term[finite].sum() / finite.sum())

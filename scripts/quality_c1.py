@@ -23,7 +23,7 @@ import paper_2509_19703_b200 as gu  # noqa: E402
 from oracle.metrics import count_crossings, neighborhood_preservation, stress  # noqa: E402
 
 
-def main(nseeds=20, out=os.path.join(ROOT, "profiles", "r01_quality_c1.json")):
+def main(nseeds=20, out=os.path.join(ROOT, "profiles", os.environ.get("QOUT", "r01_quality_c1.json"))):
     z = np.load(os.path.join(ROOT, "tests", "golden", "quality_c1.npz"))
     ref = np.stack([z["np_"], z["stress"], z["crossings"]], axis=1)
     g = gu.synth_graph("grid", 2500)

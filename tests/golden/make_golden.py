@@ -275,8 +275,42 @@ def gen_quality_c1(nseeds=20):
          layout0=layouts[0], layout1=layouts[1])
 
 
+def gen_quality_c3(nseeds=5):
+    """Check (c) at SL scale: the reference's c3 SL pipeline (BA 100k, random
+    init, 200 epochs, 10% window) for seeds 0..nseeds-1; sampled NP / stress
+    over a fixed 2000-source sample (oracle/metrics.py estimators)."""
+    import time
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    from oracle.metrics import (sample_sources, sampled_neighborhood_preservation,
+                                sampled_stress)
+    rg = gu.synth_graph("scale_free", 100000, seed=2, m0=3)
+    src = sample_sources(rg.n)
+    rows = np.empty((len(src), rg.n), np.int32)
+    O.lib().or_apsp_rows(rg.n, rg.adj_indptr.ctypes.data_as(O._i64p),
+                         np.ascontiguousarray(rg.adj_indices, np.int32).ctypes.data_as(O._i32p),
+                         src.astype(np.int64).ctypes.data_as(O._i64p), len(src),
+                         rows.ctypes.data_as(O._i32p), 8)
+    vals = []
+    for seed in range(nseeds):
+        t = time.time()
+        _, kn = gu.partial_bfs(rg, 15, seed=seed)
+        gk = gu.smooth_knn_weights(kn)
+        E = gk.edge_count
+        samp = math.log(0.1 * E) / math.log(E)
+        lay = gu.optimize_sampled(gk, gu.random_init(rg, seed, 10.0),
+                                  gu.OptimizerConfig(iterations=200, k=15, seed=seed, samp=samp))
+        npv = sampled_neighborhood_preservation(lay.coords, rows, src)
+        st = sampled_stress(lay.coords, rows, src)
+        vals.append((npv, st))
+        print("quality c3 seed", seed, vals[-1], f"{time.time() - t:.1f}s", flush=True)
+    v = np.array(vals)
+    save("quality_c3.npz", np_=v[:, 0], stress=v[:, 1], sources=src)
+
+
 def main():
-    which = sys.argv[1:] or ["partial_small", "full_small", "smooth_cases", "c1", "c3", "quality_c1"]
+    which = sys.argv[1:] or ["partial_small", "full_small", "smooth_cases", "c1", "c3", "quality_c1",
+                             "quality_c3"]
     for w in which:
         globals()["gen_" + w]()
     manifest = dict(numpy=np.__version__, scipy=scipy.__version__, numba=numba.__version__,
