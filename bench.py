@@ -25,8 +25,9 @@ Secondary lines inside the same JSON object:
   layout_e2e  SL-GUMAP on c3 (BA n=100k, 200 epochs, 10% window, random
               init) through the public API from host arrays: seconds
 The CPU baseline is the oracle's C port of the reference algorithm
-(oracle/oracle.c, all host threads) on a bounded sample of sources; the
-reference itself is Python/numba and cannot travel to the GPU box.
+(oracle/oracle.c, all host threads) over the full c5 workload, repeated to
+>= 10 s; the reference itself is Python/numba and cannot travel to the GPU
+box.
 """
 
 import argparse
@@ -431,21 +432,34 @@ def _layout_e2e(gu):
             "c1_gumap_seconds": _layout_gumap_c1(gu)}
 
 
-def _cpu_baseline(g, sample=400_000):
+def _cpu_full_pass(O, g, thr):
+    """One pass of the oracle's C port over every source of the c5 graph:
+    (seconds, TE)."""
+    t0 = time.perf_counter()
+    _, _, _, sc, _ = O.partial_bfs_raw(g, K_NN, SEED, 0, g.n, nthreads=thr, work=True)
+    return time.perf_counter() - t0, int(sc.sum())
+
+
+def _cpu_baseline(g, min_seconds=10.0, max_passes=40):
+    """The whole c5 workload on the host cores, repeated until >= min_seconds
+    of CPU work (the full workload is ~0.5 s on 16 threads, so no sampling)."""
     from oracle import oracle as O
     O.build()
     thr = O.max_threads()
-    t0 = time.perf_counter()
-    _, _, _, sc, ex = O.partial_bfs_raw(g, K_NN, SEED, 0, sample, nthreads=thr, work=True)
-    dt = time.perf_counter() - t0
-    te = int(sc.sum())
-    return {"value": round(te / dt / 1e9, 5), "unit": "GTEPS", "cores": thr, "kind": "port",
-            "sample": f"sources 0..{sample} of the c5 graph ({te} adjacency entries), "
-                      "oracle/oracle.c partial_bfs_all restatement", "seconds": round(dt, 3)}
+    tot, te, passes = 0.0, 0, 0
+    while passes < max_passes and (tot < min_seconds or passes < 2):
+        dt, t = _cpu_full_pass(O, g, thr)
+        tot, te, passes = tot + dt, te + t, passes + 1
+    return {"value": round(te / tot / 1e9, 5), "unit": "GTEPS", "cores": thr, "kind": "port",
+            "sample": f"full c5 workload (all {g.n} sources, {te // passes} adjacency entries) x "
+                      f"{passes} passes, oracle/oracle.c partial_bfs_all restatement",
+            "seconds": round(tot, 3)}
 
 
 # ---------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference algorithm's CPU implementation (oracle C port, all host
+    threads); one step = the full c5 workload, same metric as ours."""
     ws, rank, local = _dist_env()
     if rank != 0:
         return
@@ -453,26 +467,24 @@ def run_reference(args):
     O.build()
     g, _ = build_graph("c5")
     thr = O.max_threads()
-    sample = 400_000
     for _ in range(args.warmup):
-        O.partial_bfs_raw(g, K_NN, SEED, 0, 20_000, nthreads=thr)
+        _cpu_full_pass(O, g, thr)
     ts, te = [], 0
-    for i in range(args.steps):
-        s0 = (i * sample) % (g.n - sample)
-        t0 = time.perf_counter()
-        _, _, _, sc, _ = O.partial_bfs_raw(g, K_NN, SEED, s0, s0 + sample, nthreads=thr, work=True)
-        ts.append(time.perf_counter() - t0)
-        te += int(sc.sum())
+    for _ in range(args.steps):
+        dt, t = _cpu_full_pass(O, g, thr)
+        ts.append(dt)
+        te += t
     tot = sum(ts)
     v = te / tot / 1e9
     out = {"impl": "reference", "metric": "BFS-kNN GTEPS (partial BFS kNN, k=15)",
            "value": round(v, 5), "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-           "dtype": "int32", "data": "synthetic", "config": {"workload": WORKLOAD,
-                                                              "sample_sources_per_step": sample},
+           "dtype": "int32", "data": "synthetic (seeded RGG fixture, paper datasets absent)",
+           "config": {"workload": WORKLOAD, "n": g.n, "te_per_step": te // args.steps},
            "cpu_baseline": {"value": round(v, 5), "unit": "GTEPS", "cores": thr, "kind": "port",
-                            "sample": f"{sample} sources per step of the c5 graph"},
+                            "sample": f"full c5 workload (all {g.n} sources) per step, "
+                                      "oracle/oracle.c partial_bfs_all restatement"},
            "e2e": {"value": round(v, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

@@ -85,12 +85,17 @@ def _csr(g):
 # ----------------------------------------------------------------- C0 full
 def all_pairs_bfs(g, nthreads=1):
     """neighbors.py:120-134 / _kernels.py:33-57 -> int32 (n, n) matrix."""
+    return all_pairs_bfs_rows(g, np.arange(int(g.n)), nthreads)
+
+
+def all_pairs_bfs_rows(g, sources, nthreads=None):
+    """The rows of all_pairs_bfs for ``sources`` only (int32, INF32 unreachable)."""
     ip, ix = _csr(g)
     n = int(g.n)
-    out = np.empty((n, n), dtype=np.int32)
-    src = np.arange(n, dtype=np.int64)
-    lib().or_apsp_rows(n, _p(ip, _i64p), _p(ix, _i32p), _p(src, _i64p), n,
-                       _p(out, _i32p), nthreads)
+    src = np.ascontiguousarray(sources, dtype=np.int64)
+    out = np.empty((len(src), n), dtype=np.int32)
+    lib().or_apsp_rows(n, _p(ip, _i64p), _p(ix, _i32p), _p(src, _i64p), len(src),
+                       _p(out, _i32p), max_threads() if nthreads is None else nthreads)
     return out
 
 

@@ -27,11 +27,7 @@ def main(divs):
     src = z["sources"]
     g = gu.synth_graph("scale_free", 100000, seed=2, m0=3)
     O.build()
-    rows = np.empty((len(src), g.n), np.int32)
-    O.lib().or_apsp_rows(g.n, g.adj_indptr.ctypes.data_as(O._i64p),
-                         np.ascontiguousarray(g.adj_indices, np.int32).ctypes.data_as(O._i32p),
-                         src.astype(np.int64).ctypes.data_as(O._i64p), len(src),
-                         rows.ctypes.data_as(O._i32p), O.max_threads())
+    rows = O.all_pairs_bfs_rows(g, src)
     res = {"config": "c3 SL-GUMAP BA(100k, m0=3), random init, 200 epochs, 10% window; "
                      "sampled NP / stress over 2000 fixed sources",
            "reference": {"np_mean": float(z["np_"].mean()), "np_sd": float(z["np_"].std(ddof=1)),

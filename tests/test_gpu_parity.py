@@ -338,6 +338,33 @@ def test_quality_c1_vs_reference(gu):
     assert v.mean(axis=0)[2] <= ref.mean(axis=0)[2] + 4 * se[2]
 
 
+def test_quality_c3_sampled_vs_reference(gu, oracle):
+    """Check (c) at SL scale: sampled NP / stress (2000 fixed sources) of the
+    c3 SL-GUMAP layout vs the reference's 5 seeds (tests/golden/quality_c3.npz,
+    scripts/quality_c3.py for the full sweep)."""
+    from oracle.metrics import sampled_neighborhood_preservation, sampled_stress
+
+    z = load_golden("quality_c3.npz")
+    src = z["sources"]
+    g = gu.synth_graph("scale_free", 100000, seed=2, m0=3)
+    rows = oracle.all_pairs_bfs_rows(g, src)
+    vals = []
+    for seed in range(3):
+        _, knn = gu.partial_bfs(g, 15, seed=seed)
+        gk = gu.smooth_knn_weights(knn)
+        E = gk.edge_count
+        cfg = gu.OptimizerConfig(iterations=200, k=15, seed=seed,
+                                 samp=math.log(0.1 * E) / math.log(E))
+        lay = gu.optimize_sampled(gk, gu.random_init(g, seed, 10.0), cfg).coords
+        vals.append((sampled_neighborhood_preservation(lay, rows, src), sampled_stress(lay, rows, src)))
+    v = np.array(vals)
+    ref = np.stack([z["np_"], z["stress"]], axis=1)
+    print("check (c) c3 mean ratios gpu/ref [np, stress]:", v.mean(axis=0) / ref.mean(axis=0))
+    se = ref.std(axis=0, ddof=1) / math.sqrt(ref.shape[0]) + v.std(axis=0, ddof=1) / math.sqrt(v.shape[0])
+    assert v.mean(axis=0)[0] >= ref.mean(axis=0)[0] - 4 * se[0]
+    assert v.mean(axis=0)[1] <= ref.mean(axis=0)[1] + 4 * se[1]
+
+
 def test_sharded_knn_nccl_single_rank(gu):
     """The NCCL path of distributed.sharded_knn (all_gather of records) on a
     one-rank group: identical to the single-GPU kNN (partial and full)."""
