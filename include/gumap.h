@@ -35,6 +35,7 @@ extern "C" {
 int gu_version(void);                 /* ABI version, currently 1 */
 const char* gu_last_error(void);      /* thread-local message of the last failure */
 int gu_device_sync(void* stream);     /* cudaStreamSynchronize + error check */
+int gu_host_is_pinned(const void* p); /* 1 if p lies in page-locked host memory */
 
 /* ---------------------------------------------- C0+C1 partial BFS-kNN
  * Replaces _kernels.py:60-131 partial_bfs_all(indptr, indices, k, seed,

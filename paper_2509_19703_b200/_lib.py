@@ -31,6 +31,7 @@ SIGNATURES = {
     "gu_version": (ctypes.c_int, []),
     "gu_last_error": (ctypes.c_char_p, []),
     "gu_device_sync": (ctypes.c_int, [_vp]),
+    "gu_host_is_pinned": (ctypes.c_int, [_vp]),
     "gu_partial_bfs_workspace_size": (_c_sz, [_c_i64, _c_i64, _c_i32]),
     "gu_partial_bfs_knn": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i32, _c_u64, _c_i64, _c_i64,
                                           _vp, _vp, _vp, _vp, _vp, _c_sz, _c_i32, _vp]),

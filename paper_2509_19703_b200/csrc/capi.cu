@@ -152,6 +152,15 @@ extern "C" int gu_device_sync(void* stream) {
   return GU_OK;
 }
 
+extern "C" int gu_host_is_pinned(const void* ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();  // unregistered pageable memory on old drivers: clear it
+    return 0;
+  }
+  return a.type == cudaMemoryTypeHost ? 1 : 0;
+}
+
 extern "C" size_t gu_pack_records_workspace_size(int64_t nrows) { return scan_workspace(nrows); }
 
 extern "C" int gu_pack_records(int64_t nrows, int32_t k, const int32_t* rec_nbr,

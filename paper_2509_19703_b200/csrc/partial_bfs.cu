@@ -543,8 +543,11 @@ __device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
   return (int)r;
 }
 
+#ifndef TF_MINB
+#define TF_MINB 8
+#endif
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     pbfs_fast(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
               unsigned long long seed, long long src_begin, long long nsrc,
               int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
@@ -552,20 +555,37 @@ __global__ void __launch_bounds__(WARPS * 32)
               unsigned long long* __restrict__ work) {
   constexpr int HC = TF_HC;
   __shared__ __align__(16) int sm_hash[WARPS][HC];
-  __shared__ int sm_list[WARPS][TF_CAP2];
+  // +32: a chunk never writes past; +32 more: per-lane sink for the
+  // unconditional (branch-free) list store of lanes with nothing new
+  __shared__ int sm_list[WARPS][TF_CAP2 + 64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
   int* const hkey = sm_hash[warp];
   int* const lst = sm_list[warp];
   unsigned long long w_scanned = 0, w_expanded = 0;
-  auto claim = [&](int w) -> bool {
+  static_assert(TF_CAP2 + 32 + 1 + 32 <= (HC * 3) / 4, "ball budget must fit the hash");
+  // Warp-wide claim of distinct keys (one per lane, `lead` lanes only): one
+  // predicated CAS for everybody; the linear-probe loop runs only when some
+  // lane hit an occupied slot, so the common case has no divergence.
+  auto claim = [&](int w, bool lead) -> bool {
     unsigned h = hash_id(w) & (HC - 1);
-    for (;;) {
-      const int old = atomicCAS(&hkey[h], -1, w);
-      if (old == -1) return true;
-      if (old == w) return false;
-      h = (h + 1) & (HC - 1);
+    int old = w;  // predicated CAS (no branch): lanes with !lead keep old == w
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+        "@p atom.shared.cas.b32 %0, [%2], -1, %3;\n\t}"
+        : "+r"(old)
+        : "r"((unsigned)lead), "r"((unsigned)__cvta_generic_to_shared(&hkey[h])), "r"(w)
+        : "memory");
+    bool coll = old != -1 && old != w;
+    if (__any_sync(FULL, coll)) {
+      while (coll) {
+        h = (h + 1) & (HC - 1);
+        old = atomicCAS(&hkey[h], -1, w);
+        coll = old != -1 && old != w;
+      }
+      __syncwarp();
     }
+    return lead && old == -1;
   };
   for (long long item = (long long)blockIdx.x * WARPS + warp; item < nsrc;
        item += (long long)gridDim.x * WARPS) {
@@ -590,7 +610,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     __syncwarp();
     if (lane == 0) hkey[hash_id(s) & (HC - 1)] = s;
     __syncwarp();
-    if (lane < T0) claim(w1);
+    claim(w1, lane < T0);
     const unsigned long long fy_base = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
     if (T0 >= K) {
       // ---- level 1 reaches the budget: sorted adjacency, or a random subset
@@ -637,20 +657,15 @@ __global__ void __launch_bounds__(WARPS * 32)
       rn[lane] = w1;
       rd[lane] = 1;
     }
-    // ---- level 2: compact non-empty parents, prefix of their degrees
-    const unsigned nem = __ballot_sync(FULL, pd > 0);
-    const int nne = __popc(nem);
-    // compaction through the (still unused) list buffer: lane r gets the r-th
-    // non-empty parent
-    if (pd > 0) {
-      const int r = __popc(nem & lt);
-      lst[r] = pb;
-      lst[32 + r] = pd;
+    // ---- level 2: prefix of the parents' degrees.  In an undirected CSR a
+    // neighbour of s has s in its own list, so every parent is non-empty; a
+    // CSR that breaks this (one-sided entries) takes the generic tiers.
+    if (__any_sync(FULL, lane < T0 && pd <= 0)) {
+      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+      continue;
     }
-    __syncwarp();
-    const int cb = lane < nne ? lst[lane] : 0;
-    const int cdv = lane < nne ? lst[32 + lane] : 0;
-    __syncwarp();
+    const int nne = T0;
+    const int cb = pb, cdv = pd;
     const int inc = warp_incl_scan(cdv);
     const int cpre = inc - cdv;
     const int T = __shfl_sync(FULL, inc, 31);
@@ -659,37 +674,47 @@ __global__ void __launch_bounds__(WARPS * 32)
     // cbase = adjacency start - flattened start of the lane's parent, so a
     // candidate address is one shuffle and one add away
     const int cbase = cb - cpre;
-    auto load_chunk = [&](int t0, int pc, int& w, unsigned& m) {
+    // Raw candidate ids of chunk t0 (parent count of earlier chunks: pc).
+    // Lanes past T load indices[0] and keep it: they sit above every valid
+    // lane, so they are never a first occurrence and never claim.
+    auto load_chunk = [&](int t0, int pc, int& x, unsigned& m) {
       const unsigned off = (unsigned)(cpre - t0);
       m = __reduce_or_sync(FULL, (lane < nne && off < 32u) ? (1u << off) : 0u);
       const int p = pc + __popc(m & le_mask) - 1;
-      const int base = __shfl_sync(FULL, cbase, p & 31);
+      // 32-bit offset arithmetic (cbase may be negative; the sum never is)
+      const unsigned base = (unsigned)__shfl_sync(FULL, cbase, p & 31);
       const int t = t0 + lane;
-      w = t < T ? __ldg(indices + (base + t)) : -1;
+      x = __ldg(indices + (t < T ? base + (unsigned)t : 0u));
     };
-    int w;
-    unsigned m;
-    load_chunk(0, 0, w, m);
-    bool ovf = false;
-    for (int t0 = 0; t0 < T; t0 += 32) {
-      pcount += __popc(m);
-      int wn = -1;
-      unsigned mn = 0;
-      if (t0 + 32 < T) load_chunk(t0 + 32, pcount, wn, mn);
-      const unsigned grp = __match_any_sync(FULL, w);
-      const bool isnew = t0 + lane < T && lane == __ffs(grp) - 1 && claim(w);
+    // claim the chunk's first occurrences (queue order) and append them;
+    // true when the ball leaves the budget (the hash holds it: static_assert)
+    auto process = [&](int t0, int x) -> bool {
+      const unsigned grp = __match_any_sync(FULL, x);
+      const bool isnew = claim(x, t0 + lane < T && (grp & lt) == 0);
       const unsigned bal = __ballot_sync(FULL, isnew);
-      if (isnew) {
-        const int pos = nst + __popc(bal & lt);
-        if (pos < TF_CAP2) lst[pos] = w;
-      }
+      // nst <= TF_CAP2 here: in bounds; lanes with nothing new hit their sink
+      lst[isnew ? nst + __popc(bal & lt) : TF_CAP2 + 32 + lane] = x;
       nst += __popc(bal);
-      w = wn;
-      m = mn;
-      if (nst > TF_CAP2 || nst + T0 + 1 > (HC * 3) / 4) {  // ball above the budget
-        ovf = true;
-        break;
-      }
+      return nst > TF_CAP2;
+    };
+    // two chunk registers in ping-pong (unrolled by hand): the load of the
+    // next chunk stays in flight while this one is processed -- no register
+    // move or select touches an in-flight load result
+    int xa = 0, xb = 0;
+    unsigned ma = 0, mb = 0;
+    load_chunk(0, 0, xa, ma);
+    bool ovf = false;
+    for (int t0 = 0;;) {
+      pcount += __popc(ma);
+      if (t0 + 32 < T) load_chunk(t0 + 32, pcount, xb, mb);
+      if (process(t0, xa)) { ovf = true; break; }
+      t0 += 32;
+      if (t0 >= T) break;
+      pcount += __popc(mb);
+      if (t0 + 32 < T) load_chunk(t0 + 32, pcount, xa, ma);
+      if (process(t0, xb)) { ovf = true; break; }
+      t0 += 32;
+      if (t0 >= T) break;
     }
     const int remaining = K - T0;
     if (ovf || nst < remaining) {  // level 2 does not reach k (or too big): generic path

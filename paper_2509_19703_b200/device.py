@@ -9,6 +9,7 @@ calls on the same Graph (driver stages, benchmark steps) never re-upload.
 PyTorch is plumbing only here: device memory, streams, events.
 """
 
+import ctypes
 import warnings
 import weakref
 
@@ -123,6 +124,11 @@ def to_device(a, dtype, device):
         src = torch.from_numpy(a)
     if a.nbytes < _PIN_THRESHOLD:
         return src.to(device)
+    if _is_pinned(a):  # already page-locked: one DMA at link speed, no staging
+        dev = torch.empty(src.shape, dtype=src.dtype, device=device)
+        dev.copy_(src, non_blocking=True)
+        torch.cuda.current_stream(device).synchronize()  # the caller may reuse `a`
+        return dev
     # chunked, double-buffered: the host copy of chunk i+1 overlaps the DMA of i
     flat = src.reshape(-1)
     dev = torch.empty(flat.shape, dtype=src.dtype, device=device)
@@ -145,4 +151,10 @@ def to_device(a, dtype, device):
 
 
 _UPLOAD_CHUNK_BYTES = 32 << 20
+
+
+def _is_pinned(a):
+    """True when numpy array ``a`` lies in page-locked host memory (e.g. a view
+    of a torch pin_memory tensor or a cudaHostRegister'ed buffer)."""
+    return bool(_lib.load().gu_host_is_pinned(ctypes.c_void_p(a.ctypes.data)))
 

@@ -395,3 +395,27 @@ def test_sharded_knn_nccl_single_rank(gu):
         assert np.array_equal(knn2.dst, ref2.dst) and np.array_equal(knn2.dist, ref2.dist)
     finally:
         dist.destroy_process_group()
+
+
+def test_pinned_host_inputs(gu):
+    """Graph arrays in page-locked host memory take the single-DMA upload
+    path (device._is_pinned) and give the same records."""
+    import torch
+
+    from paper_2509_19703_b200.device import _is_pinned
+    from paper_2509_19703_b200.graph import Graph
+
+    g = gu.synth_graph("scale_free", 20000, seed=3, m0=3)
+
+    def pinned(a):
+        out = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True).numpy()
+        out[...] = a
+        return out
+
+    gp = Graph(n=g.n, m=g.m, adj_indptr=pinned(np.asarray(g.adj_indptr)),
+               adj_indices=pinned(np.asarray(g.adj_indices)), edges=g.edges)
+    assert _is_pinned(gp.adj_indices) and not _is_pinned(np.asarray(g.adj_indices))
+    _, a = gu.partial_bfs(g, 15, seed=7)
+    _, b = gu.partial_bfs(gp, 15, seed=7)
+    assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.dst, b.dst)
+    assert np.array_equal(a.dist, b.dist)
