@@ -546,6 +546,33 @@ __device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
 #ifndef TF_MINB
 #define TF_MINB 8
 #endif
+// Partial Fisher-Yates resolved in registers (no shared-memory swaps).  Lane
+// i < r holds its draw j_i (>= i), a_i = list[i] and a_j = list[j_i] of the
+// original list; the result is list[i] after the reference's r sequential
+// swaps swap(list[i], list[j_i]), i = 0..r-1.  Step k sends u_k -- the value
+// position k held just before it -- to position j_k; a later lane picks it up
+// as its own u when j_k is its position, and as the value it will take when
+// j_k is its draw (the last such step wins, as in the sequential loop).
+__device__ __forceinline__ int fy_registers(int r, int lane, int j, int a_i, int a_j) {
+  int u = a_i, take = a_j;
+  for (int k = 0; k + 1 < r; k++) {
+    const int jk = __shfl_sync(FULL, j, k);
+    const int uk = __shfl_sync(FULL, u, k);
+    if (lane > k) {
+      if (lane == jk) u = uk;
+      if (j == jk) take = uk;
+    }
+  }
+  return j == lane ? u : take;
+}
+
+// rank of v among the (distinct) values of lanes 0..r-1
+__device__ __forceinline__ int rank_in_warp(int r, int v) {
+  int rk = 0;
+  for (int q = 0; q < r; q++) rk += __shfl_sync(FULL, v, q) < v;
+  return rk;
+}
+
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     pbfs_fast(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
@@ -620,23 +647,12 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
           rd[lane] = 1;
         }
       } else {
-        if (lane < T0) lst[lane] = w1;
+        // the list is level 1 itself, one id per lane: all in registers
         int j = 0;
         if (lane < K) j = lane + umod64_tab(splitmix_at(fy_base, lane), T0 - lane);
-        __syncwarp();
-        for (int i = 0; i < K; i++) {
-          const int ji = __shfl_sync(FULL, j, i);
-          if (lane == 0) {
-            const int a = lst[i];
-            lst[i] = lst[ji];
-            lst[ji] = a;
-          }
-        }
-        __syncwarp();
+        const int v = fy_registers(K, lane, j, w1, __shfl_sync(FULL, w1, j & 31));
+        const int r = rank_in_warp(K, v);
         if (lane < K) {
-          const int v = lst[lane];
-          int r = 0;
-          for (int q = 0; q < K; q++) r += lst[q] < v;
           rn[r] = v;
           rd[r] = 1;
         }
@@ -686,34 +702,63 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       const int t = t0 + lane;
       x = __ldg(indices + (t < T ? base + (unsigned)t : 0u));
     };
-    // claim the chunk's first occurrences (queue order) and append them;
-    // true when the ball leaves the budget (the hash holds it: static_assert)
-    auto process = [&](int t0, int x) -> bool {
-      const unsigned grp = __match_any_sync(FULL, x);
-      const bool isnew = claim(x, t0 + lane < T && (grp & lt) == 0);
-      const unsigned bal = __ballot_sync(FULL, isnew);
+    // claim the first occurrences (queue order) of chunks t0 and t0 + 32 (when
+    // that one exists) and append them; true when the ball leaves the budget
+    // (the hash holds it: static_assert).  Both MATCHes are issued before the
+    // claims, and the second chunk's claims follow the first's, so each pair
+    // costs one dependent round trip instead of two.
+    auto process2 = [&](int t0, int xa, int xb) -> bool {
+      const bool two = t0 + 32 < T;  // warp-uniform
+      const unsigned ga = __match_any_sync(FULL, xa);
+      const unsigned gb = two ? __match_any_sync(FULL, xb) : 0u;
+      const bool na = claim(xa, t0 + lane < T && (ga & lt) == 0);
+      const unsigned ba = __ballot_sync(FULL, na);
       // nst <= TF_CAP2 here: in bounds; lanes with nothing new hit their sink
-      lst[isnew ? nst + __popc(bal & lt) : TF_CAP2 + 32 + lane] = x;
-      nst += __popc(bal);
+      lst[na ? nst + __popc(ba & lt) : TF_CAP2 + 32 + lane] = xa;
+      nst += __popc(ba);
+      if (!two) return nst > TF_CAP2;
+      if (nst > TF_CAP2) return true;
+      __syncwarp();  // chunk a's claims are visible to chunk b's
+      const bool nb = claim(xb, t0 + 32 + lane < T && (gb & lt) == 0);
+      const unsigned bb = __ballot_sync(FULL, nb);
+      lst[nb ? nst + __popc(bb & lt) : TF_CAP2 + 32 + lane] = xb;
+      nst += __popc(bb);
       return nst > TF_CAP2;
     };
-    // two chunk registers in ping-pong (unrolled by hand): the load of the
-    // next chunk stays in flight while this one is processed -- no register
+    // chunk registers in ping-pong pairs (unrolled by hand): the loads of the
+    // next pair stay in flight while this pair is processed -- no register
     // move or select touches an in-flight load result
-    int xa = 0, xb = 0;
-    unsigned ma = 0, mb = 0;
-    load_chunk(0, 0, xa, ma);
+    int x0 = 0, x1 = 0, x2 = 0, x3 = 0;
+    unsigned m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    load_chunk(0, 0, x0, m0);
+    pcount = __popc(m0);
+    if (32 < T) {
+      load_chunk(32, pcount, x1, m1);
+      pcount += __popc(m1);
+    }
     bool ovf = false;
     for (int t0 = 0;;) {
-      pcount += __popc(ma);
-      if (t0 + 32 < T) load_chunk(t0 + 32, pcount, xb, mb);
-      if (process(t0, xa)) { ovf = true; break; }
-      t0 += 32;
+      if (t0 + 64 < T) {
+        load_chunk(t0 + 64, pcount, x2, m2);
+        pcount += __popc(m2);
+        if (t0 + 96 < T) {
+          load_chunk(t0 + 96, pcount, x3, m3);
+          pcount += __popc(m3);
+        }
+      }
+      if (process2(t0, x0, x1)) { ovf = true; break; }
+      t0 += 64;
       if (t0 >= T) break;
-      pcount += __popc(mb);
-      if (t0 + 32 < T) load_chunk(t0 + 32, pcount, xa, ma);
-      if (process(t0, xb)) { ovf = true; break; }
-      t0 += 32;
+      if (t0 + 64 < T) {
+        load_chunk(t0 + 64, pcount, x0, m0);
+        pcount += __popc(m0);
+        if (t0 + 96 < T) {
+          load_chunk(t0 + 96, pcount, x1, m1);
+          pcount += __popc(m1);
+        }
+      }
+      if (process2(t0, x2, x3)) { ovf = true; break; }
+      t0 += 64;
       if (t0 >= T) break;
     }
     const int remaining = K - T0;
@@ -723,23 +768,14 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       continue;
     }
     __syncwarp();
+    int v = lst[lane];
     if (nst > remaining) {
-      int j = 0;
+      int j = lane;
       if (lane < remaining) j = lane + umod64_tab(splitmix_at(fy_base, lane), nst - lane);
-      for (int i = 0; i < remaining; i++) {
-        const int ji = __shfl_sync(FULL, j, i);
-        if (lane == 0) {
-          const int a = lst[i];
-          lst[i] = lst[ji];
-          lst[ji] = a;
-        }
-      }
-      __syncwarp();
+      v = fy_registers(remaining, lane, j, v, lst[j]);
     }
+    const int r = rank_in_warp(remaining, v);
     if (lane < remaining) {
-      const int v = lst[lane];
-      int r = 0;
-      for (int q = 0; q < remaining; q++) r += lst[q] < v;
       rn[T0 + r] = v;
       rd[T0 + r] = 2;
     }
