@@ -1,6 +1,6 @@
 // Microbenchmark: per-SM throughput of warp collectives used by the partial
 // BFS fast tier (MATCH.ANY, VOTE.ANY/ballot, REDUX.OR, SHFL, shared CAS).
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mm scripts/micro_match.cu && /tmp/mm
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/_micro_match scripts/micro_match.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 
