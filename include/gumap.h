@@ -167,6 +167,40 @@ int gu_sgd_replay_f64(int64_t n, double* coords, const int32_t* e_src, const int
                       const int64_t* wave_items, const int64_t* wave_offsets,
                       int64_t n_waves, void* stream);
 
+
+/* ----------------------------------------- layout-quality metrics (8(f) 1)
+ * Restate metrics.py:41-190 on the GPU.  coords_xy: float64 (n, 2) row-major.
+ * gu_stress: both passes of metrics.py:106-131 over GPU BFS rows (batches of
+ * at most row_budget_bytes), out3 (device, 3 doubles) = (sum of the stress
+ * terms, scale, unreachable flag); stress = out3[0] / (n*n - n). */
+size_t gu_stress_workspace_size(int64_t n, size_t row_budget_bytes);
+int gu_stress(int64_t n, const int32_t* indptr, const int32_t* indices,
+              const double* coords_xy, int32_t rescale, size_t row_budget_bytes,
+              double* out3, void* workspace, size_t ws_bytes, void* stream);
+/* count_crossings (metrics.py:176-190, _kernels.py:244-296): exact count of
+ * unordered edge pairs (edges int32 (m, 2)) whose open segments cross.
+ * gu_crossings_grid writes a g x g square grid over the coordinates' bounding
+ * box into grid_out (gu_grid_bytes); gu_crossings_incidences gives per-edge
+ * cell counts (int64[m]) whose sum n_inc sizes gu_crossings' workspace;
+ * out_count: device uint64. */
+size_t gu_grid_bytes(void);
+int gu_crossings_grid(int64_t n, const double* coords_xy, int32_t g, void* grid_out,
+                      void* stream);
+int gu_crossings_incidences(int64_t m, const int32_t* edges, const double* coords_xy,
+                            const void* grid, int64_t* out_counts, void* stream);
+size_t gu_crossings_workspace_size(int64_t m, int64_t n_inc, int32_t g);
+int gu_crossings(int64_t m, const int32_t* edges, const double* coords_xy, const void* grid,
+                 int32_t g, int64_t n_inc, uint64_t* out_count, void* workspace,
+                 size_t ws_bytes, void* stream);
+/* neighborhood_preservation (metrics.py:41-79): out_sum (device double) = the
+ * sum over v of |ball_r(v) & nearest_q(v)| / |union|; the caller divides by
+ * n.  slots = concurrent warps, each with 2n ints of scratch. */
+size_t gu_np_workspace_size(int64_t n, int32_t slots);
+int gu_neighborhood_preservation(int64_t n, const int32_t* indptr, const int32_t* indices,
+                                 const double* coords_xy, int32_t r, int32_t slots,
+                                 double* out_sum, void* workspace, size_t ws_bytes,
+                                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,7 +42,7 @@ def neighborhood_preservation(g, coords, hop=None, r=2):
     return total / n
 
 
-def stress(g, coords, hop):
+def stress(g, coords, hop, rescale=True):
     n = g.n
     coords = np.asarray(coords, np.float64)
     hop = np.asarray(hop, np.float64)
@@ -50,13 +50,15 @@ def stress(g, coords, hop):
     s_num = 0.0
     s_den = 0.0
     for start in range(0, n, chunk):
+        if not rescale:
+            break
         stop = min(start + chunk, n)
         delta = cdist(coords[start:stop], coords)
         d = hop[start:stop].copy()
         np.fill_diagonal(d[:, start:stop], np.inf)
         s_num += float((delta / d).sum())
         s_den += float((delta * delta / (d * d)).sum())
-    scale = s_num / s_den if s_den > 0 else 1.0
+    scale = s_num / s_den if (rescale and s_den > 0) else 1.0
     total = 0.0
     for start in range(0, n, chunk):
         stop = min(start + chunk, n)

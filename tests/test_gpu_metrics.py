@@ -1,0 +1,96 @@
+"""GPU layout-quality metrics (csrc/metrics.cu) vs the
+reference's own values on its own c1 layouts (tests/golden/quality_c1.npz)
+and vs the oracle restatements (oracle/metrics.py, pinned to the reference)
+on random graphs and layouts, degenerate ones included.
+
+Tolerances: crossings exact; neighborhood preservation 1e-12 absolute (a
+single differing rank moves it by >= 1/(n q), far above); stress 1e-12
+relative (summation order only)."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+NP_ABS_TOL = 1e-12
+STRESS_REL_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def gu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2509_19703_b200 as gu
+    return gu
+
+
+def _layout(gu, coords):
+    return gu.Layout(coords=np.asarray(coords, np.float64))
+
+
+def test_metrics_on_reference_c1_layouts(gu):
+    from paper_2509_19703_b200 import metrics as M
+
+    z = load_golden("quality_c1.npz")
+    g = gu.synth_graph("grid", 2500)
+    for i, lay in enumerate((z["layout0"], z["layout1"])):
+        L = _layout(gu, lay)
+        assert abs(M.neighborhood_preservation(g, L) - z["np_"][i]) < NP_ABS_TOL
+        s = M.stress(g, L)
+        assert abs(s - z["stress"][i]) <= STRESS_REL_TOL * abs(z["stress"][i])
+        assert M.count_crossings(g, L) == int(z["crossings"][i])
+
+
+def _cases(gu):
+    from paper_2509_19703_b200.fixtures import random_connected_graph
+    from paper_2509_19703_b200.graph import graph_from_edges
+
+    rng = np.random.default_rng(20261019)
+    graphs = [gu.synth_graph("grid", 400), gu.synth_graph("scale_free", 600, seed=9, m0=2)]
+    for _ in range(3):
+        n, edges = random_connected_graph(rng, n_max=300)
+        graphs.append(graph_from_edges(n, edges))
+    for g in graphs:
+        yield g, rng.uniform(-10, 10, size=(g.n, 2))
+        # integer lattice: duplicate points, collinear and touching segments
+        yield g, rng.integers(0, 6, size=(g.n, 2)).astype(np.float64)
+
+
+def test_metrics_vs_oracle_random(gu, oracle):
+    from oracle import metrics as OM
+    from paper_2509_19703_b200 import metrics as M
+
+    for g, coords in _cases(gu):
+        L = _layout(gu, coords)
+        hop = oracle.all_pairs_bfs(g, nthreads=4)
+        for r in (1, 2, 3):
+            a = M.neighborhood_preservation(g, L, r=r)
+            b = OM.neighborhood_preservation(g, coords, hop.astype(np.float64), r=r)
+            assert abs(a - b) < NP_ABS_TOL, (g.n, r, a, b)
+        for rescale in (True, False):
+            a = M.stress(g, L, rescale=rescale)
+            b = OM.stress(g, coords, hop, rescale=rescale)
+            assert abs(a - b) <= STRESS_REL_TOL * abs(b), (g.n, rescale, a, b)
+        assert M.count_crossings(g, L) == OM.count_crossings(g, coords), g.n
+
+
+def test_metrics_errors_and_small(gu):
+    from paper_2509_19703_b200 import metrics as M
+    from paper_2509_19703_b200.graph import graph_from_edges
+
+    g = graph_from_edges(4, [(0, 1), (2, 3)])
+    L = _layout(gu, np.arange(8, dtype=np.float64).reshape(4, 2))
+    with pytest.raises(M.MetricError):
+        M.stress(g, L)
+    with pytest.raises(M.MetricError):
+        M.neighborhood_preservation(g, _layout(gu, np.zeros((3, 2))))
+    one = graph_from_edges(1, [])
+    assert M.neighborhood_preservation(one, _layout(gu, np.zeros((1, 2)))) == 1.0
+    assert M.stress(one, _layout(gu, np.zeros((1, 2)))) == 0.0
+    assert M.count_crossings(g, L) == 0  # two disjoint parallel segments
+    x = graph_from_edges(4, [(0, 1), (2, 3)])
+    cross = _layout(gu, np.array([[0, 0], [2, 2], [0, 2], [2, 0]], np.float64))
+    assert M.count_crossings(x, cross) == 1
