@@ -103,21 +103,23 @@ def _cross_exact(p1, p2, p3, p4):
     return False
 
 
-def count_crossings(g, coords, block=256):
-    """Exact number of unordered edge pairs whose open segments cross."""
+def count_crossings(g, coords, block=256, rows=None):
+    """Exact number of unordered edge pairs whose open segments cross
+    (``rows`` = (i0, i1): only pairs whose first edge lies in [i0, i1))."""
     coords = np.asarray(coords, np.float64)
     e = np.asarray(g.edges, np.int64)
     m = e.shape[0]
     if m < 2:
         return 0
+    r0, r1 = (0, m) if rows is None else rows
     P = coords[e[:, 0]]
     Q = coords[e[:, 1]]
     lox, hix = np.minimum(P[:, 0], Q[:, 0]), np.maximum(P[:, 0], Q[:, 0])
     loy, hiy = np.minimum(P[:, 1], Q[:, 1]), np.maximum(P[:, 1], Q[:, 1])
     certain = 0
     amb = []
-    for i0 in range(0, m, block):
-        i1 = min(i0 + block, m)
+    for i0 in range(r0, r1, block):
+        i1 = min(i0 + block, r1)
         I = np.arange(i0, i1)[:, None]
         J = np.arange(m)[None, :]
         mask = J > I

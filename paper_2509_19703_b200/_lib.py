@@ -28,8 +28,8 @@ _vp = ctypes.c_void_p
 
 # name -> (restype, argtypes), mirrors include/gumap.h
 SIGNATURES = {
-    "gu_stress_workspace_size": (_c_sz, [_c_i64, _c_sz]),
-    "gu_stress": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i32, _c_sz, _vp, _vp, _c_sz, _vp]),
+    "gu_stress_workspace_size": (_c_sz, [_c_i64]),
+    "gu_stress": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i32, _vp, _vp, _c_sz, _vp]),
     "gu_grid_bytes": (_c_sz, []),
     "gu_crossings_grid": (ctypes.c_int, [_c_i64, _vp, _c_i32, _vp, _vp]),
     "gu_crossings_incidences": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp]),

@@ -13,6 +13,13 @@
 
 namespace gu {
 
+// ------------------------------------------- internal cross-file launchers
+// full_bfs.cu: one fused stress pass over every source (metrics.cu)
+int stress_bfs_pass(int64_t n, const int32_t* indptr, const int32_t* indices, const double* xy,
+                    int pass2, const double* scale, void* acc, int* flag, void* workspace,
+                    size_t ws_bytes, int ctas, cudaStream_t st);
+size_t stress_bfs_workspace(int64_t n, int ctas);
+
 // --------------------------------------------------------------- errors
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);

@@ -29,7 +29,20 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int FB_THREADS = 512;
 constexpr int FB_WARPS = FB_THREADS / 32;
 
-enum Mode { MODE_KNN = 0, MODE_APSP = 1 };
+enum Mode { MODE_KNN = 0, MODE_APSP = 1, MODE_STRESS = 2 };
+
+// MODE_STRESS (metrics.py:106-131 fused into the BFS): every (source, vertex)
+// pair reached at level d adds its stress terms to per-thread float64 sums --
+// the hop rows never exist.  pass2 = 0: (delta/d, delta^2/d^2) for the scale;
+// pass2 = 1: (1 - delta*scale/d)^2.  acc[blockIdx.x] receives the CTA's sums
+// (fixed ownership: deterministic); flag is set if a source misses vertices.
+struct StressArgs {
+  const double2* xy;
+  const double* scale;
+  double2* acc;
+  int* flag;
+  int pass2;
+};
 
 struct FbShared {
   int cnt[64];
@@ -40,7 +53,24 @@ struct FbShared {
   int lastlvl[64];
   unsigned keep[2];
   unsigned long long active;
+  double2 sxy[64];
+  double red[2][FB_WARPS];
 };
+
+// scipy cdist (no contraction) and the stress terms of one pair at level d
+__device__ __forceinline__ void stress_term(double2 p, double2 q, int lvl, const StressArgs& sa,
+                                            double scale, double& a, double& b) {
+  const double dx = __dsub_rn(p.x, q.x), dy = __dsub_rn(p.y, q.y);
+  const double delta = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+  const double d = (double)lvl;
+  if (!sa.pass2) {
+    a = __dadd_rn(a, __ddiv_rn(delta, d));
+    b = __dadd_rn(b, __ddiv_rn(__dmul_rn(delta, delta), __dmul_rn(d, d)));
+  } else {
+    const double u = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(delta, scale), d));
+    a = __dadd_rn(a, __dmul_rn(u, u));
+  }
+}
 
 __device__ __forceinline__ void sort_small_ids(int* ids, int m) {
   // ascending sort of m ids in global/shared memory by one warp
@@ -76,8 +106,10 @@ __global__ void __launch_bounds__(FB_THREADS)
                  int K, unsigned long long seed, long long src_begin, long long src_end,
                  int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
                  int* __restrict__ out_rows, char* __restrict__ ws, size_t slot_bytes, int L,
-                 unsigned long long* __restrict__ work) {
+                 unsigned long long* __restrict__ work, StressArgs sa) {
   __shared__ FbShared sh;
+  double st_a = 0.0, st_b = 0.0;
+  const double st_scale = (MODE == MODE_STRESS && sa.pass2) ? *sa.scale : 1.0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned long long* vis = reinterpret_cast<unsigned long long*>(ws + blockIdx.x * slot_bytes);
   unsigned long long* stack = vis + n;
@@ -90,7 +122,7 @@ __global__ void __launch_bounds__(FB_THREADS)
     const long long s0 = src_begin + bi * 64;
     const int nb = (int)min(64LL, src_end - s0);
     auto level = [&](int l) -> unsigned long long* {
-      return stack + (size_t)(MODE == MODE_APSP ? (l & 1) : l) * n;
+      return stack + (size_t)(MODE != MODE_KNN ? (l & 1) : l) * n;
     };
     unsigned long long* l1 = level(1);
     for (int v = tid; v < n; v += FB_THREADS) {
@@ -103,6 +135,7 @@ __global__ void __launch_bounds__(FB_THREADS)
         for (int v = tid; v < n; v += FB_THREADS) row[v] = (v == (int)(s0 + b)) ? 0 : GU_INF32;
       }
     }
+    if (MODE == MODE_STRESS && tid < nb) sh.sxy[tid] = sa.xy[s0 + tid];
     if (tid < 64) {
       sh.cnt[tid] = 0;
       sh.cum[tid] = 0;
@@ -127,6 +160,7 @@ __global__ void __launch_bounds__(FB_THREADS)
         int w = __ldg(indices + p);
         atomicOr(&l1[w], 1ull << b);
         if (MODE == MODE_APSP) row[w] = 1;
+        if (MODE == MODE_STRESS) stress_term(sh.sxy[b], sa.xy[w], 1, sa, st_scale, st_a, st_b);
       }
     }
     __syncthreads();
@@ -202,6 +236,8 @@ __global__ void __launch_bounds__(FB_THREADS)
           }
           if (MODE == MODE_APSP && ((nw >> b) & 1ull))
             out_rows[(s0 - src_begin + b) * (long long)n + v] = nl;
+          if (MODE == MODE_STRESS && ((nw >> b) & 1ull))
+            stress_term(sh.sxy[b], sa.xy[v], nl, sa, st_scale, st_a, st_b);
         }
       }
       if (my_cnt0) atomicAdd(&sh.cnt[lane], my_cnt0);
@@ -210,6 +246,7 @@ __global__ void __launch_bounds__(FB_THREADS)
       l = nl;
       if (MODE == MODE_KNN && l >= L) break;  // unreachable by construction
     }
+    if (MODE == MODE_STRESS && tid < nb && sh.cum[tid] + 1 < n) atomicOr(sa.flag, 1);
     if (MODE == MODE_KNN) {
       // ---- selection, one warp per source
       int* perm = perm_base + (size_t)warp * n;
@@ -318,6 +355,25 @@ __global__ void __launch_bounds__(FB_THREADS)
       }
     }
     __syncthreads();
+  }
+  if (MODE == MODE_STRESS) {
+    for (int o = 16; o > 0; o >>= 1) {
+      st_a += __shfl_down_sync(FULL, st_a, o);
+      st_b += __shfl_down_sync(FULL, st_b, o);
+    }
+    if (lane == 0) {
+      sh.red[0][warp] = st_a;
+      sh.red[1][warp] = st_b;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double x = 0.0, y = 0.0;
+      for (int i = 0; i < FB_WARPS; i++) {
+        x += sh.red[0][i];
+        y += sh.red[1][i];
+      }
+      sa.acc[blockIdx.x] = make_double2(x, y);
+    }
   }
   // TE is accumulated per thread; reduce per warp
   te = warp_sum(te);
@@ -445,6 +501,31 @@ size_t slot_bytes_for(long long n, int L, bool knn) {
 int levels_for(int k, bool knn) { return knn ? k + 2 : 2; }
 
 }  // namespace
+
+// one stress pass over every source (metrics.cu); acc: >= ctas double2
+int stress_bfs_pass(int64_t n, const int32_t* indptr, const int32_t* indices, const double* xy,
+                    int pass2, const double* scale, void* acc, int* flag, void* workspace,
+                    size_t ws_bytes, int ctas, cudaStream_t st) {
+  const long long nbatches = (n + 63) / 64;
+  if (ctas > nbatches) ctas = (int)nbatches;
+  if (ctas < 1) ctas = 1;
+  const size_t slot = slot_bytes_for(n, levels_for(0, false), false);
+  if (!workspace || ws_bytes < slot * (size_t)ctas) {
+    set_error("stress BFS: workspace %zu < %zu", ws_bytes, slot * (size_t)ctas);
+    return GU_ERR_WORKSPACE;
+  }
+  StressArgs sa{(const double2*)xy, scale, (double2*)acc, flag, pass2};
+  msbfs_kernel<MODE_STRESS><<<(unsigned)ctas, FB_THREADS, 0, st>>>(
+      (int)n, indptr, indices, 0, 0, 0, n, nullptr, nullptr, nullptr, nullptr, (char*)workspace,
+      slot, levels_for(0, false), nullptr, sa);
+  GU_CHECK_LAUNCH("msbfs_kernel<stress>");
+  return GU_OK;
+}
+
+size_t stress_bfs_workspace(int64_t n, int ctas) {
+  return slot_bytes_for(n, levels_for(0, false), false) * (size_t)(ctas > 0 ? ctas : 1);
+}
+
 }  // namespace gu
 
 using namespace gu;
@@ -486,11 +567,11 @@ static int launch_msbfs(bool knn, int64_t n, const int32_t* indptr, const int32_
   if (knn) {
     msbfs_kernel<MODE_KNN><<<(unsigned)bif, FB_THREADS, 0, st>>>(
         (int)n, indptr, indices, k, seed, src_begin, src_end, out_nbr, out_dist, out_count,
-        nullptr, (char*)workspace, slot, L, (unsigned long long*)work);
+        nullptr, (char*)workspace, slot, L, (unsigned long long*)work, StressArgs{});
   } else {
     msbfs_kernel<MODE_APSP><<<(unsigned)bif, FB_THREADS, 0, st>>>(
         (int)n, indptr, indices, 0, 0, src_begin, src_end, nullptr, nullptr, nullptr, out_rows,
-        (char*)workspace, slot, L, (unsigned long long*)work);
+        (char*)workspace, slot, L, (unsigned long long*)work, StressArgs{});
   }
   GU_CHECK_LAUNCH("msbfs_kernel");
   return GU_OK;

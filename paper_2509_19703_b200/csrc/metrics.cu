@@ -54,60 +54,10 @@ struct Carve {
 };
 
 // ================================================================= stress
+// The pair terms are accumulated inside the bitset BFS (full_bfs.cu
+// MODE_STRESS): two passes over every source, no hop rows in memory.
 constexpr int ST_THREADS = 256;
-constexpr int ST_TILE = ST_THREADS * 8;  // columns per tile
-constexpr int ST_BLOCKS = 148 * 8;
-constexpr int ST_BIF = 148 * 2;  // 64-source BFS batches in flight
-
-// pass 1 (scale terms) or pass 2 (stress terms) over a batch of BFS rows.
-// acc[block] += this block's sums: fixed block ownership across the batch
-// launches of one stream keeps the result deterministic.
-template <bool PASS2>
-__global__ void __launch_bounds__(ST_THREADS)
-    stress_rows(const int* __restrict__ rows, int row0, int nrows, int n,
-                const double2* __restrict__ xy, const double* __restrict__ scale,
-                double2* __restrict__ acc, int* __restrict__ unreachable) {
-  __shared__ double sh[ST_THREADS / 32];
-  const double s = PASS2 ? *scale : 1.0;
-  double a = 0.0, b = 0.0;
-  bool bad = false;
-  const int tpr = (n + ST_TILE - 1) / ST_TILE;
-  const long long ntiles = (long long)nrows * tpr;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int r = (int)(t / tpr);
-    const int c0 = (int)(t - (long long)r * tpr) * ST_TILE;
-    const int c1 = min(c0 + ST_TILE, n);
-    const int src = row0 + r;
-    const double2 ps = xy[src];
-    const int* row = rows + (long long)r * n;
-    for (int j = c0 + (int)threadIdx.x; j < c1; j += ST_THREADS) {
-      if (j == src) continue;  // the reference's diagonal: d = inf, term 0
-      const int h = __ldg(row + j);
-      if (h == GU_INF32) {
-        bad = true;
-        continue;
-      }
-      const double d = (double)h;
-      const double delta = cdist_xy(ps, xy[j]);
-      if (!PASS2) {
-        a = __dadd_rn(a, __ddiv_rn(delta, d));
-        b = __dadd_rn(b, __ddiv_rn(__dmul_rn(delta, delta), __dmul_rn(d, d)));
-      } else {
-        const double u = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(delta, s), d));
-        a = __dadd_rn(a, __dmul_rn(u, u));
-      }
-    }
-  }
-  if (bad) atomicOr(unreachable, 1);
-  const double sa = block_sum(a, sh);
-  const double sb = PASS2 ? 0.0 : block_sum(b, sh);
-  if (threadIdx.x == 0) {
-    double2 v = acc[blockIdx.x];
-    v.x += sa;
-    v.y += sb;
-    acc[blockIdx.x] = v;
-  }
-}
+constexpr int ST_CTAS = 148 * 2;  // 64-source BFS batches in flight
 
 __global__ void reduce_acc(const double2* __restrict__ acc, int nb, double2* __restrict__ out) {
   __shared__ double sh[ST_THREADS / 32];
@@ -127,7 +77,7 @@ __global__ void stress_scale(const double2* __restrict__ sums, int rescale, doub
   *scale = (rescale && v.y > 0.0) ? v.x / v.y : 1.0;
 }
 
-// out[0] = sum of terms, out[1] = scale, out[2] = unreachable flag (as double)
+// out[0] = sum of the stress terms, out[1] = scale, out[2] = unreachable flag
 __global__ void stress_finish(const double2* __restrict__ sums, const double* __restrict__ scale,
                               const int* __restrict__ flag, double* __restrict__ out) {
   out[0] = sums[1].x;
@@ -136,29 +86,20 @@ __global__ void stress_finish(const double2* __restrict__ sums, const double* __
 }
 
 struct StressWs {
-  char* apsp;
-  int* rows;
+  char* bfs;
+  size_t bfs_bytes;
   double2* acc;
   double2* sums;
   double* scale;
   int* flag;
 };
 
-long long stress_batch_rows(long long n, size_t budget) {
-  long long b = (long long)(budget / (4 * (size_t)(n > 0 ? n : 1)));
-  b = (b / 64) * 64;
-  if (b < 64) b = 64;
-  const long long full = ((n + 63) / 64) * 64;
-  return b > full ? full : b;
-}
-
-size_t stress_layout(long long n, size_t budget, char* base, StressWs* ws) {
-  const long long batch = stress_batch_rows(n, budget);
+size_t stress_layout(long long n, char* base, StressWs* ws) {
   Carve c{base};
   StressWs w;
-  w.apsp = c.take<char>(gu_full_bfs_workspace_size(n, 0, ST_BIF));
-  w.rows = c.take<int>((size_t)batch * (size_t)n);
-  w.acc = c.take<double2>(ST_BLOCKS);
+  w.bfs_bytes = stress_bfs_workspace(n, ST_CTAS);
+  w.bfs = c.take<char>(w.bfs_bytes);
+  w.acc = c.take<double2>(ST_CTAS);
   w.sums = c.take<double2>(2);
   w.scale = c.take<double>(1);
   w.flag = c.take<int>(1);
@@ -759,49 +700,34 @@ int np_grid_side(long long n) {
 using namespace gu;
 
 // ------------------------------------------------------------------ stress
-extern "C" size_t gu_stress_workspace_size(int64_t n, size_t row_budget_bytes) {
-  return stress_layout(n, row_budget_bytes, nullptr, nullptr);
-}
+extern "C" size_t gu_stress_workspace_size(int64_t n) { return stress_layout(n, nullptr, nullptr); }
 
 extern "C" int gu_stress(int64_t n, const int32_t* indptr, const int32_t* indices,
-                         const double* coords_xy, int32_t rescale, size_t row_budget_bytes,
-                         double* out3, void* workspace, size_t ws_bytes, void* stream) {
+                         const double* coords_xy, int32_t rescale, double* out3, void* workspace,
+                         size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 2 || n >= INT_MAX) {
     set_error("gu_stress: n=%lld out of range (n < 2 is answered by the caller)", (long long)n);
     return GU_ERR_ARG;
   }
   StressWs ws;
-  const size_t need = stress_layout(n, row_budget_bytes, (char*)workspace, &ws);
+  const size_t need = stress_layout(n, (char*)workspace, &ws);
   if (!workspace || ws_bytes < need) {
     set_error("gu_stress: workspace %zu < %zu", ws_bytes, need);
     return GU_ERR_WORKSPACE;
   }
-  const long long batch = stress_batch_rows(n, row_budget_bytes);
-  const size_t apsp_bytes = gu_full_bfs_workspace_size(n, 0, ST_BIF);
-  const double2* xy = (const double2*)coords_xy;
   GU_CHECK(cudaMemsetAsync(ws.flag, 0, sizeof(int), st));
   GU_CHECK(cudaMemsetAsync(ws.sums, 0, 2 * sizeof(double2), st));
+  GU_CHECK(cudaMemsetAsync(ws.acc, 0, sizeof(double2) * ST_CTAS, st));
   if (!rescale) {  // scale = 1 before the only pass
     stress_scale<<<1, 1, 0, st>>>(ws.sums, 0, ws.scale);
     GU_CHECK_LAUNCH("stress_scale");
   }
   for (int pass = rescale ? 0 : 1; pass < 2; pass++) {
-    GU_CHECK(cudaMemsetAsync(ws.acc, 0, sizeof(double2) * ST_BLOCKS, st));
-    for (long long r0 = 0; r0 < n; r0 += batch) {
-      const long long r1 = r0 + batch < n ? r0 + batch : n;
-      const int rc = gu_apsp_rows(n, indptr, indices, r0, r1, ws.rows, ws.apsp, apsp_bytes, ST_BIF,
-                                  stream);
-      if (rc != GU_OK) return rc;
-      if (pass == 0)
-        stress_rows<false><<<ST_BLOCKS, ST_THREADS, 0, st>>>(ws.rows, (int)r0, (int)(r1 - r0),
-                                                            (int)n, xy, ws.scale, ws.acc, ws.flag);
-      else
-        stress_rows<true><<<ST_BLOCKS, ST_THREADS, 0, st>>>(ws.rows, (int)r0, (int)(r1 - r0),
-                                                           (int)n, xy, ws.scale, ws.acc, ws.flag);
-      GU_CHECK_LAUNCH("stress_rows");
-    }
-    reduce_acc<<<1, ST_THREADS, 0, st>>>(ws.acc, ST_BLOCKS, ws.sums + pass);
+    const int rc = stress_bfs_pass(n, indptr, indices, coords_xy, pass, ws.scale, ws.acc, ws.flag,
+                                   ws.bfs, ws.bfs_bytes, ST_CTAS, st);
+    if (rc != GU_OK) return rc;
+    reduce_acc<<<1, ST_THREADS, 0, st>>>(ws.acc, ST_CTAS, ws.sums + pass);
     GU_CHECK_LAUNCH("reduce_acc");
     if (pass == 0) {
       stress_scale<<<1, 1, 0, st>>>(ws.sums, rescale, ws.scale);

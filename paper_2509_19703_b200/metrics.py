@@ -8,7 +8,8 @@ Drop-in for /root/reference/pkg/src/graph_umap/metrics.py's hot metrics:
 
 Same arguments, results and errors (MetricError on a layout / graph mismatch
 and on a disconnected graph for stress).  Every metric runs in libgumap.so
-(csrc/metrics.cu): the r-hop balls and hop rows by GPU BFS, layout-space
+(csrc/metrics.cu): the r-hop balls by GPU BFS, stress fused into the bitset
+BFS (no hop rows in memory), layout-space
 ranks with scipy cdist's float64 distances and stable id tie-break, exact
 crossing predicates.  The proximity-graph shape score is out of scope
 (DESIGN.md).
@@ -22,8 +23,7 @@ import torch
 from . import _lib
 from .device import device_csr, require_cuda, stream_ptr, workspace
 
-# scratch budgets (bytes): BFS rows per stress batch, NP per-warp balls
-STRESS_ROW_BUDGET = 2 << 30
+# scratch budget (bytes) for the NP per-warp balls
 NP_SCRATCH_BUDGET = 2 << 30
 NP_MAX_SLOTS = 148 * 64
 
@@ -90,11 +90,10 @@ def stress(g, layout, rescale=True):
     csr = device_csr(g, dev)
     xy = _coords(layout, dev)
     lib = _lib.load()
-    ws = workspace(lib.gu_stress_workspace_size(n, STRESS_ROW_BUDGET), dev)
+    ws = workspace(lib.gu_stress_workspace_size(n), dev)
     out = torch.zeros(3, dtype=torch.float64, device=dev)
     _lib.call("gu_stress", n, _lib.ptr(csr.indptr), _lib.ptr(csr.indices), _lib.ptr(xy),
-              1 if rescale else 0, STRESS_ROW_BUDGET, _lib.ptr(out), _lib.ptr(ws), ws.numel(),
-              stream_ptr(dev))
+              1 if rescale else 0, _lib.ptr(out), _lib.ptr(ws), ws.numel(), stream_ptr(dev))
     total, _scale, unreachable = out.tolist()
     if unreachable:
         raise MetricError("stress requires a connected graph")

@@ -308,6 +308,119 @@ def gen_quality_c3(nseeds=5):
     save("quality_c3.npz", np_=v[:, 0], stress=v[:, 1], sources=src)
 
 
+
+# ---- exact check (c) values at c3: workers for a process pool (top level)
+_Q = {}
+
+
+def _q_init(indptr, indices, coords, edges):
+    from oracle import oracle as O
+    _Q.update(indptr=indptr, indices=indices, coords=coords, edges=edges, O=O)
+
+
+def _q_rows(lo, hi):
+    O = _Q["O"]
+    n = _Q["indptr"].shape[0] - 1
+    src = np.arange(lo, hi, dtype=np.int64)
+    rows = np.empty((hi - lo, n), np.int32)
+    O.lib().or_apsp_rows(n, _Q["indptr"].ctypes.data_as(O._i64p),
+                         _Q["indices"].ctypes.data_as(O._i32p), src.ctypes.data_as(O._i64p),
+                         hi - lo, rows.ctypes.data_as(O._i32p), 1)
+    return rows
+
+
+def _q_chunk(args):
+    """metrics.py:41-79 (NP terms) and metrics.py:106-113 (stress scale sums)
+    for sources [lo, hi), restated chunk-wise as oracle/metrics.py does."""
+    from scipy.spatial.distance import cdist
+    lo, hi = args
+    c = _Q["coords"]
+    rows = _q_rows(lo, hi)
+    delta = cdist(c[lo:hi], c)
+    d = rows.astype(np.float64)
+    np.fill_diagonal(d[:, lo:hi], np.inf)
+    s_num = float((delta / d).sum())
+    s_den = float((delta * delta / (d * d)).sum())
+    jac = 0.0
+    for i in range(hi - lo):
+        v = lo + i
+        hv = rows[i]
+        hood = np.flatnonzero((hv >= 1) & (hv <= 2))
+        q = hood.shape[0]
+        if q == 0:
+            jac += 1.0
+            continue
+        row = delta[i].copy()
+        row[v] = np.inf
+        nearest = np.argsort(row, kind="stable")[:q]
+        inter = np.intersect1d(hood, nearest, assume_unique=True).shape[0]
+        jac += inter / (2 * q - inter)
+    return s_num, s_den, jac
+
+
+def _q_chunk2(args):
+    """metrics.py:115-131 (stress terms) for sources [lo, hi)."""
+    from scipy.spatial.distance import cdist
+    lo, hi, scale = args
+    c = _Q["coords"]
+    rows = _q_rows(lo, hi)
+    delta = cdist(c[lo:hi], c) * scale
+    d = rows.astype(np.float64)
+    np.fill_diagonal(d[:, lo:hi], np.inf)
+    term = (1.0 - delta / d) ** 2
+    np.fill_diagonal(term[:, lo:hi], 0.0)
+    return float(term.sum())
+
+
+def _q_cross(args):
+    """oracle.metrics.count_crossings (float filter + exact Fractions) for the
+    pairs whose first edge lies in [i0, i1)."""
+    from types import SimpleNamespace
+    from oracle import metrics as OM
+    return OM.count_crossings(SimpleNamespace(edges=_Q["edges"]), _Q["coords"], rows=args)
+
+
+def gen_quality_c3_full(nseeds=5, procs=8):
+    """Exact NP, stress and crossings (metrics.py:41-190 restated in
+    oracle/metrics.py, chunked) of the reference's own c3 SL layouts, seeds
+    0..nseeds-1 -- the reference side of the exact check (c) at c3.  Only the
+    scalars are frozen."""
+    import multiprocessing as mp
+    import time
+    sys.path.insert(0, ROOT)
+    rg = gu.synth_graph("scale_free", 100000, seed=2, m0=3)
+    n = rg.n
+    indptr = np.ascontiguousarray(rg.adj_indptr, np.int64)
+    indices = np.ascontiguousarray(rg.adj_indices, np.int32)
+    edges = np.ascontiguousarray(rg.edges, np.int64)
+    out = {"np_": [], "stress": [], "crossings": []}
+    for seed in range(nseeds):
+        t = time.time()
+        _, kn = gu.partial_bfs(rg, 15, seed=seed)
+        gk = gu.smooth_knn_weights(kn)
+        E = gk.edge_count
+        samp = math.log(0.1 * E) / math.log(E)
+        lay = gu.optimize_sampled(gk, gu.random_init(rg, seed, 10.0),
+                                  gu.OptimizerConfig(iterations=200, k=15, seed=seed, samp=samp))
+        coords = np.ascontiguousarray(lay.coords, np.float64)
+        chunks = [(lo, min(lo + 512, n)) for lo in range(0, n, 512)]
+        with mp.get_context("fork").Pool(procs, _q_init, (indptr, indices, coords, edges)) as pool:
+            parts = pool.map(_q_chunk, chunks)
+            s_num = sum(p[0] for p in parts)
+            s_den = sum(p[1] for p in parts)
+            scale = s_num / s_den if s_den > 0 else 1.0
+            st = sum(pool.map(_q_chunk2, [(lo, hi, scale) for lo, hi in chunks])) / (n * n - n)
+            npv = sum(p[2] for p in parts) / n
+            m = edges.shape[0]
+            bounds = np.linspace(0, m, 4 * procs + 1).astype(int)
+            cr = sum(pool.map(_q_cross, list(zip(bounds[:-1], bounds[1:]))))
+        out["np_"].append(npv)
+        out["stress"].append(st)
+        out["crossings"].append(cr)
+        print("quality c3 full seed", seed, npv, st, cr, f"{time.time() - t:.1f}s", flush=True)
+        save("quality_c3_full.npz", np_=np.array(out["np_"]), stress=np.array(out["stress"]),
+             crossings=np.array(out["crossings"], np.int64))
+
 def main():
     which = sys.argv[1:] or ["partial_small", "full_small", "smooth_cases", "c1", "c3", "quality_c1",
                              "quality_c3"]
