@@ -201,6 +201,27 @@ int gu_neighborhood_preservation(int64_t n, const int32_t* indptr, const int32_t
                                  double* out_sum, void* workspace, size_t ws_bytes,
                                  void* stream);
 
+
+/* ------------------------------------------- spectral_init (8(f) row 2)
+ * layout.py:221-304.  gu_spectral_degree: inv_sqrt = deg^-1/2, sqrt_deg.
+ * gu_spectral_op: y = P (x' + D^-1/2 A D^-1/2 x'), x' = P x, P = I - B B^T,
+ * the deflated 2I - L_sym of layout.py:270-273; basis: nb <= 4 orthonormal
+ * float64 columns (column j at basis + j*n); x != y. */
+int gu_spectral_degree(int64_t n, const int32_t* indptr, double* inv_sqrt, double* sqrt_deg,
+                       void* stream);
+size_t gu_spectral_op_workspace_size(int64_t n);
+int gu_spectral_op(int64_t n, const int32_t* indptr, const int32_t* indices,
+                   const double* inv_sqrt, const double* basis, int32_t nb, const double* x,
+                   double* y, void* workspace, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------- connected components
+ * graph.py is_connected / largest_connected_component: labels[v] = smallest
+ * vertex id of v's component (lock-free union-find); out_ncomp: device int. */
+size_t gu_components_workspace_size(int64_t n);
+int gu_connected_components(int64_t n, const int32_t* indptr, const int32_t* indices,
+                            int32_t* labels, int32_t* out_ncomp, void* workspace,
+                            size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

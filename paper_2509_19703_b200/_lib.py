@@ -28,6 +28,12 @@ _vp = ctypes.c_void_p
 
 # name -> (restype, argtypes), mirrors include/gumap.h
 SIGNATURES = {
+    "gu_spectral_degree": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
+    "gu_spectral_op_workspace_size": (_c_sz, [_c_i64]),
+    "gu_spectral_op": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _c_i32, _vp, _vp, _vp, _c_sz,
+                                      _vp]),
+    "gu_components_workspace_size": (_c_sz, [_c_i64]),
+    "gu_connected_components": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _c_sz, _vp]),
     "gu_stress_workspace_size": (_c_sz, [_c_i64]),
     "gu_stress": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i32, _vp, _vp, _c_sz, _vp]),
     "gu_grid_bytes": (_c_sz, []),

@@ -421,6 +421,31 @@ def gen_quality_c3_full(nseeds=5, procs=8):
         save("quality_c3_full.npz", np_=np.array(out["np_"]), stress=np.array(out["stress"]),
              crossings=np.array(out["crossings"], np.int64))
 
+
+def gen_spectral():
+    """spectral_init (layout.py:221-304) of the reference on graphs with n >
+    512 (the Lanczos path): BA graphs (simple spectra: coordinates compared)
+    and a grid (degenerate pairs: eigen-residual properties only)."""
+    out = {}
+    cases = [("ba700", F.scale_free(700, seed=5, m0=2), 0), ("ba1500", F.scale_free(1500, seed=6, m0=3), 3),
+             ("grid900", F.grid(900), 1)]
+    for name, g, seed in cases:
+        n = g.n
+        rg = gu.build_graph([tuple(map(int, e)) for e in g.edges])
+        assert rg.n == n
+        lay = gu.spectral_init(rg, seed=seed)
+        out[name + "_coords"] = np.asarray(lay.coords)
+        out[name + "_seed"] = np.array(seed)
+        # reference eigenvalues of L_sym (dense) for the gap
+        import scipy.sparse as sp
+        deg = np.diff(rg.adj_indptr).astype(np.float64)
+        A = sp.csr_matrix((np.ones(rg.adj_indices.shape[0]), rg.adj_indices, rg.adj_indptr), shape=(n, n))
+        isq = 1.0 / np.sqrt(deg)
+        lam = np.linalg.eigvalsh(np.eye(n) - (isq[:, None] * A.toarray()) * isq[None, :])
+        out[name + "_lam"] = lam[:6]
+        print(name, "lam", lam[:4])
+    save("spectral.npz", **out)
+
 def main():
     which = sys.argv[1:] or ["partial_small", "full_small", "smooth_cases", "c1", "c3", "quality_c1",
                              "quality_c3"]
