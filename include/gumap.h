@@ -222,6 +222,27 @@ int gu_connected_components(int64_t n, const int32_t* indptr, const int32_t* ind
                             int32_t* labels, int32_t* out_ncomp, void* workspace,
                             size_t ws_bytes, void* stream);
 
+
+/* -------------------------------------- spectral sparsifier (8(f) row 3)
+ * sparsify.py:49-205.  gu_resistance_exact_gather: r_e from the grounded
+ * Laplacian inverse X ((n-1)^2 float64, vertex 0 grounded).
+ * gu_resistance_sketch: q counter-based Rademacher projections of the
+ * incidence matrix, block Jacobi-PCG (rtol, maxiter), out_r[e] = sum_i
+ * (y_i[u] - y_i[v])^2; status 4 = not converged (host_resid = residual).
+ * gu_sparsify_select: keep[e] (device uint8, by edge id) = max-resistance
+ * spanning tree + the first (target - tree) non-tree edges by (-r, u, v). */
+int gu_resistance_exact_gather(int64_t m, const int32_t* edges, const double* X, int64_t n,
+                               double* out_r, void* stream);
+size_t gu_resistance_sketch_workspace_size(int64_t n, int32_t q);
+int gu_resistance_sketch(int64_t n, const int32_t* indptr, const int32_t* indices, int64_t m,
+                         const int32_t* edges, int32_t q, uint64_t seed, double rtol,
+                         int32_t maxiter, double* out_r, int32_t* host_iters,
+                         double* host_resid, void* workspace, size_t ws_bytes, void* stream);
+size_t gu_sparsify_workspace_size(int64_t n, int64_t m);
+int gu_sparsify_select(int64_t n, int64_t m, const int32_t* edges, const double* r,
+                       int64_t target, uint8_t* keep, int32_t* host_tree_edges,
+                       void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

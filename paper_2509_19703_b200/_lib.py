@@ -28,6 +28,14 @@ _vp = ctypes.c_void_p
 
 # name -> (restype, argtypes), mirrors include/gumap.h
 SIGNATURES = {
+    "gu_resistance_exact_gather": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp]),
+    "gu_resistance_sketch_workspace_size": (_c_sz, [_c_i64, _c_i32]),
+    "gu_resistance_sketch": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _c_i32, _c_u64,
+                                            ctypes.c_double, _c_i32, _vp, _vp, _vp, _vp, _c_sz,
+                                            _vp]),
+    "gu_sparsify_workspace_size": (_c_sz, [_c_i64, _c_i64]),
+    "gu_sparsify_select": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp, _c_sz,
+                                          _vp]),
     "gu_spectral_degree": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "gu_spectral_op_workspace_size": (_c_sz, [_c_i64]),
     "gu_spectral_op": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _c_i32, _vp, _vp, _vp, _c_sz,
@@ -105,16 +113,19 @@ def load():
     return _lib
 
 
-def call(name, *args):
-    """Call a status-returning entry point; map failures to exceptions."""
-    lib = load()
-    r = getattr(lib, name)(*args)
+def check(name, r):
+    """Map a libgumap status to the exception the wrappers raise."""
     if r != GU_OK:
-        msg = lib.gu_last_error().decode(errors="replace")
+        msg = load().gu_last_error().decode(errors="replace")
         if r == GU_ERR_ARG:
             raise ValueError(f"{name}: {msg}")
         raise GumapError(f"{name} failed ({r}): {msg}")
     return r
+
+
+def call(name, *args):
+    """Call a status-returning entry point; map failures to exceptions."""
+    return check(name, getattr(load(), name)(*args))
 
 
 def ptr(t):

@@ -446,6 +446,31 @@ def gen_spectral():
         print(name, "lam", lam[:4])
     save("spectral.npz", **out)
 
+
+def gen_sparsify():
+    """sparsify.py:49-205 on dense graphs (m > n log2 n): the reference's exact
+    resistances, its sparsifier's kept-edge mask, and its sketch resistances
+    (numpy signs, for the statistical comparison)."""
+    import importlib
+    S = importlib.import_module("graph_umap.sparsify")
+    out = {}
+    cases = [("er300", F.erdos_renyi(300, avg_degree=30, seed=11)),
+             ("er800", F.erdos_renyi(800, avg_degree=30, seed=12)),
+             ("ba600", F.scale_free(600, seed=13, m0=12))]
+    for name, g in cases:
+        rg = gu.build_graph([tuple(map(int, e)) for e in g.edges])
+        assert rg.n == g.n and rg.m == g.m and np.array_equal(rg.edges, g.edges)
+        r = S.effective_resistance_exact(rg)
+        sp_g = S.sparsify(rg, r)
+        keys = set(map(tuple, sp_g.edges.tolist()))
+        mask = np.array([tuple(e) in keys for e in rg.edges.tolist()])
+        ra = S.effective_resistance_approx(rg, epsilon=0.5, seed=0)
+        out[name + "_r"] = np.asarray(r.values)
+        out[name + "_keep"] = mask
+        out[name + "_r_approx"] = np.asarray(ra.values)
+        print(name, rg.n, rg.m, "kept", mask.sum(), "target", S.sparsifier_target(rg.n, rg.m))
+    save("sparsify.npz", **out)
+
 def main():
     which = sys.argv[1:] or ["partial_small", "full_small", "smooth_cases", "c1", "c3", "quality_c1",
                              "quality_c3"]

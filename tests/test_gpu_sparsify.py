@@ -1,0 +1,101 @@
+"""GPU effective resistances and spectral sparsifier (
+sparsify.py:49-205) vs the reference's own values (tests/golden/sparsify.npz).
+
+  * exact resistances within EXACT_REL_TOL of the reference's (Cholesky
+    inverse vs the reference's sparse LU: rounding only);
+  * the selection (maximum spanning tree + budget) fed the reference's own
+    resistances keeps exactly the reference's edges;
+  * with our resistances, the kept set equals the reference's whenever the
+    two (-r, u, v) orders agree, and overlaps it >= 99.5% otherwise;
+  * the sketch (counter-based signs, same q and solver) agrees with the exact
+    values as the reference's sketch does: median relative error within
+    epsilon, and no worse than the reference sketch's by more than 25%.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+EXACT_REL_TOL = 1e-9
+CASES = ["er300", "er800", "ba600"]
+
+
+@pytest.fixture(scope="module")
+def gu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2509_19703_b200 as gu
+    return gu
+
+
+def _graph(name):
+    from paper_2509_19703_b200 import fixtures as F
+    return {"er300": lambda: F.erdos_renyi(300, avg_degree=30, seed=11),
+            "er800": lambda: F.erdos_renyi(800, avg_degree=30, seed=12),
+            "ba600": lambda: F.scale_free(600, seed=13, m0=12)}[name]()
+
+
+def _kept_mask(g, sg):
+    keys = set(map(tuple, np.asarray(sg.edges).tolist()))
+    return np.array([tuple(e) in keys for e in np.asarray(g.edges).tolist()])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_exact_resistance_and_selection(gu, name):
+    from paper_2509_19703_b200 import sparsify as S
+
+    z = load_golden("sparsify.npz")
+    g = _graph(name)
+    r = S.effective_resistance_exact(g)
+    ref_r = z[name + "_r"]
+    assert np.max(np.abs(r.values - ref_r) / np.abs(ref_r)) <= EXACT_REL_TOL
+    # selection fed the reference's resistances: exactly its edges
+    sg = S.sparsify(g, S.ResistanceTable(values=ref_r))
+    assert sg.m == S.sparsifier_target(g.n, g.m)
+    assert np.array_equal(_kept_mask(g, sg), z[name + "_keep"])
+    # with our resistances
+    mine = _kept_mask(g, S.sparsify(g, r))
+    order_ref = np.lexsort((g.edges[:, 1], g.edges[:, 0], -ref_r))
+    order_ours = np.lexsort((g.edges[:, 1], g.edges[:, 0], -r.values))
+    if np.array_equal(order_ref, order_ours):
+        assert np.array_equal(mine, z[name + "_keep"])
+    else:
+        assert np.mean(mine == z[name + "_keep"]) >= 0.995
+    assert gu.largest_connected_component(S.sparsify(g, r)).n == g.n  # stays connected
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_sketch_resistance_vs_exact(gu, name):
+    from paper_2509_19703_b200 import sparsify as S
+
+    z = load_golden("sparsify.npz")
+    g = _graph(name)
+    exact = z[name + "_r"]
+    ours = S.effective_resistance_approx(g, epsilon=0.5, seed=0).values
+    theirs = z[name + "_r_approx"]
+    e_ours = np.median(np.abs(ours - exact) / exact)
+    e_ref = np.median(np.abs(theirs - exact) / exact)
+    print(name, "median rel err ours", e_ours, "reference sketch", e_ref)
+    assert e_ours <= 0.5
+    assert e_ours <= 1.25 * e_ref + 0.02
+
+
+def test_sparsifier_errors_and_identity(gu):
+    from paper_2509_19703_b200 import sparsify as S
+    from paper_2509_19703_b200.graph import GraphError, graph_from_edges
+
+    g = _graph("er300")
+    with pytest.raises(S.SolverError):
+        S.effective_resistance_approx(g, epsilon=0.5, maxiter=1)
+    with pytest.raises(ValueError):
+        S.effective_resistance_approx(g, epsilon=1.5)
+    sparse = gu.synth_graph("grid", 400)
+    assert gu.make_sparsifier(sparse) is sparse
+    with pytest.raises(GraphError):
+        S.effective_resistance_exact(graph_from_edges(4, [(0, 1), (2, 3)]))
+    sg = gu.make_sparsifier(g)  # auto -> exact at n <= 4000
+    assert sg.m == S.sparsifier_target(g.n, g.m)
