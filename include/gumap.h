@@ -243,6 +243,28 @@ int gu_sparsify_select(int64_t n, int64_t m, const int32_t* edges, const double*
                        int64_t target, uint8_t* keep, int32_t* host_tree_edges,
                        void* workspace, size_t ws_bytes, void* stream);
 
+
+/* ------------------------------------ graph construction / LCC (8(f) 4)
+ * graph.py:114-232.  gu_build_graph_ids: raw int64 (npairs, 2) ids on the
+ * device -> host_out = (n, canonical edge count m, self loops dropped);
+ * gu_build_graph_csr (same workspace): sorted unique ids (int64 n), edges
+ * (int64 (m, 2), (u, v) order), indptr (int64 n+1), indices (int32 2m).
+ * gu_lcc_plan: host_out = (components, champion size n2, its edges m2);
+ * gu_lcc_build: old id of each kept vertex (int32 n2), edges, CSR. */
+size_t gu_build_graph_workspace_size(int64_t npairs);
+int gu_build_graph_ids(int64_t npairs, const int64_t* raw, int64_t* host_out, void* workspace,
+                       size_t ws_bytes, void* stream);
+int gu_build_graph_csr(int64_t npairs, int64_t n, int64_t m, int64_t* out_ids,
+                       int64_t* out_edges, int64_t* out_indptr, int32_t* out_indices,
+                       void* workspace, size_t ws_bytes, void* stream);
+size_t gu_lcc_workspace_size(int64_t n, int64_t m);
+int gu_lcc_plan(int64_t n, int64_t m, const int32_t* indptr, const int32_t* indices,
+                const int64_t* edges, int64_t* host_out, void* workspace, size_t ws_bytes,
+                void* stream);
+int gu_lcc_build(int64_t n, int64_t m, int64_t n2, int64_t m2, int32_t* out_old_ids,
+                 int64_t* out_edges, int64_t* out_indptr, int32_t* out_indices, void* workspace,
+                 size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

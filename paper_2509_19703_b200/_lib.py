@@ -28,6 +28,14 @@ _vp = ctypes.c_void_p
 
 # name -> (restype, argtypes), mirrors include/gumap.h
 SIGNATURES = {
+    "gu_build_graph_workspace_size": (_c_sz, [_c_i64]),
+    "gu_build_graph_ids": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_sz, _vp]),
+    "gu_build_graph_csr": (ctypes.c_int, [_c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _c_sz,
+                                          _vp]),
+    "gu_lcc_workspace_size": (_c_sz, [_c_i64, _c_i64]),
+    "gu_lcc_plan": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _c_sz, _vp]),
+    "gu_lcc_build": (ctypes.c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _c_sz,
+                                    _vp]),
     "gu_resistance_exact_gather": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _vp]),
     "gu_resistance_sketch_workspace_size": (_c_sz, [_c_i64, _c_i32]),
     "gu_resistance_sketch": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _vp, _c_i32, _c_u64,

@@ -83,6 +83,16 @@ def device_csr(g, device=None):
     return csr
 
 
+def register_device_csr(g, csr):
+    """Seed the resident-CSR cache for ``g`` (a graph built on the device)."""
+    key = (id(g), str(csr.device))
+    try:
+        ref = weakref.ref(g, lambda _r, k=key: _CSR_CACHE.pop(k, None))
+    except TypeError:
+        return
+    _CSR_CACHE[key] = (ref, csr)
+
+
 _PIN_THRESHOLD = 1 << 20  # bytes; smaller transfers are not worth pinning
 
 

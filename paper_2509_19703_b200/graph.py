@@ -118,31 +118,109 @@ def canonical_edges(n, pairs):
     return np.stack([keys // n, keys % n], axis=1)
 
 
-def build_graph(edge_pairs, labels=None):
-    """Graph from raw integer pairs: dense relabel by sorted id, dedupe,
-    drop self loops (graph.py:132-186 for integer ids)."""
-    pairs = np.asarray(list(edge_pairs) if not isinstance(edge_pairs, np.ndarray)
-                       else edge_pairs, dtype=np.int64).reshape(-1, 2)
-    if pairs.shape[0] == 0:
-        raise GraphError("empty graph")
-    ids, inv = np.unique(pairs.reshape(-1), return_inverse=True)
-    dense = inv.reshape(-1, 2)
-    n = int(ids.shape[0])
+# integer inputs at least this large are built on the GPU when one is present
+GPU_BUILD_MIN_PAIRS = 1 << 16
+
+
+def _gpu_available():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:  # noqa: BLE001 -- no torch / no driver: host path
+        return False
+
+
+def _build_graph_labels(pairs_list):
+    """graph.py:132-186 for arbitrary comparable labels (strings, ...)."""
+    seen = set()
+    for u, v in pairs_list:
+        seen.add(u)
+        seen.add(v)
+    try:
+        ordered = sorted(seen)
+    except TypeError as exc:
+        raise GraphError("vertex ids must be mutually comparable") from exc
+    index = {label: i for i, label in enumerate(ordered)}
+    dense = np.array([(index[u], index[v]) for u, v in pairs_list], dtype=np.int64)
+    return _build_graph_dense(len(ordered), dense, tuple(ordered))
+
+
+def _build_graph_dense(n, dense, labels):
     loops = int(np.count_nonzero(dense[:, 0] == dense[:, 1]))
     canon = canonical_edges(n, dense)
     if canon.shape[0] == 0:
         raise GraphError("empty graph")
-    dups = pairs.shape[0] - loops - canon.shape[0]
-    g = graph_from_edges(n, canon, labels=tuple(int(x) for x in ids))
+    dups = dense.shape[0] - loops - canon.shape[0]
+    g = graph_from_edges(n, canon, labels=labels)
     object.__setattr__(g, "dropped_self_loops", loops)
     object.__setattr__(g, "dropped_duplicates", int(dups))
     return g
 
 
+def build_graph(edge_pairs, labels=None):
+    """Graph from raw (id, id) pairs (graph.py:132-186): dense relabel in
+    sorted label order, self loops and duplicates dropped (counted), edges
+    canonical u < v in (u, v) order.  Non-negative integer inputs of
+    GPU_BUILD_MIN_PAIRS pairs or more are built on the GPU
+    (csrc/ingest.cu), which also leaves the CSR resident for the BFS."""
+    if isinstance(edge_pairs, np.ndarray) and edge_pairs.dtype.kind in "iu":
+        pairs = edge_pairs.astype(np.int64, copy=False).reshape(-1, 2)
+    else:
+        pairs_list = list(edge_pairs)
+        if not pairs_list:
+            raise GraphError("empty graph")
+        try:
+            pairs = np.asarray(pairs_list, dtype=np.int64).reshape(-1, 2)
+        except (TypeError, ValueError):
+            return _build_graph_labels(pairs_list)
+    if pairs.shape[0] == 0:
+        raise GraphError("empty graph")
+    if pairs.shape[0] >= GPU_BUILD_MIN_PAIRS and _gpu_available() and int(pairs.min()) >= 0:
+        return _build_graph_gpu(pairs)
+    ids, inv = np.unique(pairs.reshape(-1), return_inverse=True)
+    return _build_graph_dense(int(ids.shape[0]), inv.reshape(-1, 2),
+                              tuple(ids.tolist()))
+
+
+def _build_graph_gpu(pairs):
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .device import DeviceCsr, register_device_csr, require_cuda, stream_ptr, to_device, to_host, workspace
+
+    dev = require_cuda()
+    npairs = int(pairs.shape[0])
+    raw = to_device(np.ascontiguousarray(pairs), np.int64, dev)
+    lib = _lib.load()
+    ws = workspace(lib.gu_build_graph_workspace_size(npairs), dev)
+    out = (ctypes.c_int64 * 3)()
+    _lib.call("gu_build_graph_ids", npairs, _lib.ptr(raw), out, _lib.ptr(ws), ws.numel(),
+              stream_ptr(dev))
+    n, m, loops = int(out[0]), int(out[1]), int(out[2])
+    if m == 0:
+        raise GraphError("empty graph")
+    ids = torch.empty(n, dtype=torch.int64, device=dev)
+    edges = torch.empty((m, 2), dtype=torch.int64, device=dev)
+    indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    indices = torch.empty(2 * m, dtype=torch.int32, device=dev)
+    _lib.call("gu_build_graph_csr", npairs, n, m, _lib.ptr(ids), _lib.ptr(edges), _lib.ptr(indptr),
+              _lib.ptr(indices), _lib.ptr(ws), ws.numel(), stream_ptr(dev))
+    g = Graph(n=n, m=m, adj_indptr=to_host(indptr), adj_indices=to_host(indices),
+              edges=to_host(edges), labels=tuple(to_host(ids).tolist()),
+              dropped_self_loops=loops, dropped_duplicates=npairs - loops - m)
+    register_device_csr(g, DeviceCsr(n, indptr.to(torch.int32), indices, dev))
+    return g
+
+
 def largest_connected_component(g):
     """Induced subgraph on the largest component, relabelled densely in id
-    order; ties go to the component holding the smallest vertex id
-    (graph.py:201-232)."""
+    order, labels carried (graph.py:201-232); ties go to the component
+    holding the smallest vertex id.  On the GPU when one is present
+    (csrc/ingest.cu union-find + compaction)."""
+    if g.n >= 2 and _gpu_available():
+        return _lcc_gpu(g)
     import scipy.sparse as sp
     from scipy.sparse import csgraph
 
@@ -165,4 +243,47 @@ def largest_connected_component(g):
     mask = member[g.edges[:, 0]] == champion
     edges = remap[g.edges[mask]]
     edges.sort(axis=1)
-    return graph_from_edges(len(keep), edges)
+    return _with_labels(graph_from_edges(len(keep), edges), g, keep)
+
+
+def _with_labels(h, g, keep):
+    old = getattr(g, "labels", ()) or None
+    labels = tuple(np.asarray(old, dtype=object)[keep].tolist()) if old else tuple(keep.tolist())
+    object.__setattr__(h, "labels", labels)
+    object.__setattr__(h, "dropped_self_loops", getattr(g, "dropped_self_loops", 0))
+    object.__setattr__(h, "dropped_duplicates", getattr(g, "dropped_duplicates", 0))
+    return h
+
+
+def _lcc_gpu(g):
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .device import DeviceCsr, device_csr, register_device_csr, stream_ptr, to_device, to_host, workspace
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n, m = int(g.n), int(g.m)
+    csr = device_csr(g, dev)
+    edges_dev = to_device(np.ascontiguousarray(g.edges), np.int64, dev)
+    lib = _lib.load()
+    ws = workspace(lib.gu_lcc_workspace_size(n, m), dev)
+    out = (ctypes.c_int64 * 3)()
+    _lib.call("gu_lcc_plan", n, m, _lib.ptr(csr.indptr), _lib.ptr(csr.indices), _lib.ptr(edges_dev),
+              out, _lib.ptr(ws), ws.numel(), stream_ptr(dev))
+    ncomp, n2, m2 = int(out[0]), int(out[1]), int(out[2])
+    if ncomp <= 1:
+        return g
+    old = torch.empty(n2, dtype=torch.int32, device=dev)
+    edges = torch.empty((max(m2, 1), 2), dtype=torch.int64, device=dev)
+    indptr = torch.empty(n2 + 1, dtype=torch.int64, device=dev)
+    indices = torch.empty(max(2 * m2, 1), dtype=torch.int32, device=dev)
+    _lib.call("gu_lcc_build", n, m, n2, m2, _lib.ptr(old), _lib.ptr(edges), _lib.ptr(indptr),
+              _lib.ptr(indices), _lib.ptr(ws), ws.numel(), stream_ptr(dev))
+    keep = to_host(old).astype(np.int64)
+    h = Graph(n=n2, m=m2, adj_indptr=to_host(indptr), adj_indices=to_host(indices[: 2 * m2]),
+              edges=to_host(edges[:m2]))
+    h = _with_labels(h, g, keep)
+    register_device_csr(h, DeviceCsr(n2, indptr.to(torch.int32), indices[: 2 * m2], dev))
+    return h
