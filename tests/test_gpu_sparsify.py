@@ -99,3 +99,19 @@ def test_sparsifier_errors_and_identity(gu):
         S.effective_resistance_exact(graph_from_edges(4, [(0, 1), (2, 3)]))
     sg = gu.make_sparsifier(g)  # auto -> exact at n <= 4000
     assert sg.m == S.sparsifier_target(g.n, g.m)
+
+
+def test_ss_drivers_sparsify_on_gpu(gu):
+    """run_ss_gumap / run_sssl_gumap without g_prime: make_sparsifier runs
+    (exact resistances at n <= 4000, the sketch above) and the layout covers
+    every vertex (layout.py:453-481)."""
+    from paper_2509_19703_b200 import fixtures as F
+    from paper_2509_19703_b200 import sparsify as S
+
+    for g in (F.erdos_renyi(300, avg_degree=30, seed=11), F.erdos_renyi(5000, avg_degree=40, seed=3)):
+        assert g.m > S.sparsifier_target(g.n, g.m)
+        cfg = gu.OptimizerConfig(iterations=20, k=15, seed=0)
+        for fn, tag in ((gu.run_ss_gumap, "SS"), (gu.run_sssl_gumap, "SSSL")):
+            lay, rep = fn(g, cfg)
+            assert lay.n == g.n and lay.algorithm_tag == tag and np.all(np.isfinite(lay.coords))
+            assert rep.prep_ms > 0 and rep.m == g.m
