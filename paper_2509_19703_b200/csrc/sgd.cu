@@ -187,32 +187,34 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
         lo[q] = rb;
         len[q] = q < nq ? re - rb : 0;
       }
-      // lockstep lower_bound of every candidate in the row
-      for (;;) {
-        bool any = false;
+      // speculative coordinate loads: a random candidate is a neighbour with
+      // probability ~deg/n, so the gathers go out with the draws, in parallel
+      // with the neighbour test instead of after it
+      float2 xc[SGD_NEG_BLOCK];
+#pragma unroll
+      for (int q = 0; q < SGD_NEG_BLOCK; q++) xc[q] = q < nq ? xy[cand[q]] : make_float2(0.f, 0.f);
+      // lockstep lower_bound of every candidate in the row: each step issues
+      // all the probes' loads before any compare (branch-free: a finished
+      // search probes rb again), so a step costs one round trip, not one per
+      // candidate; ceil(log2(deg + 1)) steps finish every search
+      const int steps = 32 - __clz(re - rb);
+      for (int it = 0; it < steps; it++) {
+        int x[SGD_NEG_BLOCK];
+#pragma unroll
+        for (int q = 0; q < SGD_NEG_BLOCK; q++)
+          x[q] = __ldg(nix + (len[q] > 0 ? lo[q] + (len[q] >> 1) : rb));
 #pragma unroll
         for (int q = 0; q < SGD_NEG_BLOCK; q++) {
-          if (len[q] > 0) {
-            const int half = len[q] >> 1;
-            const int x = __ldg(nix + lo[q] + half);
-            if (x < cand[q]) {
-              lo[q] += half + 1;
-              len[q] -= half + 1;
-            } else {
-              len[q] = half;
-            }
-            any = true;
-          }
+          const int half = len[q] >> 1;
+          const bool act = len[q] > 0, lt = x[q] < cand[q];
+          lo[q] = (act && lt) ? lo[q] + half + 1 : lo[q];
+          len[q] = act ? (lt ? len[q] - half - 1 : half) : 0;
         }
-        if (!any) break;
       }
-      float2 xc[SGD_NEG_BLOCK];
       bool ok[SGD_NEG_BLOCK];
 #pragma unroll
-      for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+      for (int q = 0; q < SGD_NEG_BLOCK; q++)
         ok[q] = q < nq && cand[q] != u && !(lo[q] < re && __ldg(nix + lo[q]) == cand[q]);
-        if (ok[q]) xc[q] = xy[cand[q]];
-      }
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         if (q >= nq) break;
