@@ -328,7 +328,7 @@ def _sgd_bench(gu, g, args, dev, peak):
 
     def epochs(e0, e1):
         _lib.call("gu_sgd_epochs", plan.n, plan.E, _lib.ptr(xy), _lib.ptr(plan.edges),
-                  _lib.ptr(plan.nbr_indptr), _lib.ptr(plan.nbr_indices), float(a), float(b),
+                  _lib.ptr(plan.nbr_indptr), _lib.ptr(plan.nbr_indices), _lib.ptr(plan.filter), float(a), float(b),
                   1.0, T, e0, e1, 5, E, 0, plan.seed, sgd_concurrency(plan.n), _lib.ptr(div),
                   stream_ptr(dev))
 

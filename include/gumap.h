@@ -127,7 +127,8 @@ int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* 
  * 8 draws max, per-component clip +-4, random direction for coincident
  * points), run as a Hogwild epoch over fp32 float2 coordinates.  The epoch
  * schedule (fresh order per epoch, or a sliding window of `window` edges over
- * one shuffled order) and the negatives come from Philox4x32-10 keyed by seed.
+ * one shuffled order) and the negatives come from a counter-based 64-bit hash
+ * keyed by seed.
  * edges: int4 records {src, dst, float-bits(h), (row start << 6) | degree or -1},
  * built in a shuffled order by gu_sgd_prepare_edges (perm_out, nullable,
  * receives the sym edge id of every record position).  nbr CSR int32.
@@ -136,12 +137,18 @@ int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* 
  * first epoch that produced a non-finite coordinate (init to INT32_MAX).
  * concurrency: maximum number of edge visits in flight (threads); 0 = fill
  * the GPU.  Hogwild stays statistically close to the sequential sweep only
- * while concurrency << n, so callers cap it for small graphs. */
+ * while concurrency << n, so callers cap it for small graphs.
+ * nbr_filter (nullable): per-vertex 128-bit Bloom words of the neighbour ids
+ * from gu_sgd_neighbor_filter (16 bytes x n); a negative whose bit is clear
+ * skips the row search (exact: a set bit still searches). */
 int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
                          const double* sym_w, const int32_t* nbr_indptr, uint64_t seed,
                          void* edges_int4, int32_t* perm_out, void* stream);
+int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr, const int32_t* nbr_indices,
+                           void* filter_out, void* stream);
 int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4,
-                  const int32_t* nbr_indptr, const int32_t* nbr_indices, float a, float b,
+                  const int32_t* nbr_indptr, const int32_t* nbr_indices,
+                  const void* nbr_filter, float a, float b,
                   float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
                   int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
                   int64_t concurrency, int32_t* diverged, void* stream);

@@ -85,7 +85,8 @@ SIGNATURES = {
     "gu_symmetrize": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      ctypes.POINTER(_c_i64), _vp, _c_sz, _vp]),
     "gu_sgd_prepare_edges": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _c_u64, _vp, _vp, _vp]),
-    "gu_sgd_epochs": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _c_f32, _c_f32,
+    "gu_sgd_neighbor_filter": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
+    "gu_sgd_epochs": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _c_f32, _c_f32,
                                      _c_f32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i64, _c_i32,
                                      _c_u64, _c_i64, _vp, _vp]),
     "gu_sgd_visit_order": (ctypes.c_int, [_c_i64, _c_i32, _c_i64, _c_i32, _c_u64, _vp, _vp]),

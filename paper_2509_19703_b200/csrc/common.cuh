@@ -4,7 +4,7 @@
 //   splitmix64       /root/reference/pkg/src/graph_umap/_kernels.py:13-30
 //   numpy SeedSequence + PCG64 + Generator.permutation (numpy 2.3.5), used by
 //   knn_from_full_distances (neighbors.py:213-216) for k-th distance ties.
-// Counter-based RNG for the Hogwild SGD epochs: Philox4x32-10.
+// Counter-based RNG for the Hogwild SGD epochs: sgd.cu draw64 (64-bit finaliser).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -193,20 +193,6 @@ __device__ inline void pcg64_from_seedseq(Pcg64& r, uint64_t seed, uint64_t key)
   r.buf32 = 0;
 }
 
-// ---------------------------------------------------------- Philox4x32-10
-struct Philox {
-  __device__ __forceinline__ static uint4 gen(uint4 ctr, uint2 key) {
-#pragma unroll
-    for (int i = 0; i < 10; i++) {
-      uint32_t hi0 = __umulhi(0xD2511F53u, ctr.x), lo0 = 0xD2511F53u * ctr.x;
-      uint32_t hi1 = __umulhi(0xCD9E8D57u, ctr.z), lo1 = 0xCD9E8D57u * ctr.z;
-      ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
-      key.x += 0x9E3779B9u;
-      key.y += 0xBB67AE85u;
-    }
-    return ctr;
-  }
-};
 
 // ------------------------------------------------------------ warp utils
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }

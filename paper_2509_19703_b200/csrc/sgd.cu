@@ -118,11 +118,38 @@ __device__ __forceinline__ bool is_neighbor(const int* __restrict__ ip, const in
   return false;
 }
 
+// 128-bit Bloom word of each vertex's neighbour ids (one hash bit per id):
+// a candidate whose bit is clear is certainly not a neighbour, so only the
+// ~deg/128 of draws that hit a set bit run the row search
+__device__ __forceinline__ unsigned filt_bit(int c) { return ((unsigned)c * 0x9E3779B1u) >> 25; }
+
+__global__ void neighbor_filter_kernel(int n, const int* __restrict__ nip,
+                                       const int* __restrict__ nix, uint4* __restrict__ filt) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    unsigned w[4] = {0u, 0u, 0u, 0u};
+    const int b = __ldg(nip + v), e = __ldg(nip + v + 1);
+    for (int p = b; p < e; p++) {
+      const unsigned h = filt_bit(__ldg(nix + p));
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if ((h >> 5) == (unsigned)j) w[j] |= 1u << (h & 31);
+    }
+    filt[v] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__device__ __forceinline__ bool filt_maybe(uint4 f, int c) {
+  const unsigned h = filt_bit(c);
+  const unsigned w = (h >> 5) == 0 ? f.x : ((h >> 5) == 1 ? f.y : ((h >> 5) == 2 ? f.z : f.w));
+  return (w >> (h & 31)) & 1u;
+}
+
 __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
     sgd_epoch_kernel(int n, long long E, float2* __restrict__ xy, const int4* __restrict__ edges,
-                     const int* __restrict__ nip, const int* __restrict__ nix, float a, float b,
-                     float lr, int epoch, int n_neg, long long items, long long start,
-                     int windowed, unsigned long long seed, int* __restrict__ diverged) {
+                     const int* __restrict__ nip, const int* __restrict__ nix,
+                     const uint4* __restrict__ filt, float a, float b, float lr, int epoch,
+                     int n_neg, long long items, long long start, int windowed,
+                     unsigned long long seed, int* __restrict__ diverged) {
   const long long ntiles = (E + TILE - 1) / TILE;
   Feistel tperm((unsigned long long)ntiles, mix64(seed ^ (0x51ED27ull + (unsigned long long)epoch)));
   const unsigned long long rkey = mix64(seed ^ (0xA5A5A5A5ull * (unsigned long long)(epoch + 1)));
@@ -140,6 +167,7 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
     }
     const int4 rec = __ldg(edges + p);
     const int u = rec.x, v = rec.y;
+    const uint4 fw = filt ? __ldg(filt + u) : make_uint4(~0u, ~0u, ~0u, ~0u);
     const float h = __int_as_float(rec.z);
     float2 xu = xy[u];
     const float2 xv = xy[v];
@@ -179,13 +207,16 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
       const int nq = min(SGD_NEG_BLOCK, n_neg - q0);
       int cand[SGD_NEG_BLOCK], lo[SGD_NEG_BLOCK], len[SGD_NEG_BLOCK];
       unsigned spare_q[SGD_NEG_BLOCK];
+      bool maybe_any = false;
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         const unsigned long long r = draw64(rkey, p, q0 + q, 0);
         cand[q] = (int)__umulhi((unsigned)(r >> 32), (unsigned)n);
         spare_q[q] = (unsigned)r;
         lo[q] = rb;
-        len[q] = q < nq ? re - rb : 0;
+        const bool maybe = q < nq && filt_maybe(fw, cand[q]);
+        len[q] = maybe ? re - rb : 0;
+        maybe_any |= maybe;
       }
       // speculative coordinate loads: a random candidate is a neighbour with
       // probability ~deg/n, so the gathers go out with the draws, in parallel
@@ -197,7 +228,7 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
       // all the probes' loads before any compare (branch-free: a finished
       // search probes rb again), so a step costs one round trip, not one per
       // candidate; ceil(log2(deg + 1)) steps finish every search
-      const int steps = 32 - __clz(re - rb);
+      const int steps = maybe_any ? 32 - __clz(re - rb) : 0;
       for (int it = 0; it < steps; it++) {
         int x[SGD_NEG_BLOCK];
 #pragma unroll
@@ -214,7 +245,8 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
       bool ok[SGD_NEG_BLOCK];
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++)
-        ok[q] = q < nq && cand[q] != u && !(lo[q] < re && __ldg(nix + lo[q]) == cand[q]);
+        ok[q] = q < nq && cand[q] != u &&
+                !(filt_maybe(fw, cand[q]) && lo[q] < re && __ldg(nix + lo[q]) == cand[q]);
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         if (q >= nq) break;
@@ -327,8 +359,21 @@ static void epoch_range(int64_t E, int32_t epoch, int64_t window, int32_t window
   }
 }
 
+extern "C" int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr,
+                                      const int32_t* nbr_indices, void* filter_out, void* stream) {
+  if (n <= 0 || n >= INT_MAX) {
+    set_error("gu_sgd_neighbor_filter: bad n");
+    return GU_ERR_ARG;
+  }
+  neighbor_filter_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      (int)n, nbr_indptr, nbr_indices, (uint4*)filter_out);
+  GU_CHECK_LAUNCH("neighbor_filter_kernel");
+  return GU_OK;
+}
+
 extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4,
-                             const int32_t* nbr_indptr, const int32_t* nbr_indices, float a,
+                             const int32_t* nbr_indptr, const int32_t* nbr_indices,
+                             const void* nbr_filter, float a,
                              float b, float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
                              int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
                              int64_t concurrency, int32_t* diverged, void* stream) {
@@ -347,8 +392,8 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
     const unsigned bs = block_for(concurrency);
     const unsigned gs = bs < 256 ? 1u : grid_for(items, concurrency);
     sgd_epoch_kernel<<<gs, bs, 0, st>>>(
-        (int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr, nbr_indices, a, b,
-        lr, e, n_neg, items, start, windowed, seed, diverged);
+        (int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr, nbr_indices,
+        (const uint4*)nbr_filter, a, b, lr, e, n_neg, items, start, windowed, seed, diverged);
     GU_CHECK_LAUNCH("sgd_epoch_kernel");
   }
   return GU_OK;

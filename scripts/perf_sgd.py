@@ -23,7 +23,7 @@ for ep in range(6):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     _lib.call("gu_sgd_epochs", plan.n, plan.E, _lib.ptr(xy), _lib.ptr(plan.edges),
-              _lib.ptr(plan.nbr_indptr), _lib.ptr(plan.nbr_indices), float(a), float(b), 1.0,
+              _lib.ptr(plan.nbr_indptr), _lib.ptr(plan.nbr_indices), _lib.ptr(plan.filter), float(a), float(b), 1.0,
               200, ep, ep + 1, 5, E, 0, plan.seed, conc, _lib.ptr(div), stream_ptr(dev))
     e1.record(); e1.synchronize()
     ms = e0.elapsed_time(e1)

@@ -419,3 +419,22 @@ def test_pinned_host_inputs(gu):
     _, b = gu.partial_bfs(gp, 15, seed=7)
     assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.dst, b.dst)
     assert np.array_equal(a.dist, b.dist)
+
+
+def test_sgd_neighbor_filter_covers_neighbors(gu):
+    """The SGD negative-sampling Bloom words (csrc/sgd.cu) have the bit of
+    every neighbour set, so skipping the row search on a clear bit never
+    accepts a neighbour."""
+    from paper_2509_19703_b200.layout import _plan_for
+    import torch
+
+    g = gu.synth_graph("scale_free", 5000, seed=4, m0=3)
+    _, knn = gu.partial_bfs(g, 15, seed=1)
+    gk = gu.smooth_knn_weights(knn)
+    plan = _plan_for(gk, 0, torch.device("cuda"))
+    filt = plan.filter.cpu().numpy().view(np.uint32)
+    ip, ix = gk.nbr_indptr, gk.nbr_indices
+    src = np.repeat(np.arange(gk.n), np.diff(ip))
+    h = ((ix.astype(np.uint64) * np.uint64(0x9E3779B1)) & np.uint64(0xFFFFFFFF)) >> np.uint64(25)
+    words = filt[src, (h >> np.uint64(5)).astype(np.int64)]
+    assert np.all((words >> (h & np.uint64(31)).astype(np.uint32)) & 1)
