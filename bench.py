@@ -157,7 +157,7 @@ def run_ours(args):
     import paper_2509_19703_b200 as gu
     from paper_2509_19703_b200 import _lib
     from paper_2509_19703_b200.device import device_csr, stream_ptr
-    from paper_2509_19703_b200.distributed import gather_records, pack_records, shard_range
+    from paper_2509_19703_b200.distributed import gather_shards, shard_buffers, shard_range
     from paper_2509_19703_b200.neighbors import partial_bfs_records
 
     g, gen_s = build_graph("c5")
@@ -172,11 +172,15 @@ def run_ours(args):
     torch.cuda.synchronize()
     scanned, expanded = (int(x) for x in work.cpu().tolist())
 
+    # records land in the padded shard buffers the all_gather sends as they are
+    bufs = shard_buffers(per, K_NN, dev)
+    out = (bufs[0][: end - begin], bufs[1][: end - begin], bufs[2][: end - begin])
+
     def step():
-        nbr, dd, cnt = partial_bfs_records(csr, K_NN, SEED, begin, end)
+        partial_bfs_records(csr, K_NN, SEED, begin, end, out=out)
         if ws > 1:
-            gather_records(pack_records(nbr, dd, cnt, per))
-        return nbr
+            gather_shards(bufs, n)
+        return bufs[0]
 
     for _ in range(args.warmup):
         step()
@@ -254,7 +258,8 @@ def run_ours(args):
                      "traffic": traffic, "peak_source": peak_kind,
                      "kernel": "gu_partial_bfs_knn (tier F pbfs_fast<8>, 98% of the call)",
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)},
-        "gpu_launches": 4 * args.steps,
+        # per step: tier F, tiers 1a / 1b, slot clear, tier 2 (NCCL kernels not counted)
+        "gpu_launches": 5 * args.steps,
         "clocks": clk.summary(),
         "fixture_gen_s": round(gen_s, 2),
     }
@@ -266,6 +271,8 @@ def run_ours(args):
         if not args.skip_layout:
             result["layout_e2e"] = _layout_e2e(gu)
             result["full_path"] = _full_path(gu, peak)
+        if not args.skip_next:
+            result["next_rows"] = _next_rows(gu, g)
         if not args.skip_cpu:
             result["cpu_baseline"] = _cpu_baseline(g)
         print(json.dumps(result), flush=True)
@@ -438,6 +445,56 @@ def _layout_e2e(gu):
             "c1_gumap_seconds": _layout_gumap_c1(gu)}
 
 
+
+def _next_rows(gu, g5):
+    """SURVEY 8(f) rows measured on this GPU (seconds, one warm run then the
+    best of two): quality metrics on a c3 SL layout, spectral_init on c4, the
+    sparsifier on the c2 base graph, build_graph + LCC at c5 scale.  CPU
+    comparisons: profiles/r01_{metrics,spectral,sparsify,ingest}_perf.log."""
+    import torch
+
+    from paper_2509_19703_b200 import fixtures
+    from paper_2509_19703_b200 import graph as G
+    from paper_2509_19703_b200 import metrics as M
+    from paper_2509_19703_b200 import sparsify as S
+
+    def best(fn, *a):
+        fn(*a)
+        ts = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            v = fn(*a)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t)
+        return v, round(min(ts), 4)
+
+    out = {}
+    try:
+        g3 = fixtures.scale_free(100_000, seed=2, m0=3)
+        _, knn = gu.partial_bfs(g3, 15, seed=0)
+        gk = gu.smooth_knn_weights(knn)
+        E = gk.edge_count
+        lay = gu.optimize_sampled(gk, gu.random_init(g3, 0, 10.0), gu.OptimizerConfig(
+            iterations=200, k=15, seed=0, samp=math.log(0.1 * E) / math.log(E)))
+        v1, t1 = best(M.neighborhood_preservation, g3, lay)
+        v2, t2 = best(M.stress, g3, lay)
+        v3, t3 = best(M.count_crossings, g3, lay)
+        out["metrics_c3"] = {"np": v1, "np_s": t1, "stress": v2, "stress_s": t2,
+                             "crossings": v3, "crossings_s": t3}
+        g4 = fixtures.config_graph("c4")
+        _, t = best(gu.spectral_init, g4, 0)
+        out["spectral_init_c4_s"] = t
+        g2 = fixtures.erdos_renyi(20000, avg_degree=200, seed=1)
+        sg, t = best(S.make_sparsifier, g2)
+        out["sparsify_c2_base"] = {"m_in": g2.m, "m_out": sg.m, "seconds": t}
+        pairs = np.asarray(g5.edges)
+        _, tb = best(G.build_graph, pairs)
+        out["build_graph_c5_s"] = tb
+    except Exception as exc:  # noqa: BLE001 -- report, never fail the headline
+        out["error"] = repr(exc)
+    return out
+
 def _cpu_full_pass(O, g, thr):
     """One pass of the oracle's C port over every source of the c5 graph:
     (seconds, TE)."""
@@ -505,6 +562,7 @@ def main():
     ap.add_argument("--skip-sgd", action="store_true")
     ap.add_argument("--skip-layout", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-next", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

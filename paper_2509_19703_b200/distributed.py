@@ -5,14 +5,15 @@ Every BFS source is independent and its RNG stream is per source
 ``spawn_key=(v,)``), so splitting the source range across ranks reproduces
 the single-GPU records bit for bit.  One process per GPU, the graph CSR
 replicated in each GPU's HBM; each rank computes the fixed-size records
-(k neighbour ids, k distances, count) of its contiguous source range, and a
-single ``all_gather`` (NCCL over NVLink/NVSwitch on B200s, gloo in the CPU
-tests) hands every rank the full kNN lists for C1.  C2 (SGD) stays on one GPU.
+(k neighbour ids, k distances, count) of its contiguous source range straight
+into padded per-rank buffers, and ``all_gather`` of those buffers (NCCL over
+NVLink/NVSwitch on B200s, gloo in the CPU tests) hands every rank the full kNN
+lists for C1 -- no packing copies on the data path.  C2 (SGD) stays on one
+GPU.
 
-The record packing / gather / unpacking below is backend-agnostic torch code,
-so the exchange is testable with gloo on CPU tensors; the records
-themselves only ever come from the GPU kernels (or, in tests, from the
-oracle).
+The buffer / gather code below is backend-agnostic torch, so the exchange is
+testable with gloo on CPU tensors; the records themselves only ever come
+from the GPU kernels (or, in tests, from the oracle).
 """
 
 import torch
@@ -32,28 +33,26 @@ def shard_range(n, rank, world, align=1):
     return begin, end, per
 
 
-def pack_records(nbr, dist_, cnt, per):
-    """(nbr[ns,k], dist[ns,k], cnt[ns]) -> int32 [per, 2k+1], zero padded."""
-    ns, k = nbr.shape
-    rec = torch.zeros((per, 2 * k + 1), dtype=torch.int32, device=nbr.device)
-    rec[:ns, :k] = nbr
-    rec[:ns, k:2 * k] = dist_
-    rec[:ns, 2 * k] = cnt
-    return rec
+def shard_buffers(per, k, device, dtype=torch.int32):
+    """Padded per-rank record buffers (nbr [per, k], dist [per, k], cnt [per])
+    that the kernels write in place (first ns rows) and all_gather sends as
+    they are; padding rows only ever sit past n, in the last rank's block."""
+    return (torch.empty((per, k), dtype=dtype, device=device),
+            torch.empty((per, k), dtype=dtype, device=device),
+            torch.zeros(per, dtype=dtype, device=device))
 
 
-def gather_records(rec, group=None):
-    """all_gather of equal-size record blocks -> [world * per, 2k+1]."""
+def gather_shards(bufs, n, group=None):
+    """all_gather each padded buffer -> the first n rows of the
+    concatenation: (nbr [n, k], dist [n, k], cnt [n])."""
     world = dist.get_world_size(group)
-    out = torch.empty((world * rec.shape[0], rec.shape[1]), dtype=rec.dtype, device=rec.device)
-    dist.all_gather_into_tensor(out, rec.contiguous(), group=group)
-    return out
-
-
-def unpack_records(allrec, n, k):
-    """Inverse of pack_records over the concatenation, first n rows."""
-    rows = allrec[:n]
-    return rows[:, :k].contiguous(), rows[:, k:2 * k].contiguous(), rows[:, 2 * k].contiguous()
+    out = []
+    for b in bufs:
+        full = torch.empty((world * b.shape[0],) + tuple(b.shape[1:]), dtype=b.dtype,
+                           device=b.device)
+        dist.all_gather_into_tensor(full, b.contiguous(), group=group)
+        out.append(full[:n])
+    return tuple(out)
 
 
 def sharded_knn(g, k, seed=0, mode="partial", group=None):
@@ -72,16 +71,19 @@ def sharded_knn(g, k, seed=0, mode="partial", group=None):
     if mode == "partial":
         k_eff = min(k, n - 1) if n > 1 else 0
         begin, end, per = shard_range(n, rank, world, align=1)
-        nbr, dd, cnt = partial_bfs_records(csr, k_eff, seed, begin, end)
     elif mode == "full":
         k_eff = k
         begin, end, per = shard_range(n, rank, world, align=64)
-        nbr, dd, cnt = full_knn_records(csr, k_eff, seed, begin, end)
     else:
         raise ValueError(f"unknown mode {mode!r}")
-    rec = pack_records(nbr, dd, cnt, per)
-    allrec = gather_records(rec, group)
-    nbr, dd, cnt = unpack_records(allrec, n, max(k_eff, 1))
+    bufs = shard_buffers(per, max(k_eff, 1), dev)
+    ns = end - begin
+    out = (bufs[0][:ns], bufs[1][:ns], bufs[2][:ns])
+    if mode == "partial":
+        partial_bfs_records(csr, k_eff, seed, begin, end, out=out)
+    else:
+        full_knn_records(csr, k_eff, seed, begin, end, out=out)
+    nbr, dd, cnt = gather_shards(bufs, n, group)
     short = int((cnt < k_eff).sum().item()) if n else 0
     if rank == 0:
         _warn_short(short)

@@ -309,14 +309,19 @@ def partial_bfs_records(csr, k_eff, seed, src_begin, src_end, work=None, tier2_w
     return nbr, dist, cnt
 
 
-def full_knn_records(csr, k, seed, src_begin, src_end, work=None, batches_in_flight=None):
-    """Fused full-BFS kNN records of sources [src_begin, src_end) (device)."""
+def full_knn_records(csr, k, seed, src_begin, src_end, work=None, batches_in_flight=None,
+                     out=None):
+    """Fused full-BFS kNN records of sources [src_begin, src_end) (device),
+    written into ``out`` when given."""
     dev = csr.device
     ns = src_end - src_begin
     kk = max(k, 1)
-    nbr = torch.empty((ns, kk), dtype=torch.int32, device=dev)
-    dist = torch.empty((ns, kk), dtype=torch.int32, device=dev)
-    cnt = torch.empty(ns, dtype=torch.int32, device=dev)
+    if out is None:
+        nbr = torch.empty((ns, kk), dtype=torch.int32, device=dev)
+        dist = torch.empty((ns, kk), dtype=torch.int32, device=dev)
+        cnt = torch.empty(ns, dtype=torch.int32, device=dev)
+    else:
+        nbr, dist, cnt = out
     n = csr.n
     lib = _lib.load()
     if batches_in_flight is None:

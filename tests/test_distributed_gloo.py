@@ -1,9 +1,9 @@
 """world_size-2 gloo test of the source-sharded record exchange (CPU).
 
 Each rank produces the fixed-size kNN records of its source shard (here with
-the oracle, the checker; on B200s the records come from the GPU kernels),
-packs them, all-gathers them through paper_2509_19703_b200.distributed and
-unpacks.  The gathered records must equal the single-process result
+the oracle, the checker; on B200s the GPU kernels write them in place) into
+the padded shard buffers and all-gathers them through
+paper_2509_19703_b200.distributed.  The gathered records must equal the single-process result
 bit for bit (per-source RNG streams make sharding exact).
 """
 
@@ -35,8 +35,7 @@ def _worker(rank, world, port, mode, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import oracle as O
     from paper_2509_19703_b200 import fixtures as F
-    from paper_2509_19703_b200.distributed import (gather_records, pack_records, shard_range,
-                                                   unpack_records)
+    from paper_2509_19703_b200.distributed import gather_shards, shard_buffers, shard_range
 
     g = F.scale_free(3000, seed=7, m0=2) if mode == "partial" else F.grid(900)
     k = 15
@@ -46,10 +45,12 @@ def _worker(rank, world, port, mode, out_dir):
         nbr, dd, cnt = O.partial_bfs_raw(g, k, seed=3, src_begin=b, src_end=e, nthreads=2)
     else:
         nbr, dd, cnt = O.full_knn(g, k, seed=3, src_begin=b, src_end=e, nthreads=2, packed=False)
-    rec = pack_records(torch.from_numpy(nbr.reshape(-1, k)), torch.from_numpy(dd.reshape(-1, k)),
-                       torch.from_numpy(cnt), per)
-    allrec = gather_records(rec)
-    n2, d2, c2 = unpack_records(allrec, g.n, k)
+    bufs = shard_buffers(per, k, torch.device("cpu"))
+    ns = e - b
+    bufs[0][:ns] = torch.from_numpy(nbr.reshape(-1, k))   # the kernels write these rows in place
+    bufs[1][:ns] = torch.from_numpy(dd.reshape(-1, k))
+    bufs[2][:ns] = torch.from_numpy(cnt)
+    n2, d2, c2 = gather_shards(bufs, g.n)
     np.savez(os.path.join(out_dir, f"{mode}_{rank}.npz"), nbr=n2.numpy(), dist=d2.numpy(),
              cnt=c2.numpy())
     dist.destroy_process_group()
