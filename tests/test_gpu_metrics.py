@@ -94,3 +94,35 @@ def test_metrics_errors_and_small(gu):
     x = graph_from_edges(4, [(0, 1), (2, 3)])
     cross = _layout(gu, np.array([[0, 0], [2, 2], [0, 2], [2, 0]], np.float64))
     assert M.count_crossings(x, cross) == 1
+
+
+def test_quality_c3_exact_vs_reference(gu):
+    """Check (c) at SL scale with EXACT metrics on both sides: NP, stress and
+    crossings of the GPU c3 SL layouts (GPU metrics) vs those of the
+    reference's own c3 SL layouts (oracle metrics, tests/golden/
+    quality_c3_full.npz); no worse than 4 standard errors."""
+    import math
+
+    from paper_2509_19703_b200 import metrics as M
+
+    z = load_golden("quality_c3_full.npz")
+    ref = np.stack([z["np_"], z["stress"], z["crossings"].astype(np.float64)], axis=1)
+    if ref.shape[0] < 2:
+        pytest.skip("reference fixture holds fewer than 2 seeds")
+    g = gu.synth_graph("scale_free", 100000, seed=2, m0=3)
+    vals = []
+    for seed in range(3):
+        _, knn = gu.partial_bfs(g, 15, seed=seed)
+        gk = gu.smooth_knn_weights(knn)
+        E = gk.edge_count
+        cfg = gu.OptimizerConfig(iterations=200, k=15, seed=seed,
+                                 samp=math.log(0.1 * E) / math.log(E))
+        lay = gu.optimize_sampled(gk, gu.random_init(g, seed, 10.0), cfg)
+        vals.append((M.neighborhood_preservation(g, lay), M.stress(g, lay), M.count_crossings(g, lay)))
+    v = np.array(vals, dtype=np.float64)
+    print("check (c) c3 exact mean ratios gpu/ref [np, stress, crossings]:",
+          v.mean(axis=0) / ref.mean(axis=0))
+    se = ref.std(axis=0, ddof=1) / math.sqrt(ref.shape[0]) + v.std(axis=0, ddof=1) / math.sqrt(v.shape[0])
+    assert v.mean(axis=0)[0] >= ref.mean(axis=0)[0] - 4 * se[0]
+    assert v.mean(axis=0)[1] <= ref.mean(axis=0)[1] + 4 * se[1]
+    assert v.mean(axis=0)[2] <= ref.mean(axis=0)[2] + 4 * se[2]
