@@ -78,216 +78,15 @@ __device__ __forceinline__ int umod64_small(unsigned long long x, int d) {
 // sorted adjacency in turn.  Concatenating the frontier's adjacency lists in
 // that order (the "flattened" index t) and keeping each vertex at its first
 // occurrence t -- and only if no earlier level holds it -- therefore yields
-// the next level in exactly the reference's order.  A group of G lanes walks
-// t in chunks of G: the parent of t is found from a per-level bitmap of
-// adjacency-start positions (popc), __match_any_sync elects the lowest lane of
-// equal ids inside a chunk, and that lane's atomicCAS into the per-source hash
-// succeeds iff the id was never seen in an earlier chunk or level.
-// ballot/popc compacts the winners in t order.  All warp-collective calls use
-// the full mask with loops bounded by the warp-wide maximum, so the 32/G
-// sources of a warp advance in lockstep.
-template <int G, int CAP, int PCAP, int TCAP, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    pbfs_tier1(const int* __restrict__ indptr, const int* __restrict__ indices,
-               int K, unsigned long long seed, long long src_begin, long long nsrc,
-               const int* __restrict__ list, const int* __restrict__ list_count,
-               int* __restrict__ out_nbr, int* __restrict__ out_dist,
-               int* __restrict__ out_cnt, int* __restrict__ ovf_list,
-               int* __restrict__ ovf_count, unsigned long long* __restrict__ work) {
-  using L = Tier1<G, CAP, PCAP, TCAP>;
-  constexpr int HC = L::HC, TW = L::TW, NG = L::NG;
-  constexpr unsigned GM = G == 32 ? FULL : ((1u << G) - 1u);
-  extern __shared__ __align__(16) int smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gid = lane / G, gl = lane % G, gbase = gid * G;
-  const unsigned lt_g = (1u << gl) - 1u;  // lanes below me inside the group
-  int* hkey = smem + (warp * NG + gid) * L::WORDS;
-  int* disc = hkey + HC;
-  int* ppre = disc + CAP;
-  int* pbeg = ppre + PCAP;
-  unsigned* bmap = reinterpret_cast<unsigned*>(pbeg + PCAP);
+// the next level in exactly the reference's order.  The warp tiers
+// below walk t in chunks of 32: the parent of t comes from adjacency-start
+// bits (popc), __match_any_sync elects the lowest lane of equal ids inside a
+// chunk, and that lane's atomicCAS into the per-source hash succeeds iff the
+// id was never seen in an earlier chunk or level; ballot/popc compacts the
+// winners in t order.
 
-  unsigned long long w_scanned = 0, w_expanded = 0;
-  const long long total = list ? (long long)(*list_count) : nsrc;
-  const long long stride = (long long)gridDim.x * WARPS * NG;
-  for (long long item = ((long long)blockIdx.x * WARPS + warp) * NG + gid;; item += stride) {
-    const bool has = item < total;
-    if (!__any_sync(FULL, has)) break;
-    const int s = has ? (list ? list[item] : (int)(src_begin + item)) : 0;
-    {
-      int4* h4 = reinterpret_cast<int4*>(hkey);
-#pragma unroll
-      for (int i = gl; i < HC / 4; i += G) h4[i] = make_int4(-1, -1, -1, -1);
-    }
-    __syncwarp();
-    if (has && gl == 0) {
-      hkey[hash_id(s) & (HC - 1)] = s;
-      disc[0] = s;
-    }
-    __syncwarp();
-    int lb = 0, le = 1, count = 0, depth = 0;
-    bool live = has, ovf = false, l1_sorted = false;
-    int my_v = 0, my_d = 0, my_lvl0 = 0, my_lvln = 0;  // my entry, its level's [start, end)
-    unsigned long long scanned = 0, expanded = 0;
-    while (__any_sync(FULL, live)) {
-      int f = live ? le - lb : 0;
-      if (f > PCAP) {
-        ovf = true;
-        live = false;
-        f = 0;
-      }
-      // ---- frontier: degrees, prefix, non-empty parents compacted, bitmap
-      for (int w = gl; w < TW; w += G) bmap[w] = 0u;
-      __syncwarp();
-      int carry = 0, nne = 0;
-      for (int i0 = 0; __any_sync(FULL, i0 < f); i0 += G) {
-        const int i = i0 + gl;
-        int d = 0, b = 0;
-        if (i < f) {
-          const int u = disc[lb + i];
-          b = __ldg(indptr + u);
-          d = __ldg(indptr + u + 1) - b;
-        }
-        int inc = d;
-#pragma unroll
-        for (int o = 1; o < G; o <<= 1) {
-          const int tt = __shfl_up_sync(FULL, inc, o, G);
-          if (gl >= o) inc += tt;
-        }
-        const unsigned ne = (__ballot_sync(FULL, d > 0) >> gbase) & GM;
-        if (d > 0) {
-          const int r = nne + __popc(ne & lt_g);
-          const int p0 = carry + inc - d;
-          ppre[r] = p0;
-          pbeg[r] = b;
-          if (p0 < TCAP) atomicOr(&bmap[p0 >> 5], 1u << (p0 & 31));
-        }
-        carry += __shfl_sync(FULL, inc, G - 1, G);
-        nne += __popc(ne);
-      }
-      const int T = live ? carry : 0;
-      if (T > TCAP) {
-        ovf = true;
-        live = false;
-      }
-      __syncwarp();
-      if (live) {
-        scanned += T;
-        expanded += f;
-      }
-      depth++;
-      // ---- expansion of the flattened frontier adjacency
-      const int room = CAP - le;
-      int nst = 0, pb = -1;
-      bool fail = false;
-      const int Tl = live ? T : 0;
-      for (int t0 = 0; __any_sync(FULL, t0 < Tl); t0 += G) {
-        const bool act = gl + t0 < Tl;
-        unsigned m = 0u;
-        if (t0 < Tl) {
-          m = bmap[t0 >> 5];
-          if (G < 32) m = (m >> (t0 & 31)) & GM;
-        }
-        int w = -1;
-        if (act) {
-          const int p = pb + __popc(m & ((2u << gl) - 1u));
-          w = __ldg(indices + pbeg[p] + (t0 + gl - ppre[p]));
-        }
-        pb += __popc(m);
-        const unsigned long long key = ((unsigned long long)gid << 32) | (unsigned)w;
-        const unsigned grp = __match_any_sync(FULL, key);
-        bool isnew = false;
-        if (act && lane == __ffs(grp) - 1) {
-          unsigned h = hash_id(w) & (HC - 1);
-          int probe = 0;
-          for (; probe < HC; probe++) {
-            const int old = atomicCAS(&hkey[h], -1, w);
-            if (old == -1) {
-              isnew = true;
-              break;
-            }
-            if (old == w) break;
-            h = (h + 1) & (HC - 1);
-          }
-          if (probe == HC) fail = true;
-        }
-        const unsigned bal = (__ballot_sync(FULL, isnew) >> gbase) & GM;
-        if (isnew) {
-          const int pos = nst + __popc(bal & lt_g);
-          if (pos < room) disc[le + pos] = w;
-        }
-        nst += __popc(bal);
-      }
-      if ((__ballot_sync(FULL, fail) >> gbase) & GM) fail = true;
-      if (live && (fail || nst > room - 1)) {
-        ovf = true;
-        live = false;
-      }
-      if (live && nst == 0) live = false;  // component exhausted
-      __syncwarp();
-      const int remaining = K - count;
-      const bool cross = live && nst > remaining;
-      // ---- crossing level: random subset (_kernels.py:98-105)
-      int j = 0;
-      if (cross && gl < remaining)
-        j = gl + (int)(splitmix_at(seed + SPLIT_GAMMA * (unsigned long long)(s + 1), gl) %
-                       (unsigned long long)(nst - gl));
-      const int rem_c = cross ? remaining : 0;
-      for (int i = 0; __any_sync(FULL, i < rem_c); i++) {
-        const int ji = __shfl_sync(FULL, j, i, G);
-        if (gl == 0 && i < rem_c) {
-          const int a = disc[le + i];
-          disc[le + i] = disc[le + ji];
-          disc[le + ji] = a;
-        }
-      }
-      __syncwarp();
-      if (live) {
-        const int take = cross ? remaining : nst;
-        if (depth == 1 && !cross) l1_sorted = true;  // level 1 == sorted adjacency of s
-        if (gl >= count && gl < count + take) {
-          my_v = disc[le + gl - count];
-          my_d = depth;
-          my_lvl0 = count;
-          my_lvln = count + take;
-        }
-        count += take;
-        lb = le;
-        le += nst;
-        if (count >= K) live = false;
-      }
-    }
-    // ---- output: (dist, id) order; levels are already in dist order, so
-    //      only ids inside a level need ranking (level 1 comes sorted)
-    const bool emit = has && !ovf;
-    const bool mine = emit && gl < count;
-    int pos = gl;
-    int seg = (mine && !(my_d == 1 && l1_sorted)) ? my_lvln - my_lvl0 : 0;
-    if (seg) pos = my_lvl0;
-    for (int k2 = 0; __any_sync(FULL, k2 < seg); k2++) {
-      const int src = gbase + (k2 < seg ? my_lvl0 + k2 : gl);
-      const int vj = __shfl_sync(FULL, my_v, src);
-      if (k2 < seg && vj < my_v) pos++;
-    }
-    if (mine) {
-      const long long row = (long long)s - src_begin;
-      out_nbr[row * K + pos] = my_v;
-      out_dist[row * K + pos] = my_d;
-    }
-    if (emit && gl == 0) out_cnt[(long long)s - src_begin] = count;
-    if (has && ovf && gl == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
-    if (emit) {
-      w_scanned += scanned;
-      w_expanded += expanded;
-    }
-  }
-  if (work && gl == 0) {
-    atomicAdd(work, w_scanned);
-    atomicAdd(work + 1, w_expanded);
-  }
-}
-
-// Lean warp-per-source variant of tier 1 (the default first tier).
+// Lean warp per source: tiers 1a (CAP 128) and 1b (CAP 1024), the fallbacks of
+// the register fast path F for any ball shape and k <= 32.
 //   * level 1 is the sorted adjacency of s itself: no dedupe beyond the hash
 //     insert, and (when not crossing) already in output order;
 //   * deeper levels: parent of a flattened index from a per-level bitmap of

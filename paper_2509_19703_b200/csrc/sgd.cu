@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
       p = (long long)tperm((unsigned long long)t) * TILE + (i - t * TILE);
       if (p >= E) continue;  // partial last tile maps onto itself
     }
-    const int4 rec = __ldg(edges + p);
+    const int4 rec = __ldcs(edges + p);  // streamed once per epoch: evict-first, keep L2 for x / filter / rows
     const int u = rec.x, v = rec.y;
     const uint4 fw = filt ? __ldg(filt + u) : make_uint4(~0u, ~0u, ~0u, ~0u);
     const float h = __int_as_float(rec.z);
