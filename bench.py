@@ -442,7 +442,57 @@ def _layout_e2e(gu):
     return {"metric": "end-to-end layout seconds", "config": "c3 SL-GUMAP BA(100k, m0=3), "
             "200 epochs, 10% window, random init, host arrays in/out", "value": round(min(ts), 4),
             "unit": "s", "higher_is_better": False,
-            "c1_gumap_seconds": _layout_gumap_c1(gu)}
+            "c1_gumap_seconds": _layout_gumap_c1(gu),
+            "configs": _layout_e2e_configs(gu)}
+
+
+def _layout_e2e_configs(gu):
+    """End-to-end layout seconds on BASELINE c2 (SS-GUMAP: the shared G'
+    fixture through g_prime=, all-pairs BFS kNN, 200 full epochs) and c4
+    (SSSL-GUMAP: SBM 1M, sparsifier identity at this density, partial BFS,
+    200 windowed epochs at the default samp=0.9).  Two numbers each: the
+    public driver (run_*_gumap, which starts from spectral_init as the
+    reference's drivers do) and the C0 -> C1 -> C2 pipeline from random init.
+    Graph generation is outside the timing."""
+    import torch
+
+    from paper_2509_19703_b200 import fixtures
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        return round(time.perf_counter() - t, 4)
+
+    out = {}
+    try:
+        g2p = fixtures.config_graph("c2")  # G' of ER(20000, 200)
+        cfg2 = gu.OptimizerConfig(iterations=200, k=15, seed=1)
+
+        def c2_pipe():
+            knn = gu.knn_from_full_distances(gu.all_pairs_bfs(g2p), 15, seed=1)
+            gk = gu.smooth_knn_weights(knn)
+            return gu.optimize_full(gk, gu.random_init(g2p, 1, 10.0), cfg2, tag="SS")
+
+        out["c2_ss_gumap"] = {"n": g2p.n, "m_gprime": g2p.m,
+                              "driver_s": timed(lambda: gu.run_ss_gumap(g2p, cfg2, g_prime=g2p)),
+                              "random_init_pipeline_s": timed(c2_pipe)}
+        g4 = fixtures.config_graph("c4")
+        cfg4 = gu.OptimizerConfig(iterations=200, k=15, seed=3)
+
+        def c4_pipe():
+            _, knn = gu.partial_bfs(g4, 15, seed=3)
+            gk = gu.smooth_knn_weights(knn)
+            return gu.optimize_sampled(gk, gu.random_init(g4, 3, 10.0), cfg4, tag="SSSL")
+
+        out["c4_sssl_gumap"] = {"n": g4.n, "m": g4.m,
+                                "driver_s": timed(lambda: gu.run_sssl_gumap(g4, cfg4)),
+                                "random_init_pipeline_s": timed(c4_pipe)}
+    except Exception as exc:  # noqa: BLE001 -- report, never fail the headline
+        out["error"] = repr(exc)
+    return out
 
 
 
