@@ -32,6 +32,8 @@ namespace {
 
 constexpr int TILE = 1024;
 constexpr int SGD_NEG_BLOCK = 5;
+static_assert(SGD_NEG_BLOCK <= 8, "slot bits of the cooperative search owner tag");
+constexpr unsigned FULL = 0xffffffffu;
 #ifndef SGD_MIN_BLOCKS
 #define SGD_MIN_BLOCKS 4  // <= 64 registers: 32 warps per SM
 #endif  // negatives handled in lockstep per block
@@ -144,35 +146,50 @@ __device__ __forceinline__ bool filt_maybe(uint4 f, int c) {
   return (w >> (h & 31)) & 1u;
 }
 
+constexpr int SGD_WARPS = 8;  // 256 threads per block at most (block_for)
+
 __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
     sgd_epoch_kernel(int n, long long E, float2* __restrict__ xy, const int4* __restrict__ edges,
                      const int* __restrict__ nip, const int* __restrict__ nix,
                      const uint4* __restrict__ filt, float a, float b, float lr, int epoch,
                      int n_neg, long long items, long long start, int windowed,
                      unsigned long long seed, int* __restrict__ diverged) {
+  // (candidate, row begin, row end, owner lane * 8 + slot) of the warp's
+  // filter hits, and each lane's bitmask of slots found to be neighbours
+  __shared__ int4 sh_pairs[SGD_WARPS][32 * SGD_NEG_BLOCK];
+  __shared__ unsigned sh_hit[SGD_WARPS][32];
   const long long ntiles = (E + TILE - 1) / TILE;
   Feistel tperm((unsigned long long)ntiles, mix64(seed ^ (0x51ED27ull + (unsigned long long)epoch)));
   const unsigned long long rkey = mix64(seed ^ (0xA5A5A5A5ull * (unsigned long long)(epoch + 1)));
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   bool bad = false;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < items;
-       i += (long long)gridDim.x * blockDim.x) {
-    long long p;
-    if (windowed) {
-      p = start + i;
-      if (p >= E) p -= E;
-    } else {
-      const long long t = i / TILE;
-      p = (long long)tperm((unsigned long long)t) * TILE + (i - t * TILE);
-      if (p >= E) continue;  // partial last tile maps onto itself
+  // warp-uniform loop (every lane reaches the collectives below); lanes past
+  // the end ride along inactive
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < items;
+       i0 += stride) {
+    const long long i = i0 + lane;
+    bool act = i < items;
+    long long p = 0;
+    if (act) {
+      if (windowed) {
+        p = start + i;
+        if (p >= E) p -= E;
+      } else {
+        const long long t = i / TILE;
+        p = (long long)tperm((unsigned long long)t) * TILE + (i - t * TILE);
+        if (p >= E) act = false;  // partial last tile maps onto itself
+      }
     }
-    const int4 rec = __ldcs(edges + p);  // streamed once per epoch: evict-first, keep L2 for x / filter / rows
+    // streamed once per epoch: evict-first, keep L2 for x / filter / rows
+    const int4 rec = act ? __ldcs(edges + p) : make_int4(0, 0, 0, 0);
     const int u = rec.x, v = rec.y;
     const uint4 fw = filt ? __ldg(filt + u) : make_uint4(~0u, ~0u, ~0u, ~0u);
     const float h = __int_as_float(rec.z);
     float2 xu = xy[u];
     const float2 xv = xy[v];
     float dux = 0.f, duy = 0.f;
-    {
+    if (act) {
       const float dx = xu.x - xv.x, dy = xu.y - xv.y;
       const float d2 = dx * dx + dy * dy;
       if (d2 > 0.f) {
@@ -188,71 +205,83 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
       }
     }
     // repulsions.  Try t of slot q draws 64 bits from draw64(epoch key, p,
-    // q, t): the high half picks the candidate, the low half is its theta.  The
-    // first tries of all slots are known up front, so their neighbour tests
-    // run as lockstep binary searches over the head's sorted row (bounds
-    // loaded once), and their coordinate loads are issued together; a
-    // rejected try (c == u or a neighbour: probability ~deg/n) takes the
-    // sequential retry path.  The repulsion math itself stays sequential in
-    // slot order on the register copy of x_u, as in the reference sweep.
-    int rb, re;
-    if (rec.w >= 0) {
-      rb = rec.w >> 6;
-      re = rb + (rec.w & 63);
-    } else {
-      rb = __ldg(nip + u);
-      re = __ldg(nip + u + 1);
+    // q, t): the high half picks the candidate, the low half is its theta.
+    // The first tries of all slots are known up front: their coordinate
+    // loads go out at once, and only the candidates whose neighbour-filter
+    // bit is set (~deg/128 of them) are searched in the head's sorted row --
+    // cooperatively, one (candidate, row) pair per lane across the warp.  A
+    // rejected try (c == u or a neighbour) takes the sequential retry path.
+    // The repulsion math stays sequential in slot order on the register copy
+    // of x_u, as in the reference sweep.
+    int rb = 0, re = 0;
+    if (act) {
+      if (rec.w >= 0) {
+        rb = rec.w >> 6;
+        re = rb + (rec.w & 63);
+      } else {
+        rb = __ldg(nip + u);
+        re = __ldg(nip + u + 1);
+      }
     }
     for (int q0 = 0; q0 < n_neg; q0 += SGD_NEG_BLOCK) {
       const int nq = min(SGD_NEG_BLOCK, n_neg - q0);
-      int cand[SGD_NEG_BLOCK], lo[SGD_NEG_BLOCK], len[SGD_NEG_BLOCK];
+      int cand[SGD_NEG_BLOCK];
       unsigned spare_q[SGD_NEG_BLOCK];
-      bool maybe_any = false;
+      unsigned mm = 0;  // slots whose filter bit is set
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         const unsigned long long r = draw64(rkey, p, q0 + q, 0);
         cand[q] = (int)__umulhi((unsigned)(r >> 32), (unsigned)n);
         spare_q[q] = (unsigned)r;
-        lo[q] = rb;
-        const bool maybe = q < nq && filt_maybe(fw, cand[q]);
-        len[q] = maybe ? re - rb : 0;
-        maybe_any |= maybe;
+        if (act && q < nq && filt_maybe(fw, cand[q])) mm |= 1u << q;
       }
-      // speculative coordinate loads: a random candidate is a neighbour with
-      // probability ~deg/n, so the gathers go out with the draws, in parallel
-      // with the neighbour test instead of after it
       float2 xc[SGD_NEG_BLOCK];
 #pragma unroll
-      for (int q = 0; q < SGD_NEG_BLOCK; q++) xc[q] = q < nq ? xy[cand[q]] : make_float2(0.f, 0.f);
-      // lockstep lower_bound of every candidate in the row: each step issues
-      // all the probes' loads before any compare (branch-free: a finished
-      // search probes rb again), so a step costs one round trip, not one per
-      // candidate; ceil(log2(deg + 1)) steps finish every search
-      const int steps = maybe_any ? 32 - __clz(re - rb) : 0;
-      for (int it = 0; it < steps; it++) {
-        int x[SGD_NEG_BLOCK];
+      for (int q = 0; q < SGD_NEG_BLOCK; q++)
+        xc[q] = (act && q < nq) ? xy[cand[q]] : make_float2(0.f, 0.f);
+      // warp-cooperative neighbour test of the filter hits
+      const int cnt = __popc(mm);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(FULL, incl, 31);
+      unsigned hit = 0;
+      if (total > 0) {  // warp-uniform
+        int pos = incl - cnt;
 #pragma unroll
         for (int q = 0; q < SGD_NEG_BLOCK; q++)
-          x[q] = __ldg(nix + (len[q] > 0 ? lo[q] + (len[q] >> 1) : rb));
-#pragma unroll
-        for (int q = 0; q < SGD_NEG_BLOCK; q++) {
-          const int half = len[q] >> 1;
-          const bool act = len[q] > 0, lt = x[q] < cand[q];
-          lo[q] = (act && lt) ? lo[q] + half + 1 : lo[q];
-          len[q] = act ? (lt ? len[q] - half - 1 : half) : 0;
+          if ((mm >> q) & 1u) sh_pairs[wib][pos++] = make_int4(cand[q], rb, re, lane * 8 + q);
+        sh_hit[wib][lane] = 0;
+        __syncwarp();
+        for (int t = lane; t < total; t += 32) {
+          const int4 pr = sh_pairs[wib][t];
+          int lo = pr.y, len = pr.z - pr.y;
+          while (len > 0) {
+            const int half = len >> 1;
+            if (__ldg(nix + lo + half) < pr.x) {
+              lo += half + 1;
+              len -= half + 1;
+            } else {
+              len = half;
+            }
+          }
+          if (lo < pr.z && __ldg(nix + lo) == pr.x) atomicOr(&sh_hit[wib][pr.w >> 3], 1u << (pr.w & 7));
         }
+        __syncwarp();
+        hit = sh_hit[wib][lane];
+        __syncwarp();  // the buffers are reused by the next slot block
       }
-      bool ok[SGD_NEG_BLOCK];
-#pragma unroll
-      for (int q = 0; q < SGD_NEG_BLOCK; q++)
-        ok[q] = q < nq && cand[q] != u &&
-                !(filt_maybe(fw, cand[q]) && lo[q] < re && __ldg(nix + lo[q]) == cand[q]);
+      if (!act) continue;
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         if (q >= nq) break;
-        int c = ok[q] ? cand[q] : -1;
+        const bool ok = cand[q] != u && !((hit >> q) & 1u);
+        int c = ok ? cand[q] : -1;
         unsigned spare = spare_q[q];  // theta draw of this slot
-        if (!ok[q]) {
+        if (!ok) {
           // retries 2..8 of this slot (rare)
           for (int t = 1; t < 8; t++) {
             const unsigned long long rr = draw64(rkey, p, q0 + q, t);
@@ -287,8 +316,10 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
         xu.y += gy;
       }
     }
-    if (dux != 0.f || duy != 0.f) atomicAdd(&xy[u], make_float2(dux, duy));
-    if (!isfinite(xu.x) || !isfinite(xu.y)) bad = true;
+    if (act) {
+      if (dux != 0.f || duy != 0.f) atomicAdd(&xy[u], make_float2(dux, duy));
+      if (!isfinite(xu.x) || !isfinite(xu.y)) bad = true;
+    }
   }
   if (bad) atomicMin(diverged, epoch);
 }
