@@ -76,7 +76,7 @@ class ClockSampler:
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
 
-    def __init__(self, index=0, period=0.002):
+    def __init__(self, index=0, period=0.001):
         self.index = index
         self.period = period
         self.samples = []
@@ -84,39 +84,54 @@ class ClockSampler:
         self._th = None
 
     def _run(self):
+        if self._nvml is not None:
+            pynvml, h, mx = self._nvml
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, mx, rs))
+                except Exception:  # noqa: BLE001 -- a missed sample, not a failure
+                    pass
+                self._stop.wait(self.period)
+            return
+        q = "clocks.sm,clocks.max.sm"
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip().split(",")
+                self.samples.append((float(out[0]), float(out[1]), 0))
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        # NVML is initialised here, before the timed region starts, so the
+        # sampling thread is live from the region's first microsecond
+        self._nvml = None
         try:
             import pynvml
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, mx, rs))
-                self._stop.wait(self.period)
-            pynvml.nvmlShutdown()
-        except Exception:
-            q = "clocks.sm,clocks.max.sm"
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip().split(",")
-                    self.samples.append((float(out[0]), float(out[1]), 0))
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-
-    def __enter__(self):
+            pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._nvml = (pynvml, h, mx)
+        except Exception:  # noqa: BLE001 -- fall back to nvidia-smi
+            self._nvml = None
         self._th = threading.Thread(target=self._run, daemon=True)
         self._th.start()
-        time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         if self._th:
             self._th.join(timeout=10)
+        if self._nvml is not None:
+            try:
+                self._nvml[0].nvmlShutdown()
+            except Exception:  # noqa: BLE001
+                pass
 
     def summary(self):
         if not self.samples:
@@ -127,7 +142,7 @@ class ClockSampler:
                           if int(r) & bit})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(float(x[1]) for x in self.samples),
                 "sm_min_mhz": min(sm), "reasons": reasons, "samples": len(self.samples),
-                "source": "nvml"}
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def _dist_env():
