@@ -96,21 +96,6 @@ def register_device_csr(g, csr):
 _PIN_THRESHOLD = 1 << 20  # bytes; smaller transfers are not worth pinning
 
 
-def _host_register(arr):
-    """Page-lock a host numpy buffer in place (cudaHostRegister) so the copy
-    runs at full link speed without a staging pass; returns an unregister
-    callable (no-op when registration is unavailable)."""
-    cudart = torch.cuda.cudart()
-    ptr = arr.ctypes.data
-    try:
-        err = cudart.cudaHostRegister(ptr, arr.nbytes, 0)
-    except Exception:
-        return lambda: None
-    if int(err) != 0:
-        return lambda: None
-    return lambda: cudart.cudaHostUnregister(ptr)
-
-
 def to_host(t):
     """Device tensor -> numpy, through a pinned buffer (synchronous).  The
     returned array views the pinned memory (kept alive by the array)."""

@@ -17,7 +17,6 @@ n x n ``matrix`` is only materialised if someone reads it;
 kernel instead.
 """
 
-import math
 import warnings
 
 import numpy as np

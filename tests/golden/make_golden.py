@@ -38,11 +38,6 @@ def sha(a):
     return hashlib.sha256(a.tobytes()).hexdigest()
 
 
-def ref_graph(g):
-    """Reference Graph from our arrays (identical CSR)."""
-    return gu.build_graph([tuple(map(int, e)) for e in g.edges]) if g.m < 400000 else None
-
-
 def flat(lists, dtype):
     if not lists:
         return np.zeros(0, dtype), np.zeros(1, np.int64)
@@ -472,8 +467,9 @@ def gen_sparsify():
     save("sparsify.npz", **out)
 
 def main():
+    # quality_c3_full (~1.5 h on 8 cores) runs only when named
     which = sys.argv[1:] or ["partial_small", "full_small", "smooth_cases", "c1", "c3", "quality_c1",
-                             "quality_c3"]
+                             "quality_c3", "spectral", "sparsify"]
     for w in which:
         globals()["gen_" + w]()
     manifest = dict(numpy=np.__version__, scipy=scipy.__version__, numba=numba.__version__,
