@@ -48,6 +48,84 @@ __global__ void build_keys(long long n, long long nrows, const long long* __rest
   }
 }
 
+// ---- fast path (every row holds kfix <= 32 entries): the "both" array is
+// built row by row instead of by one global 64-bit sort.  The backward
+// entries are stably sorted by their destination only (the source order of
+// the input is kept inside each destination), and each vertex's forward row
+// (sorted in registers, stable) is merged with its backward row.
+
+constexpr unsigned FULL_MASK = 0xffffffffu;
+
+__global__ void fx_indeg(long long nnz, const int* __restrict__ dst, int* __restrict__ indeg,
+                         int* __restrict__ key, int* __restrict__ val) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = dst[i];
+    atomicAdd(indeg + c, 1);
+    key[i] = c;
+    val[i] = (int)i;
+  }
+}
+
+// one warp per vertex u: forward entries u*k .. u*k+k-1 (sorted by (id, i)
+// in registers) merged with the backward entries in_e[in_ptr[u] ..) whose
+// source rows are ascending; equal ids: forward first, each side in original
+// order -- exactly the order of the stable global sort it replaces
+__global__ void fx_merge(long long n, int kfix, long long nnz, const int* __restrict__ dst,
+                         const long long* __restrict__ in_ptr, const int* __restrict__ in_e,
+                         unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long fb = u * kfix;
+    // stable register sort of the forward row by (id, position)
+    unsigned long long fk = lane < kfix ? (((unsigned long long)(unsigned)dst[fb + lane] << 32) | (unsigned)lane)
+                                        : ~0ull;
+    for (int size = 2; size <= 32; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(FULL_MASK, fk, stride);
+        const bool up = (lane & size) == 0;
+        const bool lower = (lane & stride) == 0;
+        const bool take_min = (up == lower);
+        fk = take_min ? (other < fk ? other : fk) : (other > fk ? other : fk);
+      }
+    }
+    const int fid = (int)(fk >> 32);                  // this lane's forward id (sorted)
+    const int fpos = (int)(unsigned)fk;                // its position in the row
+    const long long ib = in_ptr[u], m = in_ptr[u + 1] - ib;
+    const long long out0 = fb + ib;                    // row start in the both array
+    // forward element of rank `lane`: position lane + #backward with id < fid
+    if (lane < kfix) {
+      long long lo = 0, hi = m;
+      while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if ((int)(in_e[ib + mid] / kfix) < fid) lo = mid + 1;
+        else hi = mid;
+      }
+      const long long o = out0 + lane + lo;
+      keys[o] = (unsigned long long)u * (unsigned long long)n + (unsigned long long)fid;
+      vals[o] = (int)(fb + fpos);
+    }
+    // backward elements: position j + #forward with id <= their id
+    for (long long j0 = 0; j0 < m; j0 += 32) {
+      const long long j = j0 + lane;
+      int e = 0, bid = 0;
+      if (j < m) {
+        e = in_e[ib + j];
+        bid = e / kfix;
+      }
+      // upper bound over the sorted forward ids (held one per lane)
+      int cnt = 0;
+      for (int q = 0; q < kfix; q++) cnt += __shfl_sync(FULL_MASK, fid, q) <= bid;
+      if (j < m) {
+        const long long o = out0 + j + cnt;
+        keys[o] = (unsigned long long)u * (unsigned long long)n + (unsigned long long)bid;
+        vals[o] = (int)(nnz + e);
+      }
+    }
+  }
+}
+
 __global__ void union_flags(long long m, long long nnz, const unsigned long long* __restrict__ keys,
                             const int* __restrict__ vals, const double* __restrict__ w,
                             int* __restrict__ flag, double* __restrict__ hval) {
@@ -133,11 +211,13 @@ struct SymWs {
 size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t cub_bytes_for(long long m) {
-  size_t bytes = 0;
+  size_t bytes = 0, b2 = 0;
   cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
   cub::DoubleBuffer<int> vb(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, (int)m, 0, 64);
-  return bytes;
+  cub::DoubleBuffer<int> ikb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, b2, ikb, vb, (int)m, 0, 32);
+  return bytes > b2 ? bytes : b2;
 }
 
 size_t sym_layout(long long n, long long nnz, char* base, SymWs* ws) {
@@ -219,21 +299,51 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
       // confirm every row has kfix entries (one pass, flag in the scan workspace)
       kfix = rows_fixed(indptr, n, kfix, ws.partial, st) ? kfix : 0;
     }
-    build_keys<<<grid_for(nnz), 256, 0, st>>>(n, n, (const long long*)indptr, dst, nnz, kfix,
-                                              ws.k0, ws.v0);
-    GU_CHECK_LAUNCH("build_keys");
-    int end_bit = 1;
-    while (end_bit < 64 && ((unsigned long long)n * (unsigned long long)n) > (1ull << end_bit))
-      end_bit++;
-    cub::DoubleBuffer<unsigned long long> kb(ws.k0, ws.k1);
-    cub::DoubleBuffer<int> vb(ws.v0, ws.v1);
-    size_t cb = ws.cub_bytes;
-    GU_CHECK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, cb, kb, vb, (int)m, 0, end_bit, st));
-    union_flags<<<grid_for(m), 256, 0, st>>>(m, nnz, kb.Current(), vb.Current(), w, ws.flag, ws.h);
+    const unsigned long long* sorted_keys;
+    const int* sorted_vals;
+    if (kfix > 0 && kfix <= 32) {
+      // fast path: backward entries sorted by destination only (32-bit keys,
+      // value = entry index), then one warp merges each vertex's rows
+      int* ikey0 = reinterpret_cast<int*>(ws.k1);
+      int* ikey1 = ikey0 + nnz;
+      int* ival0 = ws.v1;
+      int* ival1 = ws.v1 + nnz;
+      int* indeg = ws.rowcnt;  // zeroed above; reset before union_write
+      fx_indeg<<<grid_for(nnz), 256, 0, st>>>(nnz, dst, indeg, ikey0, ival0);
+      GU_CHECK_LAUNCH("fx_indeg");
+      int vb_bits = 1;
+      while (vb_bits < 31 && (1ll << vb_bits) < n) vb_bits++;
+      cub::DoubleBuffer<int> kb(ikey0, ikey1);
+      cub::DoubleBuffer<int> vbuf(ival0, ival1);
+      size_t cb = ws.cub_bytes;
+      GU_CHECK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, cb, kb, vbuf, (int)nnz, 0, vb_bits, st));
+      int r0 = scan_counts(indeg, n, ws.pos, ws.partial, st);  // in_ptr in ws.pos[0..n]
+      if (r0) return r0;
+      fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, nnz, dst, ws.pos, vbuf.Current(), ws.k0,
+                                                  ws.v0);
+      GU_CHECK_LAUNCH("fx_merge");
+      GU_CHECK(cudaMemsetAsync(ws.rowcnt, 0, sizeof(int) * (size_t)(n + 1), st));
+      sorted_keys = ws.k0;
+      sorted_vals = ws.v0;
+    } else {
+      build_keys<<<grid_for(nnz), 256, 0, st>>>(n, n, (const long long*)indptr, dst, nnz, kfix,
+                                                ws.k0, ws.v0);
+      GU_CHECK_LAUNCH("build_keys");
+      int end_bit = 1;
+      while (end_bit < 64 && ((unsigned long long)n * (unsigned long long)n) > (1ull << end_bit))
+        end_bit++;
+      cub::DoubleBuffer<unsigned long long> kb(ws.k0, ws.k1);
+      cub::DoubleBuffer<int> vb(ws.v0, ws.v1);
+      size_t cb = ws.cub_bytes;
+      GU_CHECK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, cb, kb, vb, (int)m, 0, end_bit, st));
+      sorted_keys = kb.Current();
+      sorted_vals = vb.Current();
+    }
+    union_flags<<<grid_for(m), 256, 0, st>>>(m, nnz, sorted_keys, sorted_vals, w, ws.flag, ws.h);
     GU_CHECK_LAUNCH("union_flags");
     int r = scan_counts(ws.flag, m, ws.pos, ws.partial, st);
     if (r) return r;
-    union_write<<<grid_for(m), 256, 0, st>>>(m, n, kb.Current(), ws.flag, ws.h, ws.pos, sym_src,
+    union_write<<<grid_for(m), 256, 0, st>>>(m, n, sorted_keys, ws.flag, ws.h, ws.pos, sym_src,
                                             sym_dst, sym_w, ws.rowcnt);
     GU_CHECK_LAUNCH("union_write");
   } else {
