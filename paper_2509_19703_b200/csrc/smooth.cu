@@ -21,17 +21,33 @@
 namespace gu {
 namespace {
 
+// x(i) = exp(-(d_i - rho) / sigma), or 0 past the row.  Rows come sorted by
+// (distance, id), so a run of equal distances reuses the last value: the same
+// float64 expression on the same operands, i.e. bit-identical, with one exp
+// per distinct distance (2-3 per row on hop distances) instead of k.
 struct RowView {
   const int* d;
   int c;
   double rho;
   double sigma;
-  __device__ __forceinline__ double x(int i) const {
-    return i < c ? exp(-((double)d[i] - rho) / sigma) : 0.0;
+  int last_d;
+  double last_v;
+  __device__ __forceinline__ void set_sigma(double s) {
+    sigma = s;
+    last_d = -1;  // hop distances are >= 0
+  }
+  __device__ __forceinline__ double x(int i) {
+    if (i >= c) return 0.0;
+    const int di = d[i];
+    if (di != last_d) {
+      last_d = di;
+      last_v = exp(-((double)di - rho) / sigma);
+    }
+    return last_v;
   }
 };
 
-__device__ double pairwise(const RowView& r, int start, int len) {
+__device__ double pairwise(RowView& r, int start, int len) {
   if (len < 8) {
     double res = 0.;
     for (int i = 0; i < len; i++) res += r.x(start + i);
@@ -80,9 +96,9 @@ __global__ void __launch_bounds__(128)
     r.rho = rho;
     double sigma = SMAX;
     if (!all_equal) {
-      r.sigma = SMAX;
+      r.set_sigma(SMAX);
       const double s_hi = pairwise(r, 0, kmax);
-      r.sigma = SMIN;
+      r.set_sigma(SMIN);
       const double s_lo = pairwise(r, 0, kmax);
       const bool clamp_hi = s_hi < target, clamp_lo = s_lo > target;
       if (clamp_hi) sigma = SMAX;
@@ -91,7 +107,7 @@ __global__ void __launch_bounds__(128)
         double los = SMIN, his = SMAX, mid = (los + his) / 2.0;
         bool live = true;
         for (int it = 0; it < 64; it++) {
-          r.sigma = mid;
+          r.set_sigma(mid);
           const double s = pairwise(r, 0, kmax);
           if (fabs(s - target) < TOL) {
             sigma = mid;
