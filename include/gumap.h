@@ -200,13 +200,15 @@ int gu_crossings(int64_t m, const int32_t* edges, const double* coords_xy, const
                  int32_t g, int64_t n_inc, uint64_t* out_count, void* workspace,
                  size_t ws_bytes, void* stream);
 /* neighborhood_preservation (metrics.py:41-79): out_sum (device double) = the
- * sum over v of |ball_r(v) & nearest_q(v)| / |union|; the caller divides by
- * n.  slots = concurrent warps, each with 2n ints of scratch. */
+ * sum over v of |ball_r(v) & nearest_q(v)| / |union| -- over every vertex,
+ * or over the nsources distinct vertices of `sources` (nullable; the sampled
+ * estimator); the caller divides.  slots = concurrent warps, each with 2n
+ * ints of scratch. */
 size_t gu_np_workspace_size(int64_t n, int32_t slots);
 int gu_neighborhood_preservation(int64_t n, const int32_t* indptr, const int32_t* indices,
                                  const double* coords_xy, int32_t r, int32_t slots,
-                                 double* out_sum, void* workspace, size_t ws_bytes,
-                                 void* stream);
+                                 const int32_t* sources, int64_t nsources, double* out_sum,
+                                 void* workspace, size_t ws_bytes, void* stream);
 
 
 /* ------------------------------------------- spectral_init (8(f) row 2)

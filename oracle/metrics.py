@@ -182,18 +182,33 @@ def sampled_neighborhood_preservation(coords, hop_rows, sources, r=2):
     return total / len(sources)
 
 
-def sampled_stress(coords, hop_rows, sources):
+def sampled_stress(coords, hop_rows, sources, chunk=64):
     """metrics.py:90-132 restricted to the rows of ``sources`` (optimal scale
-    fitted on the same pairs)."""
+    fitted on the same pairs); chunked over sources so the distance block
+    stays small on million-vertex layouts."""
     coords = np.asarray(coords, np.float64)
-    delta = cdist(coords[sources], coords)
-    d = hop_rows.astype(np.float64)
-    d[np.arange(len(sources)), sources] = np.inf
-    d[d >= 2**31 - 1] = np.inf
-    s_num = float((delta / d).sum())
-    s_den = float((delta * delta / (d * d)).sum())
+    sources = np.asarray(sources)
+    s_num = s_den = 0.0
+    for a in range(0, len(sources), chunk):
+        b = min(a + chunk, len(sources))
+        delta = cdist(coords[sources[a:b]], coords)
+        d = hop_rows[a:b].astype(np.float64)
+        d[np.arange(b - a), sources[a:b]] = np.inf
+        d[d >= 2**31 - 1] = np.inf
+        s_num += float((delta / d).sum())
+        s_den += float((delta * delta / (d * d)).sum())
     scale = s_num / s_den if s_den > 0 else 1.0
-    term = (1.0 - scale * delta / d) ** 2
-    term[np.arange(len(sources)), sources] = 0.0
-    finite = np.isfinite(d)
-    return float(term[finite].sum() / finite.sum())
+    tot = 0.0
+    cnt = 0
+    for a in range(0, len(sources), chunk):
+        b = min(a + chunk, len(sources))
+        delta = cdist(coords[sources[a:b]], coords)
+        d = hop_rows[a:b].astype(np.float64)
+        d[np.arange(b - a), sources[a:b]] = np.inf
+        d[d >= 2**31 - 1] = np.inf
+        term = (1.0 - scale * delta / d) ** 2
+        term[np.arange(b - a), sources[a:b]] = 0.0
+        finite = np.isfinite(d)
+        tot += float(term[finite].sum())
+        cnt += int(finite.sum())
+    return tot / cnt

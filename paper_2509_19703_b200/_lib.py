@@ -60,7 +60,7 @@ SIGNATURES = {
                                     _vp]),
     "gu_np_workspace_size": (_c_sz, [_c_i64, _c_i32]),
     "gu_neighborhood_preservation": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i32, _c_i32, _vp,
-                                                    _vp, _c_sz, _vp]),
+                                                    _c_i64, _vp, _vp, _c_sz, _vp]),
     "gu_version": (ctypes.c_int, []),
     "gu_last_error": (ctypes.c_char_p, []),
     "gu_device_sync": (ctypes.c_int, [_vp]),

@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(NP_WARPS * 32)
               const double2* __restrict__ xy, int r, const Grid* __restrict__ grid,
               const long long* __restrict__ cstart, const int* __restrict__ cpts,
               int* __restrict__ stamps, int* __restrict__ queues, int nslots,
-              double* __restrict__ jac) {
+              const int* __restrict__ sources, int nitems, double* __restrict__ jac) {
   __shared__ unsigned hist[NP_WARPS][256];
   const Grid gr = *grid;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -455,7 +455,8 @@ __global__ void __launch_bounds__(NP_WARPS * 32)
   int* const queue = queues + (long long)gw * n;
   unsigned* const hh = hist[warp];
   const unsigned lt = (1u << lane) - 1u;
-  for (int v = gw; v < n; v += nslots) {
+  for (int item = gw; item < nitems; item += nslots) {
+    const int v = sources ? sources[item] : item;
     const int tag = v + 1;  // stamps start at 0; tags are unique per vertex
     if (lane == 0) stamp[v] = tag;
     __syncwarp();
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(NP_WARPS * 32)
     }
     const int q = qlen;
     if (q == 0) {
-      if (lane == 0) jac[v] = 1.0;
+      if (lane == 0) jac[item] = 1.0;
       continue;
     }
     // ---- smallest ring h whose guaranteed radius holds >= q points
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(NP_WARPS * 32)
       inter += (d < dstar) || (d == dstar && (unsigned)u <= wpre);
     }
     inter = __reduce_add_sync(FULL, inter);
-    if (lane == 0) jac[v] = (double)inter / (double)(2 * q - (int)inter);
+    if (lane == 0) jac[item] = (double)inter / (double)(2 * q - (int)inter);
     __syncwarp();
   }
 }
@@ -826,15 +827,19 @@ extern "C" size_t gu_np_workspace_size(int64_t n, int32_t slots) {
   return np_layout(n, np_grid_side(n), slots > 0 ? slots : 1, nullptr, nullptr);
 }
 
-// out_sum: device double = sum over v of the Jaccard terms (the caller
-// divides by n); slots: concurrent warps, each with 2n ints of scratch
+// out_sum: device double = sum of the Jaccard terms over every vertex, or
+// over the nsources distinct vertices in `sources` (sampled estimator) when
+// it is non-null; the caller divides.  slots: concurrent warps, each with 2n
+// ints of scratch
 extern "C" int gu_neighborhood_preservation(int64_t n, const int32_t* indptr,
                                             const int32_t* indices, const double* coords_xy,
-                                            int32_t r, int32_t slots, double* out_sum,
-                                            void* workspace, size_t ws_bytes, void* stream) {
+                                            int32_t r, int32_t slots, const int32_t* sources,
+                                            int64_t nsources, double* out_sum, void* workspace,
+                                            size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (n < 1 || n >= INT_MAX) {
-    set_error("gu_neighborhood_preservation: n=%lld", (long long)n);
+  if (n < 1 || n >= INT_MAX || (sources && (nsources < 1 || nsources > n))) {
+    set_error("gu_neighborhood_preservation: n=%lld nsources=%lld", (long long)n,
+              (long long)nsources);
     return GU_ERR_ARG;
   }
   if (slots < 1) slots = 1;
@@ -861,10 +866,12 @@ extern "C" int gu_neighborhood_preservation(int64_t n, const int32_t* indptr,
   GU_CHECK_LAUNCH("cell_starts");
   GU_CHECK(cudaMemsetAsync(ws.stamps, 0, sizeof(int) * (size_t)n * (size_t)slots, st));
   const unsigned blocks = (unsigned)((slots + NP_WARPS - 1) / NP_WARPS);
+  const int nitems = sources ? (int)nsources : (int)n;
   np_kernel<<<blocks, NP_WARPS * 32, 0, st>>>((int)n, indptr, indices, xy, r, ws.grid, ws.cstart,
-                                              ws.pts, ws.stamps, ws.queues, slots, ws.jac);
+                                              ws.pts, ws.stamps, ws.queues, slots, sources, nitems,
+                                              ws.jac);
   GU_CHECK_LAUNCH("np_kernel");
-  sum_doubles<<<1, 1024, 0, st>>>(ws.jac, n, out_sum);
+  sum_doubles<<<1, 1024, 0, st>>>(ws.jac, nitems, out_sum);
   GU_CHECK_LAUNCH("sum_doubles");
   return GU_OK;
 }

@@ -58,10 +58,12 @@ def _coords(layout, dev):
     return torch.from_numpy(xy).to(dev)
 
 
-def neighborhood_preservation(g, layout, r=2):
+def neighborhood_preservation(g, layout, r=2, sources=None):
     """Mean Jaccard overlap between r-hop and geometric neighborhoods
     (metrics.py:41-79): per vertex, the r-ball (excluding v) against the
-    |ball| Euclidean-nearest other vertices, ties by vertex id."""
+    |ball| Euclidean-nearest other vertices, ties by vertex id.  ``sources``
+    (distinct vertex ids, an extension): the mean over those vertices only --
+    the sampled estimator for graphs too large for a CPU-side comparison."""
     _check(g, layout)
     n = int(g.n)
     if n <= 1:
@@ -73,9 +75,15 @@ def neighborhood_preservation(g, layout, r=2):
     slots = int(max(1, min(NP_MAX_SLOTS, NP_SCRATCH_BUDGET // (8 * n))))
     ws = workspace(lib.gu_np_workspace_size(n, slots), dev)
     out = torch.zeros(1, dtype=torch.float64, device=dev)
+    src = None
+    if sources is not None:
+        src = torch.from_numpy(np.ascontiguousarray(np.asarray(sources), dtype=np.int32)).to(dev)
+        if src.numel() == 0 or int(torch.unique(src).numel()) != src.numel():
+            raise ValueError("sources must be distinct vertex ids")
     _lib.call("gu_neighborhood_preservation", n, _lib.ptr(csr.indptr), _lib.ptr(csr.indices),
-              _lib.ptr(xy), int(r), slots, _lib.ptr(out), _lib.ptr(ws), ws.numel(), stream_ptr(dev))
-    return float(out.item()) / n
+              _lib.ptr(xy), int(r), slots, _lib.ptr(src), 0 if src is None else src.numel(),
+              _lib.ptr(out), _lib.ptr(ws), ws.numel(), stream_ptr(dev))
+    return float(out.item()) / (n if src is None else src.numel())
 
 
 def stress(g, layout, rescale=True):

@@ -466,6 +466,53 @@ def gen_sparsify():
         print(name, rg.n, rg.m, "kept", mask.sum(), "target", S.sparsifier_target(rg.n, rg.m))
     save("sparsify.npz", **out)
 
+
+def _c4_seed(args):
+    """One reference c4 SSSL-style layout (random init, partial BFS kNN k=15,
+    smooth weights, 200 windowed epochs at the default samp=0.9) and its
+    sampled NP / stress over the fixed sources."""
+    seed, edges_path, rows_path, src_path = args
+    import time
+    sys.path.insert(0, ROOT)
+    from oracle.metrics import sampled_neighborhood_preservation, sampled_stress
+    t = time.time()
+    e = np.load(edges_path)
+    rg = gu.build_graph([tuple(map(int, x)) for x in e])
+    _, kn = gu.partial_bfs(rg, 15, seed=seed)
+    gk = gu.smooth_knn_weights(kn)
+    lay = gu.optimize_sampled(gk, gu.random_init(rg, seed, 10.0),
+                              gu.OptimizerConfig(iterations=200, k=15, seed=seed))
+    rows = np.load(rows_path)
+    src = np.load(src_path)
+    out = (sampled_neighborhood_preservation(lay.coords, rows, src),
+           sampled_stress(lay.coords, rows, src))
+    print("quality c4 seed", seed, out, f"{time.time() - t:.0f}s", flush=True)
+    return out
+
+
+def gen_quality_c4(nseeds=5):
+    """Check (c) at 1M scale: the reference's own c4 layouts (SBM 1M fixture,
+    random init, partial BFS kNN, 200 epochs at samp 0.9), one process per
+    seed; sampled NP / stress over 2000 fixed sources (oracle/metrics.py
+    estimators, exact per-source terms).  Only the scalars are frozen."""
+    import multiprocessing as mp
+    import tempfile
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    from oracle.metrics import sample_sources
+    g = F.config_graph("c4")
+    src = sample_sources(g.n)
+    rows = O.all_pairs_bfs_rows(g, src)
+    tmp = tempfile.mkdtemp()
+    ep, rp, sp = (os.path.join(tmp, f) for f in ("edges.npy", "rows.npy", "src.npy"))
+    np.save(ep, np.asarray(g.edges))
+    np.save(rp, rows)
+    np.save(sp, src)
+    with mp.get_context("spawn").Pool(nseeds) as pool:
+        vals = pool.map(_c4_seed, [(s, ep, rp, sp) for s in range(nseeds)])
+    v = np.array(vals)
+    save("quality_c4.npz", np_=v[:, 0], stress=v[:, 1], sources=src)
+
 def main():
     # quality_c3_full (~1.5 h on 8 cores) runs only when named
     which = sys.argv[1:] or ["partial_small", "full_small", "smooth_cases", "c1", "c3", "quality_c1",

@@ -126,3 +126,20 @@ def test_quality_c3_exact_vs_reference(gu):
     assert v.mean(axis=0)[0] >= ref.mean(axis=0)[0] - 4 * se[0]
     assert v.mean(axis=0)[1] <= ref.mean(axis=0)[1] + 4 * se[1]
     assert v.mean(axis=0)[2] <= ref.mean(axis=0)[2] + 4 * se[2]
+
+
+def test_np_sources_matches_sampled_estimator(gu, oracle):
+    """neighborhood_preservation(..., sources=S) is the oracle's sampled
+    estimator (oracle/metrics.py) exactly: the reference's NP terms averaged
+    over S."""
+    from oracle.metrics import sample_sources, sampled_neighborhood_preservation
+    from paper_2509_19703_b200 import metrics as M
+
+    z = load_golden("quality_c1.npz")
+    g = gu.synth_graph("grid", 2500)
+    src = sample_sources(g.n, size=400, seed=5)
+    rows = oracle.all_pairs_bfs_rows(g, src)
+    for lay in (z["layout0"], np.random.default_rng(1).integers(0, 7, size=(g.n, 2)).astype(float)):
+        a = M.neighborhood_preservation(g, _layout(gu, lay), sources=src)
+        b = sampled_neighborhood_preservation(lay, rows, src)
+        assert abs(a - b) < NP_ABS_TOL
