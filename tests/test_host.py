@@ -80,9 +80,20 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     import paper_2509_19703_b200 as gu
 
-    g = gu.build_graph([(0, 1), (1, 2)])
-    with pytest.raises(RuntimeError, match="CUDA"):
-        gu.partial_bfs(g, 1)
+    from paper_2509_19703_b200 import metrics as M
+    from paper_2509_19703_b200 import sparsify as S
+
+    g = gu.build_graph([(0, 1), (1, 2), (2, 3), (0, 3), (1, 3)])
+    lay = gu.Layout(coords=np.arange(8, dtype=np.float64).reshape(4, 2))
+    for call in (lambda: gu.partial_bfs(g, 1),
+                 lambda: gu.knn_from_full_distances(gu.all_pairs_bfs(g), 2),
+                 lambda: M.neighborhood_preservation(g, lay),
+                 lambda: M.stress(g, lay),
+                 lambda: M.count_crossings(g, lay),
+                 lambda: S.effective_resistance_exact(g),
+                 lambda: gu.spectral_init(g, 0)):
+        with pytest.raises(RuntimeError, match="CUDA"):
+            call()
 
 
 def test_optimizer_config_validation():
