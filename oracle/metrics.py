@@ -192,7 +192,7 @@ def sampled_stress(coords, hop_rows, sources, chunk=64):
     for a in range(0, len(sources), chunk):
         b = min(a + chunk, len(sources))
         delta = cdist(coords[sources[a:b]], coords)
-        d = hop_rows[a:b].astype(np.float64)
+        d = np.asarray(hop_rows[a:b]).astype(np.float64)
         d[np.arange(b - a), sources[a:b]] = np.inf
         d[d >= 2**31 - 1] = np.inf
         s_num += float((delta / d).sum())
@@ -203,7 +203,7 @@ def sampled_stress(coords, hop_rows, sources, chunk=64):
     for a in range(0, len(sources), chunk):
         b = min(a + chunk, len(sources))
         delta = cdist(coords[sources[a:b]], coords)
-        d = hop_rows[a:b].astype(np.float64)
+        d = np.asarray(hop_rows[a:b]).astype(np.float64)
         d[np.arange(b - a), sources[a:b]] = np.inf
         d[d >= 2**31 - 1] = np.inf
         term = (1.0 - scale * delta / d) ** 2

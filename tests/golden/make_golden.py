@@ -482,7 +482,7 @@ def _c4_seed(args):
     gk = gu.smooth_knn_weights(kn)
     lay = gu.optimize_sampled(gk, gu.random_init(rg, seed, 10.0),
                               gu.OptimizerConfig(iterations=200, k=15, seed=seed))
-    rows = np.load(rows_path)
+    rows = np.load(rows_path, mmap_mode="r")  # 8 GB at c4: one page-cache copy for all workers
     src = np.load(src_path)
     out = (sampled_neighborhood_preservation(lay.coords, rows, src),
            sampled_stress(lay.coords, rows, src))
@@ -508,6 +508,7 @@ def gen_quality_c4(nseeds=5):
     np.save(ep, np.asarray(g.edges))
     np.save(rp, rows)
     np.save(sp, src)
+    del rows, g
     with mp.get_context("spawn").Pool(nseeds) as pool:
         vals = pool.map(_c4_seed, [(s, ep, rp, sp) for s in range(nseeds)])
     v = np.array(vals)
