@@ -179,11 +179,13 @@ int gu_sgd_replay_f64(int64_t n, double* coords, const int32_t* e_src, const int
  * Restate metrics.py:41-190 on the GPU.  coords_xy: float64 (n, 2) row-major.
  * gu_stress: both passes of metrics.py:106-131 fused into the 64-source bitset
  * BFS (no hop rows in memory); out3 (device, 3 doubles) = (sum of the stress
- * terms, scale, unreachable flag); stress = out3[0] / (n*n - n). */
+ * terms, scale, unreachable flag); stress = out3[0] / (n*n - n).  sources
+ * (nullable, nsources distinct ids): only those rows -- the sampled estimator
+ * (scale fitted on the same pairs), stress = out3[0] / (nsources * (n - 1)). */
 size_t gu_stress_workspace_size(int64_t n);
 int gu_stress(int64_t n, const int32_t* indptr, const int32_t* indices,
-              const double* coords_xy, int32_t rescale, double* out3, void* workspace,
-              size_t ws_bytes, void* stream);
+              const double* coords_xy, int32_t rescale, const int32_t* sources,
+              int64_t nsources, double* out3, void* workspace, size_t ws_bytes, void* stream);
 /* count_crossings (metrics.py:176-190, _kernels.py:244-296): exact count of
  * unordered edge pairs (edges int32 (m, 2)) whose open segments cross.
  * gu_crossings_grid writes a g x g square grid over the coordinates' bounding

@@ -51,7 +51,8 @@ SIGNATURES = {
     "gu_components_workspace_size": (_c_sz, [_c_i64]),
     "gu_connected_components": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _c_sz, _vp]),
     "gu_stress_workspace_size": (_c_sz, [_c_i64]),
-    "gu_stress": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i32, _vp, _vp, _c_sz, _vp]),
+    "gu_stress": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _c_i32, _vp, _c_i64, _vp, _vp, _c_sz,
+                                 _vp]),
     "gu_grid_bytes": (_c_sz, []),
     "gu_crossings_grid": (ctypes.c_int, [_c_i64, _vp, _c_i32, _vp, _vp]),
     "gu_crossings_incidences": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp]),

@@ -17,7 +17,8 @@ namespace gu {
 // full_bfs.cu: one fused stress pass over every source (metrics.cu)
 int stress_bfs_pass(int64_t n, const int32_t* indptr, const int32_t* indices, const double* xy,
                     int pass2, const double* scale, void* acc, int* flag, void* workspace,
-                    size_t ws_bytes, int ctas, cudaStream_t st);
+                    size_t ws_bytes, int ctas, const int32_t* sources, int64_t nsources,
+                    cudaStream_t st);
 size_t stress_bfs_workspace(int64_t n, int ctas);
 
 // --------------------------------------------------------------- errors

@@ -42,6 +42,7 @@ struct StressArgs {
   double2* acc;
   int* flag;
   int pass2;
+  const int* sources;  // nullable: BFS from sources[src_begin .. src_end) instead of the ids
 };
 
 struct FbShared {
@@ -135,7 +136,11 @@ __global__ void __launch_bounds__(FB_THREADS)
         for (int v = tid; v < n; v += FB_THREADS) row[v] = (v == (int)(s0 + b)) ? 0 : GU_INF32;
       }
     }
-    if (MODE == MODE_STRESS && tid < nb) sh.sxy[tid] = sa.xy[s0 + tid];
+    // source id of bit b: s0 + b, or the listed source in stress mode
+    auto src_of = [&](int b) -> int {
+      return (MODE == MODE_STRESS && sa.sources) ? sa.sources[s0 + b] : (int)(s0 + b);
+    };
+    if (MODE == MODE_STRESS && tid < nb) sh.sxy[tid] = sa.xy[src_of(tid)];
     if (tid < 64) {
       sh.cnt[tid] = 0;
       sh.cum[tid] = 0;
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(FB_THREADS)
     __syncthreads();
     // ---- level 0 / level 1 (push from the sources' sorted adjacency)
     for (int b = warp; b < nb; b += FB_WARPS) {
-      const int s = (int)(s0 + b);
+      const int s = src_of(b);
       const int beg = __ldg(indptr + s), end = __ldg(indptr + s + 1);
       if (lane == 0) {
         atomicOr(&vis[s], 1ull << b);
@@ -505,8 +510,10 @@ int levels_for(int k, bool knn) { return knn ? k + 2 : 2; }
 // one stress pass over every source (metrics.cu); acc: >= ctas double2
 int stress_bfs_pass(int64_t n, const int32_t* indptr, const int32_t* indices, const double* xy,
                     int pass2, const double* scale, void* acc, int* flag, void* workspace,
-                    size_t ws_bytes, int ctas, cudaStream_t st) {
-  const long long nbatches = (n + 63) / 64;
+                    size_t ws_bytes, int ctas, const int32_t* sources, int64_t nsources,
+                    cudaStream_t st) {
+  const long long nsrc = sources ? nsources : n;
+  const long long nbatches = (nsrc + 63) / 64;
   if (ctas > nbatches) ctas = (int)nbatches;
   if (ctas < 1) ctas = 1;
   const size_t slot = slot_bytes_for(n, levels_for(0, false), false);
@@ -514,10 +521,10 @@ int stress_bfs_pass(int64_t n, const int32_t* indptr, const int32_t* indices, co
     set_error("stress BFS: workspace %zu < %zu", ws_bytes, slot * (size_t)ctas);
     return GU_ERR_WORKSPACE;
   }
-  StressArgs sa{(const double2*)xy, scale, (double2*)acc, flag, pass2};
+  StressArgs sa{(const double2*)xy, scale, (double2*)acc, flag, pass2, sources};
   msbfs_kernel<MODE_STRESS><<<(unsigned)ctas, FB_THREADS, 0, st>>>(
-      (int)n, indptr, indices, 0, 0, 0, n, nullptr, nullptr, nullptr, nullptr, (char*)workspace,
-      slot, levels_for(0, false), nullptr, sa);
+      (int)n, indptr, indices, 0, 0, 0, nsrc, nullptr, nullptr, nullptr, nullptr,
+      (char*)workspace, slot, levels_for(0, false), nullptr, sa);
   GU_CHECK_LAUNCH("msbfs_kernel<stress>");
   return GU_OK;
 }

@@ -704,11 +704,13 @@ using namespace gu;
 extern "C" size_t gu_stress_workspace_size(int64_t n) { return stress_layout(n, nullptr, nullptr); }
 
 extern "C" int gu_stress(int64_t n, const int32_t* indptr, const int32_t* indices,
-                         const double* coords_xy, int32_t rescale, double* out3, void* workspace,
-                         size_t ws_bytes, void* stream) {
+                         const double* coords_xy, int32_t rescale, const int32_t* sources,
+                         int64_t nsources, double* out3, void* workspace, size_t ws_bytes,
+                         void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (n < 2 || n >= INT_MAX) {
-    set_error("gu_stress: n=%lld out of range (n < 2 is answered by the caller)", (long long)n);
+  if (n < 2 || n >= INT_MAX || (sources && (nsources < 1 || nsources > n))) {
+    set_error("gu_stress: n=%lld nsources=%lld out of range (n < 2 is answered by the caller)",
+              (long long)n, (long long)nsources);
     return GU_ERR_ARG;
   }
   StressWs ws;
@@ -726,7 +728,7 @@ extern "C" int gu_stress(int64_t n, const int32_t* indptr, const int32_t* indice
   }
   for (int pass = rescale ? 0 : 1; pass < 2; pass++) {
     const int rc = stress_bfs_pass(n, indptr, indices, coords_xy, pass, ws.scale, ws.acc, ws.flag,
-                                   ws.bfs, ws.bfs_bytes, ST_CTAS, st);
+                                   ws.bfs, ws.bfs_bytes, ST_CTAS, sources, nsources, st);
     if (rc != GU_OK) return rc;
     reduce_acc<<<1, ST_THREADS, 0, st>>>(ws.acc, ST_CTAS, ws.sums + pass);
     GU_CHECK_LAUNCH("reduce_acc");

@@ -58,6 +58,15 @@ def _coords(layout, dev):
     return torch.from_numpy(xy).to(dev)
 
 
+def _sources(sources, dev):
+    if sources is None:
+        return None
+    src = torch.from_numpy(np.ascontiguousarray(np.asarray(sources), dtype=np.int32)).to(dev)
+    if src.numel() == 0 or int(torch.unique(src).numel()) != src.numel():
+        raise ValueError("sources must be distinct vertex ids")
+    return src
+
+
 def neighborhood_preservation(g, layout, r=2, sources=None):
     """Mean Jaccard overlap between r-hop and geometric neighborhoods
     (metrics.py:41-79): per vertex, the r-ball (excluding v) against the
@@ -75,21 +84,19 @@ def neighborhood_preservation(g, layout, r=2, sources=None):
     slots = int(max(1, min(NP_MAX_SLOTS, NP_SCRATCH_BUDGET // (8 * n))))
     ws = workspace(lib.gu_np_workspace_size(n, slots), dev)
     out = torch.zeros(1, dtype=torch.float64, device=dev)
-    src = None
-    if sources is not None:
-        src = torch.from_numpy(np.ascontiguousarray(np.asarray(sources), dtype=np.int32)).to(dev)
-        if src.numel() == 0 or int(torch.unique(src).numel()) != src.numel():
-            raise ValueError("sources must be distinct vertex ids")
+    src = _sources(sources, dev)
     _lib.call("gu_neighborhood_preservation", n, _lib.ptr(csr.indptr), _lib.ptr(csr.indices),
               _lib.ptr(xy), int(r), slots, _lib.ptr(src), 0 if src is None else src.numel(),
               _lib.ptr(out), _lib.ptr(ws), ws.numel(), stream_ptr(dev))
     return float(out.item()) / (n if src is None else src.numel())
 
 
-def stress(g, layout, rescale=True):
+def stress(g, layout, rescale=True, sources=None):
     """Mean squared relative deviation of layout distances from hop
     distances over all ordered pairs i != j (metrics.py:90-132), after the
-    closed-form optimal scale unless ``rescale=False``."""
+    closed-form optimal scale unless ``rescale=False``.  ``sources``
+    (distinct vertex ids, an extension): only the pairs (s, j), s in sources
+    -- the sampled estimator, scale fitted on the same pairs."""
     _check(g, layout)
     n = int(g.n)
     if n < 2:
@@ -100,12 +107,14 @@ def stress(g, layout, rescale=True):
     lib = _lib.load()
     ws = workspace(lib.gu_stress_workspace_size(n), dev)
     out = torch.zeros(3, dtype=torch.float64, device=dev)
+    src = _sources(sources, dev)
     _lib.call("gu_stress", n, _lib.ptr(csr.indptr), _lib.ptr(csr.indices), _lib.ptr(xy),
-              1 if rescale else 0, _lib.ptr(out), _lib.ptr(ws), ws.numel(), stream_ptr(dev))
+              1 if rescale else 0, _lib.ptr(src), 0 if src is None else src.numel(),
+              _lib.ptr(out), _lib.ptr(ws), ws.numel(), stream_ptr(dev))
     total, _scale, unreachable = out.tolist()
     if unreachable:
         raise MetricError("stress requires a connected graph")
-    return total / (n * n - n)
+    return total / ((n * n - n) if src is None else src.numel() * (n - 1))
 
 
 def _grid_side(m):

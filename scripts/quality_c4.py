@@ -1,7 +1,7 @@
 """Check (c) at 1M scale (BASELINE c4: SBM 1M fixture, random init, partial
-BFS kNN k=15, 200 epochs at the default samp=0.9): sampled NP (GPU metric
-over the fixed sources) and sampled stress (oracle estimator, same sources)
-of the GPU layouts vs the reference's own c4 layouts
+BFS kNN k=15, 200 epochs at the default samp=0.9): sampled NP and stress
+(GPU metrics over the fixed sources, the oracle's estimators) of the GPU
+layouts vs the reference's own c4 layouts
 (tests/golden/quality_c4.npz).  Mean ratios with bootstrap 95% CIs ->
 profiles/r01_quality_c4.json.
 
@@ -17,8 +17,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import paper_2509_19703_b200 as gu  # noqa: E402
-from oracle import oracle as O  # noqa: E402
-from oracle.metrics import sampled_stress  # noqa: E402
 from paper_2509_19703_b200 import metrics as M  # noqa: E402
 
 
@@ -27,8 +25,6 @@ def main(nseeds):
     ref = np.stack([z["np_"], z["stress"]], axis=1)
     src = z["sources"]
     g = gu.config_graph("c4")
-    O.build()
-    rows = O.all_pairs_bfs_rows(g, src)
     vals = []
     for seed in range(nseeds):
         _, knn = gu.partial_bfs(g, 15, seed=seed)
@@ -36,7 +32,7 @@ def main(nseeds):
         lay = gu.optimize_sampled(gk, gu.random_init(g, seed, 10.0),
                                   gu.OptimizerConfig(iterations=200, k=15, seed=seed))
         vals.append((M.neighborhood_preservation(g, lay, sources=src),
-                     sampled_stress(lay.coords, rows, src)))
+                     M.stress(g, lay, sources=src)))
         print("gpu c4 seed", seed, vals[-1], flush=True)
     v = np.array(vals)
     rng = np.random.default_rng(0)
@@ -50,6 +46,8 @@ def main(nseeds):
                               "ratio": float(v[:, i].mean() / ref[:, i].mean()),
                               "ratio_ci95": [float(np.percentile(boot[:, i], 2.5)),
                                              float(np.percentile(boot[:, i], 97.5))]}
+    with open(os.path.join(ROOT, "profiles", "r01_quality_c4.json"), "w") as f:
+        json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1))
 
 

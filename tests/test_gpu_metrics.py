@@ -129,9 +129,9 @@ def test_quality_c3_exact_vs_reference(gu):
 
 
 def test_np_sources_matches_sampled_estimator(gu, oracle):
-    """neighborhood_preservation(..., sources=S) is the oracle's sampled
-    estimator (oracle/metrics.py) exactly: the reference's NP terms averaged
-    over S."""
+    """neighborhood_preservation / stress (..., sources=S) are the oracle's
+    sampled estimators (oracle/metrics.py): the reference's terms over the
+    rows of S (stress: scale fitted on the same pairs)."""
     from oracle.metrics import sample_sources, sampled_neighborhood_preservation
     from paper_2509_19703_b200 import metrics as M
 
@@ -139,7 +139,42 @@ def test_np_sources_matches_sampled_estimator(gu, oracle):
     g = gu.synth_graph("grid", 2500)
     src = sample_sources(g.n, size=400, seed=5)
     rows = oracle.all_pairs_bfs_rows(g, src)
+    from oracle.metrics import sampled_stress
+
     for lay in (z["layout0"], np.random.default_rng(1).integers(0, 7, size=(g.n, 2)).astype(float)):
         a = M.neighborhood_preservation(g, _layout(gu, lay), sources=src)
         b = sampled_neighborhood_preservation(lay, rows, src)
         assert abs(a - b) < NP_ABS_TOL
+        a = M.stress(g, _layout(gu, lay), sources=src)
+        b = sampled_stress(lay, rows, src)
+        assert abs(a - b) <= STRESS_REL_TOL * abs(b)
+
+
+def test_quality_c4_sampled_vs_reference(gu):
+    """Check (c) at 1M scale (c4 SBM): sampled NP / stress over the 2000
+    fixed sources of the GPU layouts vs the reference's own c4 layouts
+    (tests/golden/quality_c4.npz, same estimators); 4 standard errors."""
+    import math
+    import os
+
+    from conftest import GOLDEN
+    from paper_2509_19703_b200 import metrics as M
+
+    if not os.path.exists(os.path.join(GOLDEN, "quality_c4.npz")):
+        pytest.skip("c4 reference fixture not generated")
+    z = load_golden("quality_c4.npz")
+    ref = np.stack([z["np_"], z["stress"]], axis=1)
+    src = z["sources"]
+    g = gu.config_graph("c4")
+    vals = []
+    for seed in range(2):
+        _, knn = gu.partial_bfs(g, 15, seed=seed)
+        gk = gu.smooth_knn_weights(knn)
+        lay = gu.optimize_sampled(gk, gu.random_init(g, seed, 10.0),
+                                  gu.OptimizerConfig(iterations=200, k=15, seed=seed))
+        vals.append((M.neighborhood_preservation(g, lay, sources=src), M.stress(g, lay, sources=src)))
+    v = np.array(vals)
+    print("check (c) c4 sampled mean ratios gpu/ref [np, stress]:", v.mean(axis=0) / ref.mean(axis=0))
+    se = ref.std(axis=0, ddof=1) / math.sqrt(ref.shape[0]) + v.std(axis=0, ddof=1) / math.sqrt(v.shape[0])
+    assert v.mean(axis=0)[0] >= ref.mean(axis=0)[0] - 4 * se[0]
+    assert v.mean(axis=0)[1] <= ref.mean(axis=0)[1] + 4 * se[1]
