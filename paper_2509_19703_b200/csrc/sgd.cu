@@ -24,6 +24,8 @@
 #include <climits>
 #include <cmath>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gumap.h"
 
@@ -148,12 +150,14 @@ __device__ __forceinline__ bool filt_maybe(uint4 f, int c) {
 
 constexpr int SGD_WARPS = 8;  // 256 threads per block at most (block_for)
 
+template <int LANES>
 __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
     sgd_epoch_kernel(int n, long long E, float2* __restrict__ xy, const int4* __restrict__ edges,
                      const int* __restrict__ nip, const int* __restrict__ nix,
                      const uint4* __restrict__ filt, float a, float b, float lr, int epoch,
                      int n_neg, long long items, long long start, int windowed,
                      unsigned long long seed, int* __restrict__ diverged) {
+  constexpr int lanes = LANES;
   // (candidate, row begin, row end, owner lane * 8 + slot) of the warp's
   // filter hits, and each lane's bitmask of slots found to be neighbours
   __shared__ int4 sh_pairs[SGD_WARPS][32 * SGD_NEG_BLOCK];
@@ -163,13 +167,16 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
   const unsigned long long rkey = mix64(seed ^ (0xA5A5A5A5ull * (unsigned long long)(epoch + 1)));
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   bool bad = false;
-  // warp-uniform loop (every lane reaches the collectives below); lanes past
-  // the end ride along inactive
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < items;
-       i0 += stride) {
+  // warp-uniform loop (every lane reaches the collectives below).  Each warp
+  // takes `lanes` visits per step (lanes < 32 when the concurrency cap is
+  // small: the same visits in flight spread over more warps, i.e. more
+  // independent instruction streams per scheduler); the other lanes and
+  // lanes past the end ride along inactive
+  const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long stride = (((long long)gridDim.x * blockDim.x) >> 5) * lanes;
+  for (long long i0 = gwarp * lanes; i0 < items; i0 += stride) {
     const long long i = i0 + lane;
-    bool act = i < items;
+    bool act = lane < lanes && i < items;
     long long p = 0;
     if (act) {
       if (windowed) {
@@ -420,11 +427,27 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
     const float lr = (float)((double)lr0 * (1.0 - (double)e / (double)t));
     long long items, start;
     epoch_range(E, e, window, windowed, &items, &start);
-    const unsigned bs = block_for(concurrency);
-    const unsigned gs = bs < 256 ? 1u : grid_for(items, concurrency);
-    sgd_epoch_kernel<<<gs, bs, 0, st>>>(
-        (int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr, nbr_indices,
-        (const uint4*)nbr_filter, a, b, lr, e, n_neg, items, start, windowed, seed, diverged);
+    // a cap below the resident-thread capacity (4 blocks of 256 per SM at 64
+    // registers) runs `lanes` < 32 visits per warp on cap * 32 / lanes
+    // threads: the same visits in flight, more warps to hide latency
+    const long long resident = 148LL * SGD_MIN_BLOCKS * 256;
+    // 16 lanes: measured best on c3 (8 slows full epochs); GU_SGD_MIN_LANES=32
+    // turns it off
+    static const int min_lanes = [] {
+      const char* v = getenv("GU_SGD_MIN_LANES");
+      return (v && atoi(v) >= 32) ? 32 : 16;
+    }();
+    int lanes = 32;
+    if (concurrency > 0 && concurrency < resident && min_lanes == 16 &&
+        (concurrency * 32) / 16 <= resident)
+      lanes = 16;
+    const long long threads = concurrency > 0 ? (concurrency * 32 + lanes - 1) / lanes : 0;
+    const unsigned bs = block_for(threads);
+    const unsigned gs = bs < 256 ? 1u : grid_for((items * 32 + lanes - 1) / lanes, threads);
+    auto kern = lanes == 32 ? sgd_epoch_kernel<32> : sgd_epoch_kernel<16>;
+    kern<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr,
+                            nbr_indices, (const uint4*)nbr_filter, a, b, lr, e, n_neg, items,
+                            start, windowed, seed, diverged);
     GU_CHECK_LAUNCH("sgd_epoch_kernel");
   }
   return GU_OK;
