@@ -279,8 +279,9 @@ def run_ours(args):
         "fixture_gen_s": round(gen_s, 2),
     }
 
+    e2e = _e2e_partial(gu, g, args, gteps_te=te_tot, ws=ws, rank=rank, dev=dev)
     if rank == 0:
-        result["e2e"] = _e2e_partial(gu, g, args, gteps_te=te_tot)
+        result["e2e"] = e2e
         if not args.skip_sgd:
             result["sgd"] = _sgd_bench(gu, g, args, dev, peak)
         if not args.skip_layout:
@@ -296,9 +297,14 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _e2e_partial(gu, g, args, gteps_te):
-    """Public API, host arrays in, numpy DirectedKnn out, copies timed."""
+def _e2e_partial(gu, g, args, gteps_te, ws=1, rank=0, dev=None):
+    """Public API end to end: pinned host Graph arrays in, numpy DirectedKnn
+    out, copies timed.  At N > 1 every rank runs the sharded public call
+    (distributed.sharded_knn: replicated upload, source shards, NCCL
+    all_gather) and rank 0 reads the result back; max over ranks."""
     import torch
+    import torch.distributed as dist
+    from paper_2509_19703_b200.distributed import sharded_knn
     from paper_2509_19703_b200.graph import Graph
 
     def pinned(a):  # the step's inputs live in pinned host memory (contract)
@@ -315,20 +321,31 @@ def _e2e_partial(gu, g, args, gteps_te):
     h2d = d2h = 0
     for i in range(max(1, args.warmup) + args.steps):
         gg = fresh()
+        if ws > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        _, knn = gu.partial_bfs(gg, K_NN, seed=SEED)
-        ip, dst, dd = knn.indptr, knn.dst, knn.dist
+        if ws > 1:
+            knn = sharded_knn(gg, K_NN, seed=SEED, mode="partial")
+        else:
+            _, knn = gu.partial_bfs(gg, K_NN, seed=SEED)
+        if rank == 0:
+            ip, dst, dd = knn.indptr, knn.dst, knn.dist
+            d2h = ip.nbytes + dst.nbytes + dd.nbytes
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i >= max(1, args.warmup):
             times.append(dt)
-        h2d = (g.n + 1) * 4 + g.adj_indices.shape[0] * 4
-        d2h = ip.nbytes + dst.nbytes + dd.nbytes
+        h2d = ws * (gg.adj_indptr.nbytes + gg.adj_indices.nbytes)
     t = sum(times) / len(times)
+    if ws > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    api = ("paper_2509_19703_b200.distributed.sharded_knn(Graph(pinned host arrays), 15, seed=4)"
+           if ws > 1 else "paper_2509_19703_b200.partial_bfs(Graph(pinned host arrays), 15, seed=4)")
     return {"value": round(gteps_te / t / 1e9, 4), "unit": "GTEPS", "seconds": round(t, 4),
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "api": "paper_2509_19703_b200.partial_bfs(Graph(pinned host arrays), 15, seed=4)"}
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "api": api}
 
 
 def _sgd_bench(gu, g, args, dev, peak):
