@@ -108,6 +108,67 @@ def to_host(t):
     return out.numpy()
 
 
+_COPY_POOL = None
+
+
+def _copy_pool():
+    global _COPY_POOL
+    if _COPY_POOL is None:
+        import concurrent.futures
+        import os
+        _COPY_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+    return _COPY_POOL
+
+
+def _par_copyto(dst, src):
+    """np.copyto split over host threads (numpy releases the GIL): the page
+    faults of a fresh destination and the memcpy both scale with threads."""
+    pool = _copy_pool()
+    parts = pool._max_workers
+    n = dst.shape[0]
+    if n < (1 << 20) or parts <= 1:
+        np.copyto(dst, src)
+        return
+    bounds = np.linspace(0, n, parts + 1).astype(np.int64)
+    futs = [pool.submit(np.copyto, dst[a:b], src[a:b]) for a, b in zip(bounds[:-1], bounds[1:])]
+    for f in futs:
+        f.result()
+
+
+def to_host_into(t, out, chunk_bytes=64 << 20):
+    """Device tensor -> an existing (pageable) numpy array of the same shape
+    and dtype: double-buffered pinned staging, the (multi-threaded) host copy
+    of one chunk overlapping the DMA of the next."""
+    flat = t.detach().reshape(-1)
+    dst = out.reshape(-1)
+    if flat.numel() * flat.element_size() < _PIN_THRESHOLD:
+        dst[...] = flat.cpu().numpy()
+        return out
+    step = max(1, chunk_bytes // flat.element_size())
+    bufs = [torch.empty(min(step, flat.numel()), dtype=flat.dtype, pin_memory=True)
+            for _ in range(2)]
+    evs = [None, None]
+    copy_stream = torch.cuda.Stream(device=flat.device)
+    copy_stream.wait_stream(torch.cuda.current_stream(flat.device))
+    pending = None
+    for i, lo in enumerate(range(0, flat.numel(), step)):
+        hi = min(lo + step, flat.numel())
+        b = i & 1
+        with torch.cuda.stream(copy_stream):
+            bufs[b][: hi - lo].copy_(flat[lo:hi], non_blocking=True)
+            evs[b] = torch.cuda.Event()
+            evs[b].record(copy_stream)
+        if pending is not None:  # host copy of the previous chunk overlaps this DMA
+            pb, plo, phi = pending
+            evs[pb].synchronize()
+            _par_copyto(dst[plo:phi], bufs[pb][: phi - plo].numpy())
+        pending = (b, lo, hi)
+    pb, plo, phi = pending
+    evs[pb].synchronize()
+    _par_copyto(dst[plo:phi], bufs[pb][: phi - plo].numpy())
+    return out
+
+
 def to_device(a, dtype, device):
     """numpy -> device tensor.  Large buffers are staged through a pinned
     buffer from torch's caching host allocator (multi-threaded host copy, then

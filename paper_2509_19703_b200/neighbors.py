@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import device_csr, require_cuda, stream_ptr, to_device, to_host, workspace
+from .device import to_host_into, device_csr, require_cuda, stream_ptr, to_device, to_host, workspace
 
 #: sentinel hop distance for unreachable pairs (neighbors.py:17-18)
 UNREACHABLE = 2**31 - 1
@@ -212,23 +212,31 @@ def fuzzy_union(a, b):
 
 
 # ------------------------------------------------------------------ C0 full
+# device row budget of one all_pairs_bfs call (the rows of up to 296 64-source
+# batches at once keep every CTA slot busy; the reference's `chunk` is a host
+# processing granularity and does not bound the GPU batch)
+_APSP_ROW_BUDGET = 8 << 30
+
+
 def _apsp_matrix(g, chunk=1024):
-    """int32 (n, n) hop distances computed on the GPU in source chunks."""
+    """int32 (n, n) hop distances: GPU bitset BFS over as many sources per
+    call as the row budget holds, copied back through pinned staging."""
     dev = require_cuda()
     csr = device_csr(g, dev)
     n = csr.n
     out = np.empty((n, n), dtype=np.int32)
     if n == 0:
         return out
-    chunk = max(64, (int(chunk) // 64) * 64)
-    bif = max(1, min(148 * 2, (chunk + 63) // 64))
+    full = ((n + 63) // 64) * 64
+    rows_per = min(full, max(64, (_APSP_ROW_BUDGET // (4 * n)) // 64 * 64))
+    bif = max(1, min(148 * 2, rows_per // 64))
     ws = workspace(_lib.load().gu_full_bfs_workspace_size(n, 0, bif), dev)
-    rows = torch.empty((min(chunk, n), n), dtype=torch.int32, device=dev)
-    for start in range(0, n, chunk):
-        stop = min(start + chunk, n)
+    rows = torch.empty((rows_per, n), dtype=torch.int32, device=dev)
+    for start in range(0, n, rows_per):
+        stop = min(start + rows_per, n)
         _lib.call("gu_apsp_rows", n, _lib.ptr(csr.indptr), _lib.ptr(csr.indices), start, stop,
                   _lib.ptr(rows), _lib.ptr(ws), ws.numel(), bif, stream_ptr(dev))
-        out[start:stop] = to_host(rows[: stop - start])
+        to_host_into(rows[: stop - start], out[start:stop])
     return out
 
 
