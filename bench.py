@@ -194,7 +194,7 @@ def run_ours(args):
     def step():
         partial_bfs_records(csr, K_NN, SEED, begin, end, out=out)
         if ws > 1:
-            gather_shards(bufs, n)
+            gather_shards(bufs, n, k=K_NN)
         return bufs[0]
 
     for _ in range(args.warmup):

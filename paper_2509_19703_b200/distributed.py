@@ -42,16 +42,25 @@ def shard_buffers(per, k, device, dtype=torch.int32):
             torch.zeros(per, dtype=dtype, device=device))
 
 
-def gather_shards(bufs, n, group=None):
+def gather_shards(bufs, n, group=None, k=None):
     """all_gather each padded buffer -> the first n rows of the
-    concatenation: (nbr [n, k], dist [n, k], cnt [n])."""
+    concatenation: (nbr [n, k], dist [n, k], cnt [n]).  Hop distances of a
+    kNN record never exceed k (every BFS level up to the k-th neighbour holds
+    at least one vertex), so for k <= 255 the distance block travels as uint8
+    and is widened after the gather: a third less traffic on the link."""
     world = dist.get_world_size(group)
+    narrow = k is not None and k <= 255
     out = []
-    for b in bufs:
-        full = torch.empty((world * b.shape[0],) + tuple(b.shape[1:]), dtype=b.dtype,
-                           device=b.device)
-        dist.all_gather_into_tensor(full, b.contiguous(), group=group)
-        out.append(full[:n])
+    for j, b in enumerate(bufs):
+        send = b
+        if j == 1 and narrow:
+            send = b.to(torch.uint8)
+        send = send.contiguous()
+        full = torch.empty((world * send.shape[0],) + tuple(send.shape[1:]), dtype=send.dtype,
+                           device=send.device)
+        dist.all_gather_into_tensor(full, send, group=group)
+        full = full[:n]
+        out.append(full.to(b.dtype) if full.dtype != b.dtype else full)
     return tuple(out)
 
 
@@ -83,7 +92,7 @@ def sharded_knn(g, k, seed=0, mode="partial", group=None):
         partial_bfs_records(csr, k_eff, seed, begin, end, out=out)
     else:
         full_knn_records(csr, k_eff, seed, begin, end, out=out)
-    nbr, dd, cnt = gather_shards(bufs, n, group)
+    nbr, dd, cnt = gather_shards(bufs, n, group, k=max(k_eff, 1))
     short = int((cnt < k_eff).sum().item()) if n else 0
     if rank == 0:
         _warn_short(short)

@@ -50,7 +50,7 @@ def _worker(rank, world, port, mode, out_dir):
     bufs[0][:ns] = torch.from_numpy(nbr.reshape(-1, k))   # the kernels write these rows in place
     bufs[1][:ns] = torch.from_numpy(dd.reshape(-1, k))
     bufs[2][:ns] = torch.from_numpy(cnt)
-    n2, d2, c2 = gather_shards(bufs, g.n)
+    n2, d2, c2 = gather_shards(bufs, g.n, k=k)  # distances travel as uint8
     np.savez(os.path.join(out_dir, f"{mode}_{rank}.npz"), nbr=n2.numpy(), dist=d2.numpy(),
              cnt=c2.numpy())
     dist.destroy_process_group()
