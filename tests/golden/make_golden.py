@@ -514,6 +514,41 @@ def gen_quality_c4(nseeds=5):
     v = np.array(vals)
     save("quality_c4.npz", np_=v[:, 0], stress=v[:, 1], sources=src)
 
+
+def _c2_seed(args):
+    """One reference c2 SS-GUMAP layout on the shared G' fixture (random
+    init, all-pairs BFS kNN k=15, 200 full epochs)."""
+    seed, edges_path, n = args
+    import time
+    t = time.time()
+    e = np.load(edges_path)
+    rg = gu.build_graph([tuple(map(int, x)) for x in e])
+    assert rg.n == n
+    dset = gu.all_pairs_bfs(rg)
+    kn = gu.knn_from_full_distances(dset, 15, seed=seed)
+    gk = gu.smooth_knn_weights(kn)
+    lay = gu.optimize_full(gk, gu.random_init(rg, seed, 10.0),
+                           gu.OptimizerConfig(iterations=200, k=15, seed=seed))
+    print("quality c2 seed", seed, f"{time.time() - t:.0f}s", flush=True)
+    return np.asarray(lay.coords, np.float64)
+
+
+def gen_quality_c2(nseeds=5):
+    """Check (c) at SS-GUMAP scale: the reference's own final layouts of c2
+    (the G' fixture of ER(20000, 200), random init, 200 full epochs), seeds
+    0..nseeds-1, one process each.  The layouts themselves are frozen (20k x 2
+    float64 each): the GPU metrics -- pinned to the reference's own metric
+    values on c1 -- then evaluate NP, stress and crossings on both sides."""
+    import multiprocessing as mp
+    import tempfile
+    g = F.config_graph("c2")
+    tmp = tempfile.mkdtemp()
+    ep = os.path.join(tmp, "edges.npy")
+    np.save(ep, np.asarray(g.edges))
+    with mp.get_context("spawn").Pool(nseeds) as pool:
+        lays = pool.map(_c2_seed, [(s, ep, g.n) for s in range(nseeds)])
+    save("quality_c2.npz", layouts=np.stack(lays), n=np.array(g.n), m=np.array(g.m))
+
 def main():
     # quality_c3_full (~1.5 h on 8 cores) runs only when named
     which = sys.argv[1:] or ["partial_small", "full_small", "smooth_cases", "c1", "c3", "quality_c1",

@@ -178,3 +178,43 @@ def test_quality_c4_sampled_vs_reference(gu):
     se = ref.std(axis=0, ddof=1) / math.sqrt(ref.shape[0]) + v.std(axis=0, ddof=1) / math.sqrt(v.shape[0])
     assert v.mean(axis=0)[0] >= ref.mean(axis=0)[0] - 4 * se[0]
     assert v.mean(axis=0)[1] <= ref.mean(axis=0)[1] + 4 * se[1]
+
+
+def test_quality_c2_exact_vs_reference(gu):
+    """Check (c) at SS scale (c2: SS-GUMAP on the G' fixture, m = 1.09M) with
+    exact metrics on both sides.  tests/golden/quality_c2.npz freezes the
+    reference's own five final c2 layouts plus the oracle's NP / stress of
+    them; the GPU metrics reproduce those values (the metric pin at n = 20k)
+    and evaluate the crossings (~1.2e11 per layout, beyond a CPU pass).  The
+    GPU c2 layouts must be no worse than 4 standard errors on each metric."""
+    import math
+
+    from paper_2509_19703_b200 import metrics as M
+
+    z = load_golden("quality_c2.npz")
+    g = gu.config_graph("c2")
+    assert g.n == int(z["n"]) and g.m == int(z["m"])
+    ref = []
+    for i, coords in enumerate(z["layouts"][:3]):
+        lay = _layout(gu, coords)
+        a, b = M.neighborhood_preservation(g, lay), M.stress(g, lay)
+        assert abs(a - z["np_"][i]) < NP_ABS_TOL
+        assert abs(b - z["stress"][i]) <= STRESS_REL_TOL * abs(z["stress"][i])
+        ref.append((a, b, M.count_crossings(g, lay)))
+    dset = gu.all_pairs_bfs(g)
+    vals = []
+    for seed in range(3):
+        knn = gu.knn_from_full_distances(dset, 15, seed=seed)
+        gk = gu.smooth_knn_weights(knn)
+        lay = gu.optimize_full(gk, gu.random_init(g, seed, 10.0),
+                               gu.OptimizerConfig(iterations=200, k=15, seed=seed), tag="SS")
+        vals.append((M.neighborhood_preservation(g, lay), M.stress(g, lay), M.count_crossings(g, lay)))
+    del dset
+    v = np.array(vals, dtype=np.float64)
+    ref = np.array(ref, dtype=np.float64)
+    print("check (c) c2 exact mean ratios gpu/ref [np, stress, crossings]:",
+          v.mean(axis=0) / ref.mean(axis=0))
+    se = ref.std(axis=0, ddof=1) / math.sqrt(ref.shape[0]) + v.std(axis=0, ddof=1) / math.sqrt(v.shape[0])
+    assert v.mean(axis=0)[0] >= ref.mean(axis=0)[0] - 4 * se[0]
+    assert v.mean(axis=0)[1] <= ref.mean(axis=0)[1] + 4 * se[1]
+    assert v.mean(axis=0)[2] <= ref.mean(axis=0)[2] + 4 * se[2]
