@@ -138,9 +138,9 @@ int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* 
  * concurrency: maximum number of edge visits in flight (threads); 0 = fill
  * the GPU.  Hogwild stays statistically close to the sequential sweep only
  * while concurrency << n, so callers cap it for small graphs.
- * nbr_filter (nullable): per-vertex 128-bit Bloom words of the neighbour ids
- * from gu_sgd_neighbor_filter (16 bytes x n); a negative whose bit is clear
- * skips the row search (exact: a set bit still searches). */
+ * nbr_filter (nullable): per-vertex 64-bit Bloom words of the neighbour ids
+ * (2 hash bits per id) from gu_sgd_neighbor_filter (8 bytes x n); a negative
+ * with a clear bit skips the row search (exact: a hit still searches). */
 int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
                          const double* sym_w, const int32_t* nbr_indptr, uint64_t seed,
                          void* edges_int4, int32_t* perm_out, void* stream);

@@ -4,7 +4,7 @@
 //   splitmix64       /root/reference/pkg/src/graph_umap/_kernels.py:13-30
 //   numpy SeedSequence + PCG64 + Generator.permutation (numpy 2.3.5), used by
 //   knn_from_full_distances (neighbors.py:213-216) for k-th distance ties.
-// Counter-based RNG for the Hogwild SGD epochs: sgd.cu draw64 (64-bit finaliser).
+// Counter-based RNG for the Hogwild SGD epochs: sgd.cu draw32 (per-visit 64-bit finaliser, 32-bit per draw).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

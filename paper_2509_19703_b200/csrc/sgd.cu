@@ -25,6 +25,8 @@
 #include <cmath>
 
 #include <cstdlib>
+#include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "gumap.h"
@@ -36,6 +38,9 @@ constexpr int TILE = 1024;
 constexpr int SGD_NEG_BLOCK = 5;
 static_assert(SGD_NEG_BLOCK <= 8, "slot bits of the cooperative search owner tag");
 constexpr unsigned FULL = 0xffffffffu;
+#ifndef SGD_SCAN
+#define SGD_SCAN 16  // neighbour-row entries compared with independent loads
+#endif
 #ifndef SGD_MIN_BLOCKS
 #define SGD_MIN_BLOCKS 4  // <= 64 registers: 32 warps per SM
 #endif  // negatives handled in lockstep per block
@@ -50,12 +55,27 @@ __device__ __host__ __forceinline__ unsigned long long mix64(unsigned long long 
   return x;
 }
 
-// counter-based draw for (edge position p, negative slot q, try t) of one
-// epoch: two rounds of a 64-bit finaliser over the packed counter
-__device__ __forceinline__ unsigned long long draw64(unsigned long long key, long long p, int q,
-                                                     int t) {
-  return mix64(mix64(key ^ (unsigned long long)p) ^ (((unsigned long long)q << 8) | (unsigned)t));
+// counter-based draws: one 64-bit finaliser per visit (base = mix64(epoch
+// key ^ edge position)), then a 32-bit finaliser per (negative slot q, try
+// t) over a Weyl step of the base -- distinct (q, t) of a visit give
+// distinct pre-images, so the draws of a visit never repeat.  The candidate
+// is the draw scaled to [0, n); the coincident-point angle is a second
+// finaliser of the same draw, evaluated only when it is needed.
+__device__ __forceinline__ unsigned fmix32(unsigned h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
 }
+
+__device__ __forceinline__ unsigned draw32(unsigned long long base, int q, int t) {
+  return fmix32(((unsigned)base + (unsigned)(q * 8 + t + 1) * 0x9E3779B9u) ^
+                (unsigned)(base >> 32));
+}
+
+__device__ __forceinline__ unsigned theta_draw(unsigned h) { return fmix32(h ^ 0x68e31da4u); }
 
 struct Feistel {
   unsigned long long m;
@@ -122,30 +142,65 @@ __device__ __forceinline__ bool is_neighbor(const int* __restrict__ ip, const in
   return false;
 }
 
-// 128-bit Bloom word of each vertex's neighbour ids (one hash bit per id):
-// a candidate whose bit is clear is certainly not a neighbour, so only the
-// ~deg/128 of draws that hit a set bit run the row search
-__device__ __forceinline__ unsigned filt_bit(int c) { return ((unsigned)c * 0x9E3779B1u) >> 25; }
+// Per-vertex Bloom word of the neighbour ids (FILT_WORDS 32-bit words,
+// FILT_K hash bits per id): a candidate with any of its bits clear is
+// certainly not a neighbour, so only the filter hits (true neighbours and
+// false positives) run the row search and the test stays exact.
+// 64 bits with 2 hash bits per id measured best (c5 epoch 3.39 -> 3.21 ms,
+// c3 0.341 -> 0.295 ms against 128 bits / 1 bit): the same false-positive
+// rate for ~12 neighbours in half the footprint, so the filter and the
+// coordinates stay L2-resident together (profiles/README.md)
+#ifndef SGD_FILT_WORDS
+#define SGD_FILT_WORDS 2
+#endif
+#ifndef SGD_FILT_K
+#define SGD_FILT_K 2
+#endif
+constexpr int FILT_WORDS = SGD_FILT_WORDS, FILT_K = SGD_FILT_K;
+static_assert(FILT_WORDS == 2 || FILT_WORDS == 4, "filter word size");
+static_assert(FILT_K >= 1 && FILT_K <= 3, "filter hash count");
+constexpr int FILT_SHIFT = FILT_WORDS == 4 ? 25 : 26;  // 32 - log2(bits)
+using FiltWord = typename std::conditional<FILT_WORDS == 4, uint4, uint2>::type;
+
+__device__ __forceinline__ unsigned filt_bit(int c, int j) {
+  const unsigned m = j == 0 ? 0x9E3779B1u : (j == 1 ? 0x85EBCA77u : 0xC2B2AE3Du);
+  return ((unsigned)c * m) >> FILT_SHIFT;
+}
+
+__device__ __forceinline__ unsigned filt_word(const uint4& f, unsigned w) {
+  return w == 0 ? f.x : (w == 1 ? f.y : (w == 2 ? f.z : f.w));
+}
+__device__ __forceinline__ unsigned filt_word(const uint2& f, unsigned w) { return w ? f.y : f.x; }
 
 __global__ void neighbor_filter_kernel(int n, const int* __restrict__ nip,
-                                       const int* __restrict__ nix, uint4* __restrict__ filt) {
+                                       const int* __restrict__ nix, FiltWord* __restrict__ filt) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     unsigned w[4] = {0u, 0u, 0u, 0u};
     const int b = __ldg(nip + v), e = __ldg(nip + v + 1);
     for (int p = b; p < e; p++) {
-      const unsigned h = filt_bit(__ldg(nix + p));
+      const int c = __ldg(nix + p);
 #pragma unroll
-      for (int j = 0; j < 4; j++)
-        if ((h >> 5) == (unsigned)j) w[j] |= 1u << (h & 31);
+      for (int k = 0; k < FILT_K; k++) {
+        const unsigned h = filt_bit(c, k);
+#pragma unroll
+        for (int j = 0; j < FILT_WORDS; j++)
+          if ((h >> 5) == (unsigned)j) w[j] |= 1u << (h & 31);
+      }
     }
-    filt[v] = make_uint4(w[0], w[1], w[2], w[3]);
+    FiltWord f;
+    memcpy(&f, w, sizeof(f));
+    filt[v] = f;
   }
 }
 
-__device__ __forceinline__ bool filt_maybe(uint4 f, int c) {
-  const unsigned h = filt_bit(c);
-  const unsigned w = (h >> 5) == 0 ? f.x : ((h >> 5) == 1 ? f.y : ((h >> 5) == 2 ? f.z : f.w));
-  return (w >> (h & 31)) & 1u;
+__device__ __forceinline__ bool filt_maybe(const FiltWord& f, int c) {
+  bool all = true;
+#pragma unroll
+  for (int k = 0; k < FILT_K; k++) {
+    const unsigned h = filt_bit(c, k);
+    all = all && ((filt_word(f, h >> 5) >> (h & 31)) & 1u);
+  }
+  return all;
 }
 
 constexpr int SGD_WARPS = 8;  // 256 threads per block at most (block_for)
@@ -154,7 +209,7 @@ template <int LANES>
 __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
     sgd_epoch_kernel(int n, long long E, float2* __restrict__ xy, const int4* __restrict__ edges,
                      const int* __restrict__ nip, const int* __restrict__ nix,
-                     const uint4* __restrict__ filt, float a, float b, float lr, int epoch,
+                     const FiltWord* __restrict__ filt, float a, float b, float lr, int epoch,
                      int n_neg, long long items, long long start, int windowed,
                      unsigned long long seed, int* __restrict__ diverged) {
   constexpr int lanes = LANES;
@@ -174,24 +229,34 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
   // lanes past the end ride along inactive
   const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long stride = (((long long)gridDim.x * blockDim.x) >> 5) * lanes;
-  for (long long i0 = gwarp * lanes; i0 < items; i0 += stride) {
+  // full mode: the `lanes` visits of one warp step share one tile (TILE is a
+  // multiple of 32 and i0 a multiple of lanes), so the tile permutation is
+  // evaluated lane-parallel for the next 32 steps and handed out by shuffle
+  unsigned tile_batch = 0;
+  int step = 0;
+  for (long long i0 = gwarp * lanes; i0 < items; i0 += stride, step = (step + 1) & 31) {
     const long long i = i0 + lane;
     bool act = lane < lanes && i < items;
     long long p = 0;
-    if (act) {
-      if (windowed) {
-        p = start + i;
-        if (p >= E) p -= E;
-      } else {
-        const long long t = i / TILE;
-        p = (long long)tperm((unsigned long long)t) * TILE + (i - t * TILE);
-        if (p >= E) act = false;  // partial last tile maps onto itself
+    if (windowed) {
+      p = start + i;
+      if (p >= E) p -= E;
+    } else {
+      if (step == 0) {
+        const long long il = i0 + (long long)lane * stride;
+        tile_batch = il < items ? (unsigned)tperm((unsigned long long)(il / TILE)) : 0u;
       }
+      const long long tile = (long long)__shfl_sync(FULL, tile_batch, step);
+      p = tile * TILE + (i - (i0 / TILE) * TILE);
+      if (p >= E) act = false;  // partial last tile maps onto itself
     }
+    if (!act) p = 0;
     // streamed once per epoch: evict-first, keep L2 for x / filter / rows
     const int4 rec = act ? __ldcs(edges + p) : make_int4(0, 0, 0, 0);
     const int u = rec.x, v = rec.y;
-    const uint4 fw = filt ? __ldg(filt + u) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    FiltWord fw;
+    if (filt) fw = __ldg(filt + u);
+    else memset(&fw, 0xff, sizeof(fw));
     const float h = __int_as_float(rec.z);
     float2 xu = xy[u];
     const float2 xv = xy[v];
@@ -213,8 +278,8 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
         if (!isfinite(xv.x - gx) || !isfinite(xv.y - gy)) bad = true;
       }
     }
-    // repulsions.  Try t of slot q draws 64 bits from draw64(epoch key, p,
-    // q, t): the high half picks the candidate, the low half is its theta.
+    // repulsions.  Try t of slot q draws 32 bits from draw32(visit base, q,
+    // t): they pick the candidate, and a second finaliser gives its theta.
     // The first tries of all slots are known up front: their coordinate
     // loads go out at once, and only the candidates whose neighbour-filter
     // bit is set (~deg/128 of them) are searched in the head's sorted row --
@@ -222,6 +287,7 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
     // rejected try (c == u or a neighbour) takes the sequential retry path.
     // The repulsion math stays sequential in slot order on the register copy
     // of x_u, as in the reference sweep.
+    const unsigned long long vbase = mix64(rkey ^ (unsigned long long)p);
     int rb = 0, re = 0;
     if (act) {
       if (rec.w >= 0) {
@@ -235,13 +301,12 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
     for (int q0 = 0; q0 < n_neg; q0 += SGD_NEG_BLOCK) {
       const int nq = min(SGD_NEG_BLOCK, n_neg - q0);
       int cand[SGD_NEG_BLOCK];
-      unsigned spare_q[SGD_NEG_BLOCK];
+      unsigned draw_q[SGD_NEG_BLOCK];
       unsigned mm = 0;  // slots whose filter bit is set
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
-        const unsigned long long r = draw64(rkey, p, q0 + q, 0);
-        cand[q] = (int)__umulhi((unsigned)(r >> 32), (unsigned)n);
-        spare_q[q] = (unsigned)r;
+        draw_q[q] = draw32(vbase, q0 + q, 0);
+        cand[q] = (int)__umulhi(draw_q[q], (unsigned)n);
         if (act && q < nq && filt_maybe(fw, cand[q])) mm |= 1u << q;
       }
       float2 xc[SGD_NEG_BLOCK];
@@ -268,7 +333,10 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
         for (int t = lane; t < total; t += 32) {
           const int4 pr = sh_pairs[wib][t];
           int lo = pr.y, len = pr.z - pr.y;
-          while (len > 0) {
+          // binary steps only above SCAN entries (long rows); the rest of the
+          // row is read with independent loads: one memory round trip
+          // instead of a chain of dependent probes
+          while (len > SGD_SCAN) {
             const int half = len >> 1;
             if (__ldg(nix + lo + half) < pr.x) {
               lo += half + 1;
@@ -277,7 +345,13 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
               len = half;
             }
           }
-          if (lo < pr.z && __ldg(nix + lo) == pr.x) atomicOr(&sh_hit[wib][pr.w >> 3], 1u << (pr.w & 7));
+          int x[SGD_SCAN];
+#pragma unroll
+          for (int q = 0; q < SGD_SCAN; q++) x[q] = q < len ? __ldg(nix + lo + q) : -1;
+          bool found = false;
+#pragma unroll
+          for (int q = 0; q < SGD_SCAN; q++) found |= x[q] == pr.x;
+          if (found) atomicOr(&sh_hit[wib][pr.w >> 3], 1u << (pr.w & 7));
         }
         __syncwarp();
         hit = sh_hit[wib][lane];
@@ -289,15 +363,15 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
         if (q >= nq) break;
         const bool ok = cand[q] != u && !((hit >> q) & 1u);
         int c = ok ? cand[q] : -1;
-        unsigned spare = spare_q[q];  // theta draw of this slot
+        unsigned draw = draw_q[q];  // the accepted try's draw (angle source)
         if (!ok) {
           // retries 2..8 of this slot (rare)
           for (int t = 1; t < 8; t++) {
-            const unsigned long long rr = draw64(rkey, p, q0 + q, t);
-            const int cc = (int)__umulhi((unsigned)(rr >> 32), (unsigned)n);
+            const unsigned rr = draw32(vbase, q0 + q, t);
+            const int cc = (int)__umulhi(rr, (unsigned)n);
             if (cc == u || is_neighbor(nip, nix, u, cc)) continue;
             c = cc;
-            spare = (unsigned)rr;
+            draw = rr;
             break;
           }
           if (c < 0) continue;
@@ -311,7 +385,7 @@ __global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
           gx = clip4(g * dx);
           gy = clip4(g * dy);
         } else {
-          const float th = (float)spare * (6.283185307179586f / 4294967296.0f);
+          const float th = (float)theta_draw(draw) * (6.283185307179586f / 4294967296.0f);
           float sn, cs;
           __sincosf(th, &sn, &cs);
           gx = 4.0f * cs;
@@ -406,7 +480,7 @@ extern "C" int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr,
     return GU_ERR_ARG;
   }
   neighbor_filter_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
-      (int)n, nbr_indptr, nbr_indices, (uint4*)filter_out);
+      (int)n, nbr_indptr, nbr_indices, (FiltWord*)filter_out);
   GU_CHECK_LAUNCH("neighbor_filter_kernel");
   return GU_OK;
 }
@@ -448,7 +522,7 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
     const unsigned gs = bs < 256 ? 1u : grid_for((items * 32 + lanes - 1) / lanes, threads);
     auto kern = lanes == 32 ? sgd_epoch_kernel<32> : sgd_epoch_kernel<16>;
     kern<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr,
-                            nbr_indices, (const uint4*)nbr_filter, a, b, lr, e, n_neg, items,
+                            nbr_indices, (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, items,
                             start, windowed, seed, diverged);
     GU_CHECK_LAUNCH("sgd_epoch_kernel");
   }

@@ -435,6 +435,8 @@ def test_sgd_neighbor_filter_covers_neighbors(gu):
     filt = plan.filter.cpu().numpy().view(np.uint32)
     ip, ix = gk.nbr_indptr, gk.nbr_indices
     src = np.repeat(np.arange(gk.n), np.diff(ip))
-    h = ((ix.astype(np.uint64) * np.uint64(0x9E3779B1)) & np.uint64(0xFFFFFFFF)) >> np.uint64(25)
-    words = filt[src, (h >> np.uint64(5)).astype(np.int64)]
-    assert np.all((words >> (h & np.uint64(31)).astype(np.uint32)) & 1)
+    assert filt.shape == (gk.n, 2)
+    for mult in (0x9E3779B1, 0x85EBCA77):  # the two hash bits of an id
+        h = ((ix.astype(np.uint64) * np.uint64(mult)) & np.uint64(0xFFFFFFFF)) >> np.uint64(26)
+        words = filt[src, (h >> np.uint64(5)).astype(np.int64)]
+        assert np.all((words >> (h & np.uint64(31)).astype(np.uint32)) & 1)
