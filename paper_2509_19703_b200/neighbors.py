@@ -252,18 +252,19 @@ def all_pairs_bfs(g, chunk=1024):
 
 
 # --------------------------------------------------------------- records
-def _pack(n_rows, k, rec_nbr, rec_dist, rec_cnt, dev, full=None):
+def _pack(n_rows, k, rec_nbr, rec_dist, rec_cnt, dev, full=None, indptr=None):
     """Fixed-stride records -> (indptr int64, dst int32, dist int32) on device.
 
     When every row is full (``full``; computed if None) the records already
-    are the packed CSR and the indptr is k * arange."""
-    indptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
+    are the packed CSR and the indptr is k * arange (``indptr`` when given)."""
     total_max = n_rows * k
     if full is None:
         full = bool(total_max) and bool((rec_cnt == k).all())
     if total_max and full:
-        torch.arange(0, (n_rows + 1) * k, k, dtype=torch.int64, device=dev, out=indptr)
+        if indptr is None:
+            indptr = torch.arange(0, (n_rows + 1) * k, k, dtype=torch.int64, device=dev)
         return indptr, rec_nbr.reshape(-1)[:total_max], rec_dist.reshape(-1)[:total_max]
+    indptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
     ws = workspace(_lib.load().gu_pack_records_workspace_size(n_rows), dev)
     dst = torch.empty(max(total_max, 1), dtype=torch.int32, device=dev)
     dist = torch.empty(max(total_max, 1), dtype=torch.int32, device=dev)
@@ -367,19 +368,29 @@ def partial_bfs(g, k, seed=0):
     dist = torch.empty((n, kk), dtype=torch.int32, device=dev)
     cnt = torch.empty(n, dtype=torch.int32, device=dev)
     prefetch = _HostPrefetch(dev, n * kk, ("dst", "dist")) if n * kk * 8 >= (64 << 20) else None
-    nchunk = 4 if prefetch is not None else 1
-    bounds = [n * i // nchunk for i in range(nchunk + 1)]
+    ip_full = None
+    if prefetch is not None:
+        # small first chunks, so the row copies start early; the indptr of
+        # the all-rows-full outcome goes down during the first kernel and is
+        # used when no row turns out short
+        bounds = sorted({0, n // 16, n // 4, n // 2, (3 * n) // 4, n})
+        ip_full = torch.arange(0, (n + 1) * kk, kk, dtype=torch.int64, device=dev)
+        prefetch.copy_extra("indptr", ip_full)
+    else:
+        bounds = [0, n]
     tw = _tier2_warps(n)
-    ws = workspace(_lib.load().gu_partial_bfs_workspace_size(n, bounds[1] - bounds[0] + 1, tw), dev)
-    for c in range(nchunk):
-        b, e = bounds[c], bounds[c + 1]
+    most = max(e - b for b, e in zip(bounds[:-1], bounds[1:]))
+    ws = workspace(_lib.load().gu_partial_bfs_workspace_size(n, most + 1, tw), dev)
+    for b, e in zip(bounds[:-1], bounds[1:]):
         partial_bfs_records(csr, k_eff, seed, b, e, tier2_warps=tw, out=(nbr[b:e], dist[b:e], cnt[b:e]),
                             ws=ws)
         if prefetch is not None:
             prefetch.copy_rows(dict(dst=nbr, dist=dist), b * kk, e * kk)
     short = int((cnt < k_eff).sum().item()) if n else 0
     _warn_short(short)
-    indptr, dst, dd = _pack(n, k_eff, nbr, dist, cnt, dev, full=(short == 0 and k_eff > 0))
+    full = short == 0 and k_eff > 0
+    indptr, dst, dd = _pack(n, k_eff, nbr, dist, cnt, dev, full=full,
+                            indptr=ip_full if full else None)
     host = {}
     if prefetch is not None and short == 0:
         host = prefetch.finish()  # rows are the packed arrays: host copies are valid
@@ -413,6 +424,18 @@ class _HostPrefetch:
                 self.host[nm][lo:hi].copy_(t.reshape(-1)[lo:hi], non_blocking=True)
         self.done = torch.cuda.Event()
         self.done.record(self.stream)
+
+    def copy_extra(self, name, t):
+        """Whole-tensor copy of ``t`` (ordered after the compute stream's work
+        so far) into a pinned buffer delivered by finish() under ``name``."""
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        buf = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        with torch.cuda.stream(self.stream):
+            self.stream.wait_event(ev)
+            buf.copy_(t, non_blocking=True)
+        t.record_stream(self.stream)
+        self.host[name] = buf
 
     def finish(self):
         return {nm: (h, self.done) for nm, h in self.host.items()}

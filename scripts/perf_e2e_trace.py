@@ -24,7 +24,7 @@ def T():
     return time.perf_counter()
 
 
-for rep in range(5):
+for rep in range(12):
     gg = Graph(n=g.n, m=g.m, adj_indptr=pinned(np.asarray(g.adj_indptr)),
                adj_indices=pinned(np.asarray(g.adj_indices)), edges=g.edges)
     t0 = T()
