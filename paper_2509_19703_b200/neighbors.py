@@ -45,7 +45,8 @@ class _LazyArrays:
     def _init_lazy(self, host, dev):
         object.__setattr__(self, "_host", dict(host))
         object.__setattr__(self, "_dev", dict(dev))
-        object.__setattr__(self, "_pending", {})  # name -> (pinned tensor, event)
+        object.__setattr__(self, "_pending", {})  # name -> (pinned tensor, waiter)
+        object.__setattr__(self, "_pending_bytes", None)
 
     def _get_host(self, name):
         h = self._host.get(name)
@@ -367,7 +368,9 @@ def partial_bfs(g, k, seed=0):
     nbr = torch.empty((n, kk), dtype=torch.int32, device=dev)
     dist = torch.empty((n, kk), dtype=torch.int32, device=dev)
     cnt = torch.empty(n, dtype=torch.int32, device=dev)
-    prefetch = _HostPrefetch(dev, n * kk, ("dst", "dist")) if n * kk * 8 >= (64 << 20) else None
+    # rows cross PCIe as int32 ids and (hop distances <= k) uint8 distances
+    prefetch = (_HostPrefetch(dev, n * kk, ("dst", "dist"), narrow=("dist",) if kk <= 255 else ())
+                if n * kk * 8 >= (64 << 20) else None)
     ip_full = None
     if prefetch is not None:
         # small first chunks, so the row copies start early; the indptr of
@@ -400,30 +403,90 @@ def partial_bfs(g, k, seed=0):
     for name, pend in host.items():
         knn._pending[name] = pend
         dset._pending["nbr" if name == "dst" else name] = pend
+    if host:
+        # bytes that crossed PCIe for the host arrays (narrowed rows count as
+        # sent); reported by bench.py's e2e line
+        object.__setattr__(knn, "_pending_bytes", sum(
+            t.numel() * (1 if nm in prefetch.narrow else t.element_size()) for nm, (t, _) in host.items()))
     return dset, knn
+
+
+_WIDEN_POOL = None
+
+
+def _widen_pool():
+    """Host threads that widen narrowed row copies (numpy releases the GIL in
+    casting copies; torch releases it in Event.synchronize)."""
+    global _WIDEN_POOL
+    if _WIDEN_POOL is None:
+        import concurrent.futures
+        import os
+        workers = int(os.environ.get("GU_WIDEN_THREADS", 0)) or max(1, (os.cpu_count() or 1) - 2)
+        _WIDEN_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=workers)
+    return _WIDEN_POOL
+
+
+class _Waiter:
+    """Completion of a pending host array: a CUDA event and/or host futures."""
+
+    def __init__(self, event=None, futures=()):
+        self.event = event
+        self.futures = list(futures)
+
+    def synchronize(self):
+        if self.event is not None:
+            self.event.synchronize()
+        for f in self.futures:
+            f.result()
 
 
 class _HostPrefetch:
     """Asynchronous device -> pinned-host copies of row ranges on a side
-    stream, ordered after the compute stream's work so far."""
+    stream, ordered after the compute stream's work so far.
+
+    Arrays named in ``narrow`` (small non-negative ints, e.g. hop distances
+    <= k <= 255) cross PCIe as uint8 -- a quarter of the bytes -- and are
+    widened back to int32 by host threads as each range lands, overlapping
+    the remaining copies."""
 
     _streams = {}
 
-    def __init__(self, dev, numel, names):
+    def __init__(self, dev, numel, names, narrow=()):
         self.dev = dev
         self.stream = self._streams.setdefault(str(dev), torch.cuda.Stream(device=dev))
         self.host = {nm: torch.empty(numel, dtype=torch.int32, pin_memory=True) for nm in names}
+        self.narrow = {nm: (torch.empty(numel, dtype=torch.uint8, device=dev),
+                            torch.empty(numel, dtype=torch.uint8, pin_memory=True))
+                       for nm in narrow if nm in names}
+        self.futures = {nm: [] for nm in self.narrow}
         self.done = None
 
     def copy_rows(self, srcs, lo, hi):
+        for nm, (stage, _) in self.narrow.items():
+            stage[lo:hi].copy_(srcs[nm].reshape(-1)[lo:hi])  # int32 -> uint8 on the device
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(self.stream):
             self.stream.wait_event(ev)
             for nm, t in srcs.items():
-                self.host[nm][lo:hi].copy_(t.reshape(-1)[lo:hi], non_blocking=True)
+                if nm in self.narrow:
+                    stage, pin8 = self.narrow[nm]
+                    pin8[lo:hi].copy_(stage[lo:hi], non_blocking=True)
+                    stage.record_stream(self.stream)
+                else:
+                    self.host[nm][lo:hi].copy_(t.reshape(-1)[lo:hi], non_blocking=True)
         self.done = torch.cuda.Event()
         self.done.record(self.stream)
+        if self.narrow:
+            pool = _widen_pool()
+            parts = pool._max_workers
+            bounds = np.linspace(lo, hi, parts + 1).astype(np.int64)
+            for nm, (_, pin8) in self.narrow.items():
+                src = pin8.numpy()
+                dst = self.host[nm].numpy()
+                for a, b in zip(bounds[:-1], bounds[1:]):
+                    if b > a:
+                        self.futures[nm].append(pool.submit(_widen, self.done, dst[a:b], src[a:b]))
 
     def copy_extra(self, name, t):
         """Whole-tensor copy of ``t`` (ordered after the compute stream's work
@@ -438,7 +501,13 @@ class _HostPrefetch:
         self.host[name] = buf
 
     def finish(self):
-        return {nm: (h, self.done) for nm, h in self.host.items()}
+        return {nm: (h, _Waiter(self.done, self.futures.get(nm, ())))
+                for nm, h in self.host.items()}
+
+
+def _widen(event, dst, src):
+    event.synchronize()
+    np.copyto(dst, src, casting="unsafe")
 
 
 def knn_from_full_distances(dist_set, k, seed=0):
