@@ -70,10 +70,16 @@ __global__ void fx_indeg(long long nnz, const int* __restrict__ dst, int* __rest
 // one warp per vertex u: forward entries u*k .. u*k+k-1 (sorted by (id, i)
 // in registers) merged with the backward entries in_e[in_ptr[u] ..) whose
 // source rows are ascending; equal ids: forward first, each side in original
-// order -- exactly the order of the stable global sort it replaces
+// order -- exactly the order of the stable global sort it replaces.  The
+// union is resolved here too (what union_flags does for the generic path):
+// the head of each key -- its first forward entry, or its first backward
+// entry when no forward entry has that id -- gets h = (a + b) - a*b from the
+// key's first forward weight a and first backward weight b (0 when absent)
+// and the flag h != 0; every other entry of the key gets flag 0.
 __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __restrict__ dst,
-                         const long long* __restrict__ in_ptr, const int* __restrict__ in_e,
-                         unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+                         const double* __restrict__ w, const long long* __restrict__ in_ptr,
+                         const int* __restrict__ in_e, unsigned long long* __restrict__ keys,
+                         int* __restrict__ flag, double* __restrict__ hval) {
   const int lane = threadIdx.x & 31;
   for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
        u += ((long long)gridDim.x * blockDim.x) >> 5) {
@@ -92,6 +98,7 @@ __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __rest
     }
     const int fid = (int)(fk >> 32);                  // this lane's forward id (sorted)
     const int fpos = (int)(unsigned)fk;                // its position in the row
+    const int prev_fid = __shfl_up_sync(FULL_MASK, fid, 1);
     const long long ib = in_ptr[u], m = in_ptr[u + 1] - ib;
     const long long out0 = fb + ib;                    // row start in the both array
     // forward element of rank `lane`: position lane + #backward with id < fid
@@ -104,9 +111,23 @@ __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __rest
       }
       const long long o = out0 + lane + lo;
       keys[o] = (unsigned long long)u * (unsigned long long)n + (unsigned long long)fid;
-      vals[o] = (int)(fb + fpos);
+      int f = 0;
+      double h = 0.0;
+      if (lane == 0 || prev_fid != fid) {  // first forward entry of this id
+        const double a = w[fb + fpos];
+        double b = 0.0;
+        if (lo < m) {
+          const int e = in_e[ib + lo];
+          if (e / kfix == fid) b = w[e];  // first backward entry of this id
+        }
+        h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
+        f = h != 0.0;
+      }
+      flag[o] = f;
+      hval[o] = h;
     }
     // backward elements: position j + #forward with id <= their id
+    int carry = -1;  // source id of the previous chunk's last backward entry
     for (long long j0 = 0; j0 < m; j0 += 32) {
       const long long j = j0 + lane;
       int e = 0, bid = 0;
@@ -116,11 +137,27 @@ __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __rest
       }
       // upper bound over the sorted forward ids (held one per lane)
       int cnt = 0;
-      for (int q = 0; q < kfix; q++) cnt += __shfl_sync(FULL_MASK, fid, q) <= bid;
+      bool in_fwd = false;
+      for (int q = 0; q < kfix; q++) {
+        const int x = __shfl_sync(FULL_MASK, fid, q);
+        cnt += x <= bid;
+        in_fwd |= x == bid;
+      }
+      const int up = __shfl_up_sync(FULL_MASK, bid, 1);
+      const int prev = lane == 0 ? carry : up;
+      carry = __shfl_sync(FULL_MASK, bid, 31);
       if (j < m) {
         const long long o = out0 + j + cnt;
         keys[o] = (unsigned long long)u * (unsigned long long)n + (unsigned long long)bid;
-        vals[o] = (int)(nnz + e);
+        int f = 0;
+        double h = 0.0;
+        if (!in_fwd && prev != bid) {  // key with no forward entry: its first backward one
+          const double a = 0.0, b = w[e];
+          h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
+          f = h != 0.0;
+        }
+        flag[o] = f;
+        hval[o] = h;
       }
     }
   }
@@ -300,7 +337,6 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
       kfix = rows_fixed(indptr, n, kfix, ws.partial, st) ? kfix : 0;
     }
     const unsigned long long* sorted_keys;
-    const int* sorted_vals;
     if (kfix > 0 && kfix <= 32) {
       // fast path: backward entries sorted by destination only (32-bit keys,
       // value = entry index), then one warp merges each vertex's rows
@@ -319,12 +355,11 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
       GU_CHECK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, cb, kb, vbuf, (int)nnz, 0, vb_bits, st));
       int r0 = scan_counts(indeg, n, ws.pos, ws.partial, st);  // in_ptr in ws.pos[0..n]
       if (r0) return r0;
-      fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, nnz, dst, ws.pos, vbuf.Current(), ws.k0,
-                                                  ws.v0);
+      fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, nnz, dst, w, ws.pos, vbuf.Current(),
+                                                  ws.k0, ws.flag, ws.h);
       GU_CHECK_LAUNCH("fx_merge");
       GU_CHECK(cudaMemsetAsync(ws.rowcnt, 0, sizeof(int) * (size_t)(n + 1), st));
       sorted_keys = ws.k0;
-      sorted_vals = ws.v0;
     } else {
       build_keys<<<grid_for(nnz), 256, 0, st>>>(n, n, (const long long*)indptr, dst, nnz, kfix,
                                                 ws.k0, ws.v0);
@@ -337,10 +372,9 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
       size_t cb = ws.cub_bytes;
       GU_CHECK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, cb, kb, vb, (int)m, 0, end_bit, st));
       sorted_keys = kb.Current();
-      sorted_vals = vb.Current();
+      union_flags<<<grid_for(m), 256, 0, st>>>(m, nnz, sorted_keys, vb.Current(), w, ws.flag, ws.h);
+      GU_CHECK_LAUNCH("union_flags");
     }
-    union_flags<<<grid_for(m), 256, 0, st>>>(m, nnz, sorted_keys, sorted_vals, w, ws.flag, ws.h);
-    GU_CHECK_LAUNCH("union_flags");
     int r = scan_counts(ws.flag, m, ws.pos, ws.partial, st);
     if (r) return r;
     union_write<<<grid_for(m), 256, 0, st>>>(m, n, sorted_keys, ws.flag, ws.h, ws.pos, sym_src,
