@@ -10,6 +10,8 @@
 // inside a key and each keeps its original order, so the first forward entry
 // is a and the first backward entry is b.  h = (a + b) - a*b rounded step by
 // step (explicit _rn intrinsics: no FMA), kept iff h != 0.
+#include <climits>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -78,8 +80,8 @@ __global__ void fx_indeg(long long nnz, const int* __restrict__ dst, int* __rest
 // and the flag h != 0; every other entry of the key gets flag 0.
 __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __restrict__ dst,
                          const double* __restrict__ w, const long long* __restrict__ in_ptr,
-                         const int* __restrict__ in_e, unsigned long long* __restrict__ keys,
-                         int* __restrict__ flag, double* __restrict__ hval) {
+                         const int* __restrict__ in_e, int* __restrict__ other,
+                         double* __restrict__ hval, int* __restrict__ rowcnt) {
   const int lane = threadIdx.x & 31;
   for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
        u += ((long long)gridDim.x * blockDim.x) >> 5) {
@@ -101,37 +103,54 @@ __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __rest
     const int prev_fid = __shfl_up_sync(FULL_MASK, fid, 1);
     const long long ib = in_ptr[u], m = in_ptr[u + 1] - ib;
     const long long out0 = fb + ib;                    // row start in the both array
+    int kept = 0;                                      // this lane's kept keys
+    // first backward chunk, one entry per lane (the whole list when m <= 32)
+    const int e_first = lane < m ? in_e[ib + lane] : 0;
+    const int bid_first = lane < m ? e_first / kfix : INT_MAX;
     // forward element of rank `lane`: position lane + #backward with id < fid
-    if (lane < kfix) {
-      long long lo = 0, hi = m;
-      while (lo < hi) {
-        const long long mid = (lo + hi) >> 1;
-        if ((int)(in_e[ib + mid] / kfix) < fid) lo = mid + 1;
-        else hi = mid;
+    if (lane < kfix || m <= 32) {  // (warp-uniform shuffles when m <= 32)
+      long long lo = 0;
+      if (m <= 32) {  // lower bound over the register-resident backward ids
+#pragma unroll
+        for (int step = 32; step > 0; step >>= 1) {
+          const int x = __shfl_sync(FULL_MASK, bid_first, (int)(lo + step - 1) & 31);
+          if (lo + step - 1 < m && x < fid) lo += step;
+        }
+      } else {
+        long long hi = m;
+        while (lo < hi) {
+          const long long mid = (lo + hi) >> 1;
+          if ((int)(in_e[ib + mid] / kfix) < fid) lo = mid + 1;
+          else hi = mid;
+        }
       }
+      const int e_lo = m <= 32 ? __shfl_sync(FULL_MASK, e_first, (int)lo & 31) : 0;
+      if (lane < kfix) {
       const long long o = out0 + lane + lo;
-      keys[o] = (unsigned long long)u * (unsigned long long)n + (unsigned long long)fid;
-      int f = 0;
+      other[o] = fid;
       double h = 0.0;
       if (lane == 0 || prev_fid != fid) {  // first forward entry of this id
         const double a = w[fb + fpos];
         double b = 0.0;
         if (lo < m) {
-          const int e = in_e[ib + lo];
+          const int e = m <= 32 ? e_lo : in_e[ib + lo];
           if (e / kfix == fid) b = w[e];  // first backward entry of this id
         }
         h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
-        f = h != 0.0;
+        kept += h != 0.0;
       }
-      flag[o] = f;
       hval[o] = h;
+      }
     }
     // backward elements: position j + #forward with id <= their id
     int carry = -1;  // source id of the previous chunk's last backward entry
     for (long long j0 = 0; j0 < m; j0 += 32) {
       const long long j = j0 + lane;
       int e = 0, bid = 0;
-      if (j < m) {
+      if (j0 == 0) {
+        e = e_first;
+        bid = lane < m ? bid_first : 0;
+      } else if (j < m) {
         e = in_e[ib + j];
         bid = e / kfix;
       }
@@ -148,17 +167,45 @@ __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __rest
       carry = __shfl_sync(FULL_MASK, bid, 31);
       if (j < m) {
         const long long o = out0 + j + cnt;
-        keys[o] = (unsigned long long)u * (unsigned long long)n + (unsigned long long)bid;
-        int f = 0;
+        other[o] = bid;
         double h = 0.0;
         if (!in_fwd && prev != bid) {  // key with no forward entry: its first backward one
           const double a = 0.0, b = w[e];
           h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
-          f = h != 0.0;
+          kept += h != 0.0;
         }
-        flag[o] = f;
         hval[o] = h;
       }
+    }
+    kept = warp_sum(kept);
+    if (lane == 0) rowcnt[u] = kept;
+  }
+}
+
+// one warp per vertex: the kept entries (h != 0: only key heads can be) of
+// its both-array segment, in order, to its output row nbr_indptr[u] ..
+__global__ void fx_compact(long long n, int kfix, const long long* __restrict__ in_ptr,
+                           const int* __restrict__ other, const double* __restrict__ hval,
+                           const long long* __restrict__ out_ptr, int* __restrict__ sym_src,
+                           int* __restrict__ sym_dst, double* __restrict__ sym_w) {
+  const int lane = threadIdx.x & 31;
+  for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long ib = in_ptr[u];
+    const long long seg = u * kfix + ib, len = kfix + (in_ptr[u + 1] - ib);
+    long long o = out_ptr[u];
+    for (long long j0 = 0; j0 < len; j0 += 32) {
+      const long long j = j0 + lane;
+      const double h = j < len ? hval[seg + j] : 0.0;
+      const bool keep = h != 0.0;
+      const unsigned bal = __ballot_sync(FULL_MASK, keep);
+      if (keep) {
+        const long long q = o + __popc(bal & ((1u << lane) - 1u));
+        sym_src[q] = (int)u;
+        sym_dst[q] = other[seg + j];
+        sym_w[q] = h;
+      }
+      o += __popc(bal);
     }
   }
 }
@@ -344,7 +391,7 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
       int* ikey1 = ikey0 + nnz;
       int* ival0 = ws.v1;
       int* ival1 = ws.v1 + nnz;
-      int* indeg = ws.rowcnt;  // zeroed above; reset before union_write
+      int* indeg = ws.rowcnt;  // zeroed above; fx_merge then overwrites it with the kept counts
       fx_indeg<<<grid_for(nnz), 256, 0, st>>>(nnz, dst, indeg, ikey0, ival0);
       GU_CHECK_LAUNCH("fx_indeg");
       int vb_bits = 1;
@@ -355,11 +402,22 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
       GU_CHECK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp, cb, kb, vbuf, (int)nnz, 0, vb_bits, st));
       int r0 = scan_counts(indeg, n, ws.pos, ws.partial, st);  // in_ptr in ws.pos[0..n]
       if (r0) return r0;
+      // merge + union per vertex (other endpoint and h per both-array slot,
+      // kept count per vertex), scan of the counts = nbr_indptr, compaction
       fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, nnz, dst, w, ws.pos, vbuf.Current(),
-                                                  ws.k0, ws.flag, ws.h);
+                                                  ws.v0, ws.h, ws.rowcnt);
       GU_CHECK_LAUNCH("fx_merge");
-      GU_CHECK(cudaMemsetAsync(ws.rowcnt, 0, sizeof(int) * (size_t)(n + 1), st));
-      sorted_keys = ws.k0;
+      int r1 = scan_counts(ws.rowcnt, n, (long long*)nbr_indptr, ws.partial, st);
+      if (r1) return r1;
+      fx_compact<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, ws.pos, ws.v0, ws.h,
+                                                    (const long long*)nbr_indptr, sym_src, sym_dst,
+                                                    sym_w);
+      GU_CHECK_LAUNCH("fx_compact");
+      long long E = 0;
+      GU_CHECK(cudaMemcpyAsync(&E, nbr_indptr + n, sizeof(long long), cudaMemcpyDeviceToHost, st));
+      GU_CHECK(cudaStreamSynchronize(st));
+      *host_E = E;
+      return GU_OK;
     } else {
       build_keys<<<grid_for(nnz), 256, 0, st>>>(n, n, (const long long*)indptr, dst, nnz, kfix,
                                                 ws.k0, ws.v0);
