@@ -421,6 +421,28 @@ def test_pinned_host_inputs(gu):
     assert np.array_equal(a.dist, b.dist)
 
 
+def test_partial_bfs_host_path_matches_records(gu):
+    """The public partial_bfs at a size where its host path engages (chunked
+    row copies on a side stream, distances sent as uint8 and widened by host
+    threads, all-rows-full indptr copied during the first kernel) returns
+    exactly the device records, and the distance set shares them."""
+    from paper_2509_19703_b200.device import device_csr
+    from paper_2509_19703_b200.neighbors import partial_bfs_records
+
+    g = gu.synth_graph("scale_free", 700_000, seed=5, m0=3)  # n * k * 8 B >= 64 MB
+    dset, knn = gu.partial_bfs(g, 15, seed=9)
+    assert knn._pending_bytes is not None  # the narrowed copy path ran
+    assert knn._pending_bytes == (g.n + 1) * 8 + g.n * 15 * (4 + 1)
+    nbr, dist, cnt = partial_bfs_records(device_csr(g), 15, 9, 0, g.n)
+    assert np.all(cnt.cpu().numpy() == 15)
+    assert knn.indptr.dtype == np.int64 and knn.dst.dtype == np.int32 and knn.dist.dtype == np.int32
+    assert np.array_equal(knn.indptr, 15 * np.arange(g.n + 1))
+    assert np.array_equal(knn.dst, nbr.cpu().numpy().reshape(-1))
+    assert np.array_equal(knn.dist, dist.cpu().numpy().reshape(-1))
+    assert np.array_equal(dset.nbr, knn.dst) and np.array_equal(dset.dist, knn.dist)
+    assert np.array_equal(dset.indptr, knn.indptr)
+
+
 def test_sgd_neighbor_filter_covers_neighbors(gu):
     """The SGD negative-sampling Bloom words (csrc/sgd.cu) have the bit of
     every neighbour set, so skipping the row search on a clear bit never
