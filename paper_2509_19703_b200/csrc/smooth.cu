@@ -76,54 +76,223 @@ __device__ double pairwise(RowView& r, int start, int len) {
   }
 }
 
-__global__ void __launch_bounds__(128)
-    smooth_kernel(long long n, const long long* __restrict__ indptr, const int* __restrict__ dist,
-                  int kmax, double target, double* __restrict__ rho_out,
-                  double* __restrict__ sigma_out, double* __restrict__ w_out) {
+// sigma of one row (the reference's control flow, see the file header);
+// rho_out receives the row minimum
+__device__ double row_sigma(const int* d, int c, int kmax, double target, double* rho_out) {
   const double SMIN = 1e-3, SMAX = 1e3, TOL = 1e-5;
-  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (long long)gridDim.x * blockDim.x) {
-    const long long lo = indptr[v];
-    const int c = (int)(indptr[v + 1] - lo);
-    RowView r;
-    r.d = dist + lo;
-    r.c = c < kmax ? c : kmax;
-    double rho = INFINITY;
-    for (int i = 0; i < r.c; i++) rho = fmin(rho, (double)r.d[i]);
-    bool all_equal = true;
-    for (int i = 0; i < r.c; i++)
-      if ((double)r.d[i] != rho) all_equal = false;
-    r.rho = rho;
-    double sigma = SMAX;
-    if (!all_equal) {
-      r.set_sigma(SMAX);
-      const double s_hi = pairwise(r, 0, kmax);
-      r.set_sigma(SMIN);
-      const double s_lo = pairwise(r, 0, kmax);
-      const bool clamp_hi = s_hi < target, clamp_lo = s_lo > target;
-      if (clamp_hi) sigma = SMAX;
-      if (clamp_lo) sigma = SMIN;
-      if (!clamp_hi && !clamp_lo) {
-        double los = SMIN, his = SMAX, mid = (los + his) / 2.0;
-        bool live = true;
-        for (int it = 0; it < 64; it++) {
-          r.set_sigma(mid);
-          const double s = pairwise(r, 0, kmax);
-          if (fabs(s - target) < TOL) {
-            sigma = mid;
-            live = false;
+  RowView r;
+  r.d = d;
+  r.c = c < kmax ? c : kmax;
+  double rho = INFINITY;
+  for (int i = 0; i < r.c; i++) rho = fmin(rho, (double)r.d[i]);
+  bool all_equal = true;
+  for (int i = 0; i < r.c; i++)
+    if ((double)r.d[i] != rho) all_equal = false;
+  r.rho = rho;
+  *rho_out = rho;
+  double sigma = SMAX;
+  if (!all_equal) {
+    r.set_sigma(SMAX);
+    const double s_hi = pairwise(r, 0, kmax);
+    r.set_sigma(SMIN);
+    const double s_lo = pairwise(r, 0, kmax);
+    const bool clamp_hi = s_hi < target, clamp_lo = s_lo > target;
+    if (clamp_hi) sigma = SMAX;
+    if (clamp_lo) sigma = SMIN;
+    if (!clamp_hi && !clamp_lo) {
+      double los = SMIN, his = SMAX, mid = (los + his) / 2.0;
+      bool live = true;
+      for (int it = 0; it < 64; it++) {
+        r.set_sigma(mid);
+        const double s = pairwise(r, 0, kmax);
+        if (fabs(s - target) < TOL) {
+          sigma = mid;
+          live = false;
+          break;
+        }
+        if (s > target) his = mid; else los = mid;
+        mid = (los + his) / 2.0;
+      }
+      if (live) sigma = mid;
+    }
+  }
+  return sigma;
+}
+
+// ---- memoised sigma.  A row's sigma is a function of its padded distance
+// vector alone, and rows arrive sorted by (distance, id), so the vector is
+// its run-length profile (distance, count) per run.  kNN rows of hop
+// distances have a handful of profiles (c5: 4M rows, ~10^2 profiles), so the
+// bisection runs once per profile: rows are keyed (<= 4 runs, distance < 256,
+// count < 64), the keys deduplicated into a device table, sigma solved per
+// table entry on a representative row, and every row reads it back.  Rows
+// that do not fit a key, or find the table full, are solved directly.  The
+// result is the same float64 computation on the same operands: bit-identical.
+constexpr int SIG_TABLE = 8192;
+constexpr unsigned long long SIG_EMPTY = 0ull;
+__device__ unsigned long long g_sig_key[SIG_TABLE];
+__device__ long long g_sig_rep[SIG_TABLE];
+__device__ double g_sig_val[SIG_TABLE];
+__device__ double g_sig_rho[SIG_TABLE];
+__device__ double g_sig_w[SIG_TABLE][4];     // weight of each run
+__device__ unsigned g_sig_ends[SIG_TABLE];   // cumulative run ends, 8 bits each
+
+__device__ __forceinline__ unsigned long long sig_mix(unsigned long long x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  return x;
+}
+
+// 64-bit profile key (bit 63 marks a key; 0 = none): up to 4 runs of 14 bits
+__device__ __forceinline__ unsigned long long row_key(const int* d, int c) {
+  unsigned long long key = 1ull << 63;
+  int runs = 0, i = 0;
+  while (i < c) {
+    const int di = d[i];
+    int j = i + 1;
+    while (j < c && d[j] == di) j++;
+    const int cnt = j - i;
+    if (runs == 4 || di < 0 || di > 255 || cnt > 63) return SIG_EMPTY;
+    key |= (unsigned long long)((di << 6) | cnt) << (14 * runs);
+    runs++;
+    i = j;
+  }
+  return key | ((unsigned long long)runs << 56);
+}
+
+__global__ void sig_clear() {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < SIG_TABLE; i += gridDim.x * blockDim.x)
+    g_sig_key[i] = SIG_EMPTY;
+}
+
+// pass 1 (thread per row): key -> table slot, kept in slot_out (-1: direct)
+__global__ void sig_keys(long long n, const long long* __restrict__ indptr,
+                         const int* __restrict__ dist, int kmax, int* __restrict__ slot_out) {
+  const int lane = threadIdx.x & 31;
+  for (long long base = (long long)blockIdx.x * blockDim.x + threadIdx.x - lane; base < n;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long v = base + lane;
+    unsigned long long key = SIG_EMPTY;
+    if (v < n) {
+      const long long lo = indptr[v];
+      const int c = (int)(indptr[v + 1] - lo);
+      if (c <= kmax) key = row_key(dist + lo, c);
+    }
+    // one table lookup per distinct key of the warp
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(grp) - 1;
+    int slot = -1;
+    if (lane == leader && key != SIG_EMPTY) {
+      unsigned h = (unsigned)sig_mix(key) & (SIG_TABLE - 1);
+      for (int probe = 0; probe < SIG_TABLE; probe++) {
+        unsigned long long cur = *(volatile unsigned long long*)&g_sig_key[h];
+        if (cur == SIG_EMPTY) {
+          cur = atomicCAS(&g_sig_key[h], SIG_EMPTY, key);
+          if (cur == SIG_EMPTY) {  // inserted: this row represents the profile
+            g_sig_rep[h] = v;
+            slot = (int)h;
             break;
           }
-          if (s > target) his = mid; else los = mid;
-          mid = (los + his) / 2.0;
         }
-        if (live) sigma = mid;
+        if (cur == key) {
+          slot = (int)h;
+          break;
+        }
+        h = (h + 1) & (SIG_TABLE - 1);
       }
     }
-    rho_out[v] = rho;
-    sigma_out[v] = sigma;
-    if (w_out)
-      for (int i = 0; i < c; i++) w_out[lo + i] = exp(-((double)r.d[i] - rho) / sigma);
+    slot = __shfl_sync(0xffffffffu, slot, leader);
+    if (v < n) slot_out[v] = slot;
+  }
+}
+
+// pass 2 (thread per table entry): sigma of each profile on its representative
+__global__ void sig_solve(const long long* __restrict__ indptr, const int* __restrict__ dist,
+                          int kmax, double target) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < SIG_TABLE; s += gridDim.x * blockDim.x) {
+    if (g_sig_key[s] == SIG_EMPTY) continue;
+    const long long v = g_sig_rep[s];
+    const long long lo = indptr[v];
+    double rho;
+    const int c = (int)(indptr[v + 1] - lo);
+    const double sigma = row_sigma(dist + lo, c, kmax, target, &rho);
+    g_sig_val[s] = sigma;
+    g_sig_rho[s] = rho;
+    // per-run weights: the same expression the per-entry path evaluates
+    const unsigned long long key = g_sig_key[s];
+    const int runs = (int)((key >> 56) & 7);
+    unsigned ends = 0;
+    int end = 0;
+    for (int j = 0; j < 4; j++) {
+      if (j < runs) {
+        const int dj = (int)((key >> (14 * j + 6)) & 255);
+        end += (int)((key >> (14 * j)) & 63);
+        g_sig_w[s][j] = exp(-((double)dj - rho) / sigma);
+      }
+      ends |= (unsigned)(j < runs ? end : 255) << (8 * j);
+    }
+    g_sig_ends[s] = ends;
+  }
+}
+
+// pass 3 (warp per 32 consecutive rows): lane l takes row base + l's rho and
+// sigma (table, or solved directly), then the warp writes the weights of the
+// 32 rows' entries coalesced, each entry finding its row among the lanes by
+// a shuffle search; w = exp(-(d - rho) / sigma) as in the reference
+__global__ void __launch_bounds__(128)
+    smooth_kernel(long long n, const long long* __restrict__ indptr, const int* __restrict__ dist,
+                  int kmax, double target, const int* __restrict__ slot_in,
+                  double* __restrict__ rho_out, double* __restrict__ sigma_out,
+                  double* __restrict__ w_out) {
+  const int lane = threadIdx.x & 31;
+  for (long long base = (long long)blockIdx.x * blockDim.x + threadIdx.x - lane; base < n;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long v = base + lane;
+    const bool valid = v < n;
+    const long long lo = valid ? indptr[v] : 0;
+    const long long hi = valid ? indptr[v + 1] : 0;
+    double rho = 0.0, sigma = 0.0;
+    const int slot = valid && slot_in ? slot_in[v] : -1;
+    if (valid) {
+      if (slot >= 0) {
+        rho = g_sig_rho[slot];
+        sigma = g_sig_val[slot];
+      } else {
+        sigma = row_sigma(dist + lo, (int)(hi - lo), kmax, target, &rho);
+      }
+      rho_out[v] = rho;
+      sigma_out[v] = sigma;
+    }
+    if (!w_out) continue;
+    const int nv = (int)min(32LL, n - base);  // valid lanes
+    const long long e0 = __shfl_sync(0xffffffffu, lo, 0);
+    const long long e1 = __shfl_sync(0xffffffffu, hi, nv - 1);
+    for (long long eb = e0; eb < e1; eb += 32) {
+      const long long e = eb + lane;
+      int l = 0;  // last lane whose row starts at or before e
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const long long s0 = __shfl_sync(0xffffffffu, lo, (l + step) & 31);
+        if (l + step < nv && s0 <= e) l += step;
+      }
+      const int r_slot = __shfl_sync(0xffffffffu, slot, l);
+      const long long r_lo = __shfl_sync(0xffffffffu, lo, l);
+      const double r_rho = __shfl_sync(0xffffffffu, rho, l);
+      const double r_sig = __shfl_sync(0xffffffffu, sigma, l);
+      if (e < e1) {
+        double w;
+        if (r_slot >= 0) {  // profiled row: its run's precomputed weight
+          const unsigned ends = g_sig_ends[r_slot];
+          const unsigned i = (unsigned)(e - r_lo);
+          const int j = (i >= (ends & 255u)) + (i >= ((ends >> 8) & 255u)) + (i >= ((ends >> 16) & 255u));
+          w = g_sig_w[r_slot][j];
+        } else {
+          w = exp(-((double)dist[e] - r_rho) / r_sig);
+        }
+        w_out[e] = w;
+      }
+    }
   }
 }
 
@@ -139,10 +308,39 @@ extern "C" int gu_smooth_knn(int64_t n, const int64_t* indptr, const int32_t* di
     return GU_ERR_ARG;
   }
   if (n == 0) return GU_OK;
+  cudaStream_t st = (cudaStream_t)stream;
   long long blocks = (n + 127) / 128;
   if (blocks > 148LL * 32) blocks = 148LL * 32;
-  smooth_kernel<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(
-      n, (const long long*)indptr, dist, kmax, target, rho, sigma, w);
+  // per-row table slots live in a stream-ordered scratch allocation; the
+  // device's default pool keeps its memory between calls (no OS round trip)
+  static int pool_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (pool_dev != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    pool_dev = dev;
+  }
+  int* slots = nullptr;
+  if (n >= 4096 && cudaMallocAsync((void**)&slots, sizeof(int) * (size_t)n, st) != cudaSuccess) {
+    cudaGetLastError();
+    slots = nullptr;  // no scratch: every row solved directly
+  }
+  if (slots) {
+    sig_clear<<<8, 256, 0, st>>>();
+    GU_CHECK_LAUNCH("sig_clear");
+    sig_keys<<<(unsigned)blocks, 128, 0, st>>>(n, (const long long*)indptr, dist, kmax, slots);
+    GU_CHECK_LAUNCH("sig_keys");
+    sig_solve<<<SIG_TABLE / 128, 128, 0, st>>>((const long long*)indptr, dist, kmax, target);
+    GU_CHECK_LAUNCH("sig_solve");
+  }
+  smooth_kernel<<<(unsigned)blocks, 128, 0, st>>>(n, (const long long*)indptr, dist, kmax, target,
+                                                  slots, rho, sigma, w);
   GU_CHECK_LAUNCH("smooth_kernel");
+  if (slots) GU_CHECK(cudaFreeAsync(slots, st));
   return GU_OK;
 }
