@@ -69,6 +69,17 @@ __global__ void fx_indeg(long long nnz, const int* __restrict__ dst, int* __rest
   }
 }
 
+// e / k for the entry indices of fixed-k rows: one multiply-high by
+// M = ceil(2^32 / k), exact for e < 2^32 / k (the host checks nnz against
+// that bound and passes M = 0 to fall back to the division)
+struct RowOf {
+  unsigned magic;
+  int k;
+  __device__ __forceinline__ int operator()(int e) const {
+    return magic ? (int)__umulhi((unsigned)e, magic) : e / k;
+  }
+};
+
 // one warp per vertex u: forward entries u*k .. u*k+k-1 (sorted by (id, i)
 // in registers) merged with the backward entries in_e[in_ptr[u] ..) whose
 // source rows are ascending; equal ids: forward first, each side in original
@@ -78,7 +89,7 @@ __global__ void fx_indeg(long long nnz, const int* __restrict__ dst, int* __rest
 // entry when no forward entry has that id -- gets h = (a + b) - a*b from the
 // key's first forward weight a and first backward weight b (0 when absent)
 // and the flag h != 0; every other entry of the key gets flag 0.
-__global__ void fx_merge(long long n, int kfix, long long nnz, const int* __restrict__ dst,
+__global__ void fx_merge(long long n, int kfix, RowOf row_of, long long nnz, const int* __restrict__ dst,
                          const double* __restrict__ w, const long long* __restrict__ in_ptr,
                          const int* __restrict__ in_e, int* __restrict__ other,
                          double* __restrict__ hval, int* __restrict__ rowcnt) {
@@ -106,7 +117,7 @@ __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __rest
     int kept = 0;                                      // this lane's kept keys
     // first backward chunk, one entry per lane (the whole list when m <= 32)
     const int e_first = lane < m ? in_e[ib + lane] : 0;
-    const int bid_first = lane < m ? e_first / kfix : INT_MAX;
+    const int bid_first = lane < m ? row_of(e_first) : INT_MAX;
     // forward element of rank `lane`: position lane + #backward with id < fid
     if (lane < kfix || m <= 32) {  // (warp-uniform shuffles when m <= 32)
       long long lo = 0;
@@ -120,7 +131,7 @@ __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __rest
         long long hi = m;
         while (lo < hi) {
           const long long mid = (lo + hi) >> 1;
-          if ((int)(in_e[ib + mid] / kfix) < fid) lo = mid + 1;
+          if (row_of(in_e[ib + mid]) < fid) lo = mid + 1;
           else hi = mid;
         }
       }
@@ -134,7 +145,7 @@ __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __rest
         double b = 0.0;
         if (lo < m) {
           const int e = m <= 32 ? e_lo : in_e[ib + lo];
-          if (e / kfix == fid) b = w[e];  // first backward entry of this id
+          if (row_of(e) == fid) b = w[e];  // first backward entry of this id
         }
         h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
         kept += h != 0.0;
@@ -152,7 +163,7 @@ __global__ void fx_merge(long long n, int kfix, long long nnz, const int* __rest
         bid = lane < m ? bid_first : 0;
       } else if (j < m) {
         e = in_e[ib + j];
-        bid = e / kfix;
+        bid = row_of(e);
       }
       // upper bound over the sorted forward ids (held one per lane)
       int cnt = 0;
@@ -404,7 +415,12 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
       if (r0) return r0;
       // merge + union per vertex (other endpoint and h per both-array slot,
       // kept count per vertex), scan of the counts = nbr_indptr, compaction
-      fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, nnz, dst, w, ws.pos, vbuf.Current(),
+      RowOf row_of;
+      row_of.k = kfix;
+      row_of.magic = (unsigned long long)nnz * (unsigned long long)kfix < (1ull << 32)
+                         ? (unsigned)(((1ull << 32) + kfix - 1) / kfix)
+                         : 0u;
+      fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, row_of, nnz, dst, w, ws.pos, vbuf.Current(),
                                                   ws.v0, ws.h, ws.rowcnt);
       GU_CHECK_LAUNCH("fx_merge");
       int r1 = scan_counts(ws.rowcnt, n, (long long*)nbr_indptr, ws.partial, st);
