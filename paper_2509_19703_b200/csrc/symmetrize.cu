@@ -11,6 +11,7 @@
 // is a and the first backward entry is b.  h = (a + b) - a*b rounded step by
 // step (explicit _rn intrinsics: no FMA), kept iff h != 0.
 #include <climits>
+#include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -190,6 +191,116 @@ __global__ void fx_merge(long long n, int kfix, RowOf row_of, long long nnz, con
     }
     kept = warp_sum(kept);
     if (lane == 0) rowcnt[u] = kept;
+  }
+}
+
+// fx_merge with two vertices per warp (k <= 16): lanes 0-15 take vertex
+// 2w, lanes 16-31 vertex 2w + 1.  Same per-vertex algorithm on 16 lanes: a
+// 16-wide bitonic sort of the forward row, in-rows of <= 16 entries held in
+// registers (longer ones searched in memory), backward entries 16 at a time
+// (the warp loops to the longer of its two in-rows).  Bit-identical output.
+__global__ void fx_merge16(long long n, int kfix, RowOf row_of, long long nnz,
+                           const int* __restrict__ dst, const double* __restrict__ w,
+                           const long long* __restrict__ in_ptr, const int* __restrict__ in_e,
+                           int* __restrict__ other, double* __restrict__ hval,
+                           int* __restrict__ rowcnt) {
+  const int lane = threadIdx.x & 31, hl = lane & 15, hb = lane & 16;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long u0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2; u0 < n;
+       u0 += 2 * nw) {
+    const long long u = u0 + (lane >> 4);
+    const bool valid = u < n;
+    const long long fb = u * kfix;
+    unsigned long long fk = (valid && hl < kfix)
+                                ? (((unsigned long long)(unsigned)dst[fb + hl] << 32) | (unsigned)hl)
+                                : ~0ull;
+    for (int size = 2; size <= 16; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(FULL_MASK, fk, stride);
+        const bool up = (hl & size) == 0;
+        const bool lower = (hl & stride) == 0;
+        fk = (up == lower) ? (o < fk ? o : fk) : (o > fk ? o : fk);
+      }
+    }
+    const int fid = (int)(fk >> 32);
+    const int fpos = (int)(unsigned)fk;
+    const int prev_fid = __shfl_up_sync(FULL_MASK, fid, 1);
+    const long long ib = valid ? in_ptr[u] : 0;
+    const int m = valid ? (int)(in_ptr[u + 1] - ib) : 0;
+    const long long out0 = fb + ib;
+    int kept = 0;
+    const int e_first = hl < m ? in_e[ib + hl] : 0;
+    const int bid_first = hl < m ? row_of(e_first) : INT_MAX;
+    // forward ranks: lower bound of fid among the backward ids
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int x = __shfl_sync(FULL_MASK, bid_first, hb + ((lo + step - 1) & 15));
+      if (lo + step - 1 < m && x < fid) lo += step;
+    }
+    const int e_lo = __shfl_sync(FULL_MASK, e_first, hb + (lo & 15));
+    if (valid && hl < kfix) {
+      if (m > 16) {  // long in-row: search it in memory
+        int a = 0, b = m;
+        while (a < b) {
+          const int mid = (a + b) >> 1;
+          if (row_of(in_e[ib + mid]) < fid) a = mid + 1;
+          else b = mid;
+        }
+        lo = a;
+      }
+      const long long o = out0 + hl + lo;
+      other[o] = fid;
+      double h = 0.0;
+      if (hl == 0 || prev_fid != fid) {
+        const double a = w[fb + fpos];
+        double b = 0.0;
+        if (lo < m) {
+          const int e = m <= 16 ? e_lo : in_e[ib + lo];
+          if (row_of(e) == fid) b = w[e];
+        }
+        h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
+        kept += h != 0.0;
+      }
+      hval[o] = h;
+    }
+    const int mloop = max(__shfl_sync(FULL_MASK, m, 0), __shfl_sync(FULL_MASK, m, 16));
+    int carry = -1;
+    for (int j0 = 0; j0 < mloop; j0 += 16) {
+      const int j = j0 + hl;
+      int e = 0, bid = 0;
+      if (j0 == 0) {
+        e = e_first;
+        bid = hl < m ? bid_first : 0;
+      } else if (j < m) {
+        e = in_e[ib + j];
+        bid = row_of(e);
+      }
+      int cnt = 0;
+      bool in_fwd = false;
+      for (int q = 0; q < kfix; q++) {
+        const int x = __shfl_sync(FULL_MASK, fid, hb + q);
+        cnt += x <= bid;
+        in_fwd |= x == bid;
+      }
+      const int up = __shfl_up_sync(FULL_MASK, bid, 1);
+      const int prev = hl == 0 ? carry : up;
+      carry = __shfl_sync(FULL_MASK, bid, hb + 15);
+      if (j < m) {
+        const long long o = out0 + j + cnt;
+        other[o] = bid;
+        double h = 0.0;
+        if (!in_fwd && prev != bid) {
+          const double a = 0.0, b = w[e];
+          h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
+          kept += h != 0.0;
+        }
+        hval[o] = h;
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) kept += __shfl_xor_sync(FULL_MASK, kept, o);
+    if (valid && hl == 0) rowcnt[u] = kept;
   }
 }
 
@@ -420,8 +531,16 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
       row_of.magic = (unsigned long long)nnz * (unsigned long long)kfix < (1ull << 32)
                          ? (unsigned)(((1ull << 32) + kfix - 1) / kfix)
                          : 0u;
-      fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, row_of, nnz, dst, w, ws.pos, vbuf.Current(),
-                                                  ws.v0, ws.h, ws.rowcnt);
+      static const bool merge16 = [] {
+        const char* v = getenv("GU_SYM_MERGE16");
+        return !(v && v[0] == '0');
+      }();
+      if (kfix <= 16 && merge16)
+        fx_merge16<<<grid_for(n * 16), 256, 0, st>>>(n, kfix, row_of, nnz, dst, w, ws.pos,
+                                                      vbuf.Current(), ws.v0, ws.h, ws.rowcnt);
+      else
+        fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, row_of, nnz, dst, w, ws.pos,
+                                                    vbuf.Current(), ws.v0, ws.h, ws.rowcnt);
       GU_CHECK_LAUNCH("fx_merge");
       int r1 = scan_counts(ws.rowcnt, n, (long long*)nbr_indptr, ws.partial, st);
       if (r1) return r1;
