@@ -390,6 +390,38 @@ __global__ void check_rows_fixed(const long long* __restrict__ indptr, long long
     if (indptr[r + 1] - indptr[r] != kfix) *bad = 1;
 }
 
+// fx_compact with two vertices per warp (half-warp each, 16 entries a step)
+__global__ void fx_compact16(long long n, int kfix, const long long* __restrict__ in_ptr,
+                             const int* __restrict__ other, const double* __restrict__ hval,
+                             const long long* __restrict__ out_ptr, int* __restrict__ sym_src,
+                             int* __restrict__ sym_dst, double* __restrict__ sym_w) {
+  const int lane = threadIdx.x & 31, hl = lane & 15, hb = lane & 16;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long u0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2; u0 < n;
+       u0 += 2 * nw) {
+    const long long u = u0 + (lane >> 4);
+    const bool valid = u < n;
+    const long long ib = valid ? in_ptr[u] : 0;
+    const long long seg = u * kfix + ib;
+    const int len = valid ? kfix + (int)(in_ptr[u + 1] - ib) : 0;
+    long long o = valid ? out_ptr[u] : 0;
+    const int lmax = max(__shfl_sync(FULL_MASK, len, 0), __shfl_sync(FULL_MASK, len, 16));
+    for (int j0 = 0; j0 < lmax; j0 += 16) {
+      const int j = j0 + hl;
+      const double h = j < len ? hval[seg + j] : 0.0;
+      const bool keep = h != 0.0;
+      const unsigned bal = (__ballot_sync(FULL_MASK, keep) >> hb) & 0xffffu;
+      if (keep) {
+        const long long q = o + __popc(bal & ((1u << hl) - 1u));
+        sym_src[q] = (int)u;
+        sym_dst[q] = other[seg + j];
+        sym_w[q] = h;
+      }
+      o += __popc(bal);
+    }
+  }
+}
+
 unsigned grid_for(long long items);
 
 bool rows_fixed(const int64_t* indptr, long long n, int kfix, long long* scratch, cudaStream_t st) {
@@ -544,9 +576,14 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
       GU_CHECK_LAUNCH("fx_merge");
       int r1 = scan_counts(ws.rowcnt, n, (long long*)nbr_indptr, ws.partial, st);
       if (r1) return r1;
-      fx_compact<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, ws.pos, ws.v0, ws.h,
-                                                    (const long long*)nbr_indptr, sym_src, sym_dst,
-                                                    sym_w);
+      if (kfix <= 16 && merge16)
+        fx_compact16<<<grid_for(n * 16), 256, 0, st>>>(n, kfix, ws.pos, ws.v0, ws.h,
+                                                        (const long long*)nbr_indptr, sym_src,
+                                                        sym_dst, sym_w);
+      else
+        fx_compact<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, ws.pos, ws.v0, ws.h,
+                                                      (const long long*)nbr_indptr, sym_src,
+                                                      sym_dst, sym_w);
       GU_CHECK_LAUNCH("fx_compact");
       long long E = 0;
       GU_CHECK(cudaMemcpyAsync(&E, nbr_indptr + n, sizeof(long long), cudaMemcpyDeviceToHost, st));
