@@ -5,10 +5,12 @@ Every BFS source is independent and its RNG stream is per source
 ``spawn_key=(v,)``), so splitting the source range across ranks reproduces
 the single-GPU records bit for bit.  One process per GPU, the graph CSR
 replicated in each GPU's HBM; each rank computes the fixed-size records
-(k neighbour ids, k distances, count) of its contiguous source range straight
-into padded per-rank buffers, and ``all_gather`` of those buffers (NCCL over
-NVLink/NVSwitch on B200s, gloo in the CPU tests) hands every rank the full kNN
-lists for C1 -- no packing copies on the data path.  C2 (SGD) stays on one
+(k neighbour ids, k distances, count) of its sources straight into record
+buffers, and ``all_gather`` of those buffers (NCCL over NVLink/NVSwitch on
+B200s, gloo in the CPU tests) hands every rank the full kNN lists for C1 --
+no packing copies on the data path.  ``exchange_records`` interleaves the
+source blocks over a few rounds so each round's gather overlaps the next
+round's compute and still lands in source order.  C2 (SGD) stays on one
 GPU.
 
 The buffer / gather code below is backend-agnostic torch, so the exchange is
@@ -64,6 +66,57 @@ def gather_shards(bufs, n, group=None, k=None):
     return tuple(out)
 
 
+def chunk_rows(n, world, chunks, align=1):
+    """Rows per (rank, chunk) of the interleaved source layout: chunk c of
+    rank r covers sources [(c*world + r)*ch, (c*world + r + 1)*ch) clipped to
+    n, ch a multiple of ``align`` (64 = one bitset word)."""
+    per = -(-n // (world * chunks))
+    return max(align, -(-per // align) * align)
+
+
+def exchange_records(compute, n, k, device, group=None, chunks=4, align=1):
+    """Source-sharded records of all n sources on every rank, the exchange
+    overlapped with the compute.
+
+    The sources are split into ``chunks`` rounds of ``world`` blocks; round c
+    gives rank r the block (c*world + r).  ``compute(b, e, out)`` writes the
+    records of sources [b, e) into ``out`` = (nbr [e-b, k], dist [e-b, k],
+    cnt [e-b]) on the current stream; each round's blocks are then
+    all-gathered asynchronously (``async_op``: the collective waits for the
+    round's records on its own stream) while the next round computes.  A
+    round's gather lands as one contiguous row block of the result, because
+    the round's blocks are consecutive in source order: no permutation copy.
+    Distances travel as uint8 when k <= 255 (hop distances never exceed k).
+    Returns (nbr [n, k], dist [n, k], cnt [n])."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ch = chunk_rows(n, world, chunks, align)
+    total = world * chunks * ch
+    narrow = k <= 255
+    nbr_full = torch.empty((total, k), dtype=torch.int32, device=device)
+    dist_full = torch.empty((total, k), dtype=torch.uint8 if narrow else torch.int32, device=device)
+    cnt_full = torch.empty(total, dtype=torch.int32, device=device)
+    works, keep = [], []
+    for c in range(chunks):
+        b = (c * world + rank) * ch
+        e = min(b + ch, n)
+        ns = max(0, e - b)
+        nbr_c = torch.empty((ch, k), dtype=torch.int32, device=device)
+        dist_c = torch.empty((ch, k), dtype=torch.int32, device=device)
+        cnt_c = torch.zeros(ch, dtype=torch.int32, device=device)
+        if ns:
+            compute(b, e, (nbr_c[:ns], dist_c[:ns], cnt_c[:ns]))
+        send_d = dist_c.to(torch.uint8) if narrow else dist_c
+        lo, hi = c * world * ch, (c + 1) * world * ch
+        for full, send in ((nbr_full, nbr_c), (dist_full, send_d), (cnt_full, cnt_c)):
+            works.append(dist.all_gather_into_tensor(full[lo:hi], send, group=group, async_op=True))
+        keep.append((nbr_c, send_d, cnt_c))  # alive until the gathers finish
+    for w in works:
+        w.wait()
+    d = dist_full[:n]
+    return nbr_full[:n], (d.to(torch.int32) if narrow else d), cnt_full[:n]
+
+
 def sharded_knn(g, k, seed=0, mode="partial", group=None):
     """kNN lists of every vertex, sources sharded over the process group.
 
@@ -79,20 +132,26 @@ def sharded_knn(g, k, seed=0, mode="partial", group=None):
     csr = device_csr(g, dev)
     if mode == "partial":
         k_eff = min(k, n - 1) if n > 1 else 0
-        begin, end, per = shard_range(n, rank, world, align=1)
     elif mode == "full":
         k_eff = k
-        begin, end, per = shard_range(n, rank, world, align=64)
     else:
         raise ValueError(f"unknown mode {mode!r}")
-    bufs = shard_buffers(per, max(k_eff, 1), dev)
-    ns = end - begin
-    out = (bufs[0][:ns], bufs[1][:ns], bufs[2][:ns])
+    kk = max(k_eff, 1)
     if mode == "partial":
-        partial_bfs_records(csr, k_eff, seed, begin, end, out=out)
+        from .device import workspace
+        from .neighbors import _tier2_warps
+        from . import _lib
+        tw = _tier2_warps(n)
+        ch = chunk_rows(n, world, 4, 1)
+        ws = workspace(_lib.load().gu_partial_bfs_workspace_size(n, ch, tw), dev)
+
+        def compute(b, e, out):
+            partial_bfs_records(csr, k_eff, seed, b, e, out=out, tier2_warps=tw, ws=ws)
     else:
-        full_knn_records(csr, k_eff, seed, begin, end, out=out)
-    nbr, dd, cnt = gather_shards(bufs, n, group, k=max(k_eff, 1))
+        def compute(b, e, out):
+            full_knn_records(csr, k_eff, seed, b, e, out=out)
+    nbr, dd, cnt = exchange_records(compute, n, kk, dev, group, chunks=4,
+                                    align=1 if mode == "partial" else 64)
     short = int((cnt < k_eff).sum().item()) if n else 0
     if rank == 0:
         _warn_short(short)
