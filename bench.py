@@ -302,8 +302,9 @@ def run_ours(args):
                      "traffic": traffic, "peak_source": peak_kind,
                      "kernel": "gu_partial_bfs_knn (tier F pbfs_fast<8>, 98% of the call)",
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)},
-        # per step: tier F, tiers 1a / 1b, slot clear, tier 2 (NCCL kernels not counted)
-        "gpu_launches": 5 * args.steps,
+        # per step: tier F, tiers 1a / 1b, slot clear, tier 2 -- once, or once
+        # per exchange round at N > 1 (NCCL and dtype-cast kernels not counted)
+        "gpu_launches": 5 * args.steps * (4 if ws > 1 else 1),
         "clocks": clk.summary(),
         "fixture_gen_s": round(gen_s, 2),
     }
