@@ -164,6 +164,45 @@ def test_smooth_cases_golden(gu):
         assert np.array_equal(gk.nbr_indptr, split(z["nbr_indptr"], z["nbr_indptr_off"], i))
 
 
+def test_smooth_memo_profiles_vs_oracle(gu, oracle):
+    """The memoised-sigma path (n >= 4096): rows keyed by run-length profile,
+    rows that do not fit a key (> 4 runs, distance > 255, run > 63 long) and
+    short rows, mixed in one call -- rho / sigma bit-exact, weights and the
+    union as in the oracle."""
+    rng = np.random.default_rng(11)
+    n, k = 6000, 15
+    rows_d, rows_j = [], []
+    for v in range(n):
+        kind = v % 5
+        if kind == 0:    # the common kNN shape: two hop levels, full row
+            t0 = int(rng.integers(1, k))
+            d = [1] * t0 + [2] * (k - t0)
+        elif kind == 1:  # short row, three levels
+            c = int(rng.integers(1, k))
+            d = sorted(int(x) for x in rng.integers(1, 4, size=c))
+        elif kind == 2:  # > 4 runs: solved directly
+            d = sorted(int(x) for x in rng.integers(1, 9, size=k))
+        elif kind == 3:  # large distances (> 255): solved directly
+            d = sorted(int(x) for x in rng.integers(200, 400, size=k))
+        else:            # all equal (sigma clamps to 1e3)
+            d = [3] * k
+        ids = rng.choice(np.setdiff1d(np.arange(n), [v]), size=len(d), replace=False)
+        # rows sorted by (distance, id), as the kNN producers emit them
+        order = np.lexsort((ids, np.array(d)))
+        rows_d.append(np.array(d, dtype=np.int32)[order])
+        rows_j.append(ids[order].astype(np.int32))
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum([len(r) for r in rows_d])
+    dist = np.concatenate(rows_d)
+    dst = np.concatenate(rows_j)
+    knn = gu.DirectedKnn(n=n, k=k, indptr=indptr, dst=dst, dist=dist)
+    gk = gu.smooth_knn_weights(knn)
+    o = oracle.smooth_knn_weights(n, indptr, dst, dist, k)
+    assert np.array_equal(gk.rho, o["rho"]) and np.array_equal(gk.sigma, o["sigma"])
+    assert np.array_equal(gk.sym_src, o["sym_src"]) and np.array_equal(gk.sym_dst, o["sym_dst"])
+    assert _ulps(gk.sym_w, o["sym_w"]).max(initial=0) <= WEIGHT_ULPS
+
+
 def test_smooth_rejects_empty_row(gu):
     knn = gu.DirectedKnn(n=2, k=1, indptr=np.array([0, 1, 1]), dst=np.array([1], np.int32),
                          dist=np.array([1], np.int32))
