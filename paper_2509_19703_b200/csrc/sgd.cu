@@ -205,8 +205,12 @@ __device__ __forceinline__ bool filt_maybe(const FiltWord& f, int c) {
 
 constexpr int SGD_WARPS = 8;  // 256 threads per block at most (block_for)
 
-template <int LANES>
-__global__ void __launch_bounds__(256, SGD_MIN_BLOCKS)
+// MINB: CTAs per SM the register budget is sized for -- 4 (64 registers) for
+// GPU-filling epochs, 2 (96 registers) for the small-cap 16-lane mode, whose
+// few resident warps are latency-bound and gain from the longer register
+// budget (c3 epoch 0.295 -> 0.276 ms; at 96 registers c5 would lose 8%)
+template <int LANES, int MINB>
+__global__ void __launch_bounds__(256, MINB)
     sgd_epoch_kernel(int n, long long E, float2* __restrict__ xy, const int4* __restrict__ edges,
                      const int* __restrict__ nip, const int* __restrict__ nix,
                      const FiltWord* __restrict__ filt, float a, float b, float lr, int epoch,
@@ -515,12 +519,12 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
     }();
     int lanes = 32;
     if (concurrency > 0 && concurrency < resident && min_lanes == 16 &&
-        (concurrency * 32) / 16 <= resident)
+        (concurrency * 32) / 16 <= 148LL * 2 * 256)  // fits the 2-CTA/SM kernel
       lanes = 16;
     const long long threads = concurrency > 0 ? (concurrency * 32 + lanes - 1) / lanes : 0;
     const unsigned bs = block_for(threads);
     const unsigned gs = bs < 256 ? 1u : grid_for((items * 32 + lanes - 1) / lanes, threads);
-    auto kern = lanes == 32 ? sgd_epoch_kernel<32> : sgd_epoch_kernel<16>;
+    auto kern = lanes == 32 ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS> : sgd_epoch_kernel<16, 2>;
     kern<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr,
                             nbr_indices, (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, items,
                             start, windowed, seed, diverged);
