@@ -211,19 +211,18 @@ __global__ void fx_merge16(long long n, int kfix, RowOf row_of, long long nnz,
     const long long u = u0 + (lane >> 4);
     const bool valid = u < n;
     const long long fb = u * kfix;
-    unsigned long long fk = (valid && hl < kfix)
-                                ? (((unsigned long long)(unsigned)dst[fb + hl] << 32) | (unsigned)hl)
-                                : ~0ull;
+    // 32-bit sort key (id << 4 | position): ids < 2^27 (host check), k <= 16
+    unsigned fk = (valid && hl < kfix) ? (((unsigned)dst[fb + hl] << 4) | (unsigned)hl) : ~0u;
     for (int size = 2; size <= 16; size <<= 1) {
       for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        const unsigned long long o = __shfl_xor_sync(FULL_MASK, fk, stride);
+        const unsigned o = __shfl_xor_sync(FULL_MASK, fk, stride);
         const bool up = (hl & size) == 0;
         const bool lower = (hl & stride) == 0;
-        fk = (up == lower) ? (o < fk ? o : fk) : (o > fk ? o : fk);
+        fk = (up == lower) ? min(o, fk) : max(o, fk);
       }
     }
-    const int fid = (int)(fk >> 32);
-    const int fpos = (int)(unsigned)fk;
+    const int fid = fk == ~0u ? -1 : (int)(fk >> 4);
+    const int fpos = (int)(fk & 15u);
     const int prev_fid = __shfl_up_sync(FULL_MASK, fid, 1);
     const long long ib = valid ? in_ptr[u] : 0;
     const int m = valid ? (int)(in_ptr[u + 1] - ib) : 0;
@@ -567,7 +566,7 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
         const char* v = getenv("GU_SYM_MERGE16");
         return !(v && v[0] == '0');
       }();
-      if (kfix <= 16 && merge16)
+      if (kfix <= 16 && merge16 && n < (1LL << 27))
         fx_merge16<<<grid_for(n * 16), 256, 0, st>>>(n, kfix, row_of, nnz, dst, w, ws.pos,
                                                       vbuf.Current(), ws.v0, ws.h, ws.rowcnt);
       else
