@@ -376,7 +376,7 @@ def partial_bfs(g, k, seed=0):
         # small first chunks, so the row copies start early; the indptr of
         # the all-rows-full outcome goes down during the first kernel and is
         # used when no row turns out short
-        bounds = sorted({0, n // 16, n // 4, n // 2, (3 * n) // 4, n})
+        bounds = sorted({0, n // 16, n // 4, n // 2, (3 * n) // 4, (15 * n) // 16, n})
         ip_full = torch.arange(0, (n + 1) * kk, kk, dtype=torch.int64, device=dev)
         prefetch.copy_extra("indptr", ip_full)
     else:
