@@ -203,6 +203,31 @@ def test_smooth_memo_profiles_vs_oracle(gu, oracle):
     assert _ulps(gk.sym_w, o["sym_w"]).max(initial=0) <= WEIGHT_ULPS
 
 
+def test_smooth_memo_table_overflow_vs_oracle(gu, oracle):
+    """More distinct distance profiles than the 8192-entry table: rows that
+    find it full are solved directly -- still bit-exact."""
+    rng = np.random.default_rng(12)
+    n, k = 20000, 15
+    rows_d = []
+    for v in range(n):
+        cuts = np.sort(rng.choice(np.arange(1, k), size=3, replace=False))
+        levels = np.sort(rng.choice(np.arange(1, 250), size=4, replace=False))
+        d = np.repeat(levels, np.diff(np.concatenate([[0], cuts, [k]])))
+        rows_d.append(d.astype(np.int32))
+    dist = np.concatenate(rows_d)
+    dst = np.concatenate([rng.choice(np.setdiff1d(np.arange(n), [v]), size=k, replace=False)
+                          for v in range(n)]).astype(np.int32)
+    # rows sorted by (distance, id)
+    for v in range(n):
+        sl = slice(v * k, (v + 1) * k)
+        o = np.lexsort((dst[sl], dist[sl]))
+        dst[sl], dist[sl] = dst[sl][o], dist[sl][o]
+    indptr = (k * np.arange(n + 1)).astype(np.int64)
+    gk = gu.smooth_knn_weights(gu.DirectedKnn(n=n, k=k, indptr=indptr, dst=dst, dist=dist))
+    rho, sigma = oracle.smooth_rho_sigma(indptr, dist, k)
+    assert np.array_equal(gk.rho, rho) and np.array_equal(gk.sigma, sigma)
+
+
 def test_smooth_rejects_empty_row(gu):
     knn = gu.DirectedKnn(n=2, k=1, indptr=np.array([0, 1, 1]), dst=np.array([1], np.int32),
                          dist=np.array([1], np.int32))
