@@ -301,7 +301,10 @@ def run_ours(args):
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "peak_source": peak_kind,
                      "kernel": "gu_partial_bfs_knn (tier F pbfs_fast<8>, 98% of the call)",
-                     "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)},
+                     "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4),
+                     "limiter": "issue + dependent latency, not HBM: ~640 warp instructions per "
+                                "source at 69% of peak issue, ~4 dependent memory round trips per "
+                                "source, DRAM at 18% of peak (profiles/r01_ncu_fast4.txt, DESIGN.md K3)"},
         # per step: tier F, tiers 1a / 1b, slot clear, tier 2 -- once, or once
         # per exchange round at N > 1 (NCCL and dtype-cast kernels not counted)
         "gpu_launches": 5 * args.steps * (4 if ws > 1 else 1),
@@ -425,7 +428,10 @@ def _sgd_bench(gu, g, args, dev, peak):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": _profile_traffic("sgd_epoch_kernel"),
-                         "alg_bytes_per_update": 88},
+                         "alg_bytes_per_update": 88,
+                         "limiter": "per-visit dependent chain (record -> endpoints and filter -> "
+                                    "row test) at 48% occupancy (64 registers); 49% long-scoreboard "
+                                    "stalls (profiles/r01_ncu_sgd.txt, DESIGN.md K7)"},
             "diverged": int(div.item()) != INT32_MAX}
 
 
