@@ -163,3 +163,24 @@ def test_shard_ranges_cover_sources():
                 assert len(pers) == 1
                 if n < 5000:
                     assert got == list(range(n))
+
+
+def test_exchange_rounds_cover_sources_in_order():
+    """The interleaved rounds of distributed.exchange_records: block
+    (c*world + r) of ch rows for rank r in round c covers every source once,
+    and a round's gathered blocks are consecutive in source order."""
+    from paper_2509_19703_b200.distributed import chunk_rows
+
+    for n in (1, 7, 64, 1000, 4099):
+        for world in (1, 2, 3, 8):
+            for chunks in (1, 3, 4):
+                for align in (1, 64):
+                    ch = chunk_rows(n, world, chunks, align)
+                    assert ch % align == 0 and world * chunks * ch >= n
+                    seen = []
+                    for c in range(chunks):
+                        # all_gather order: rank 0..world-1 of this round
+                        for r in range(world):
+                            b = (c * world + r) * ch
+                            seen.extend(range(b, min(b + ch, n)))
+                    assert seen == list(range(n))
