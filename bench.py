@@ -3,6 +3,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1)
 
+Without a launcher, --gpus N > 1 re-executes itself under
+torch.distributed.run with N ranks; under a launcher WORLD_SIZE must equal
+--gpus.  --cpu-dry-run rehearses the N-rank record exchange on CPU (gloo).
+
 Workload (BASELINE.json configs[4], the scaling-sweep config): partial-BFS
 kNN, k = 15, on a random geometric graph in the unit square, n = 4,000,000,
 radius for average degree 12, seed 4, largest component (3,999,956
@@ -153,6 +157,19 @@ def _dist_env():
     return ws, rank, local
 
 
+def bench_config(n, m, te, ws):
+    """The workload description both arms print, key for key (the driver
+    compares the two arms' config objects)."""
+    per = -(-n // ws)
+    return {"workload": WORKLOAD, "n": n, "m": int(m), "k": K_NN, "seed": SEED,
+            "sources_per_rank": per, "te_per_step": int(te),
+            "l2": "CSR 208 MB > 126 MB L2; L2 flushed before every timed step (256 MB write, "
+                  "then a 256 MB read that writes the dirty lines back outside the step)",
+            "parallelism": f"sources sharded over {ws} GPU(s)"
+            + (", records all-gathered over NCCL in 4 rounds overlapped with the kernels"
+               if ws > 1 else "")}
+
+
 def build_graph(name="c5"):
     from paper_2509_19703_b200 import fixtures
     t = time.time()
@@ -291,12 +308,7 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "int32",
         "data": "synthetic (seeded RGG fixture, paper datasets absent)",
-        "config": {"workload": WORKLOAD, "n": n, "m": int(g.m), "k": K_NN, "seed": SEED,
-                   "sources_per_rank": per, "te_per_step": te_tot,
-                   "l2": "CSR 208 MB > 126 MB L2; L2 flushed before every timed step (256 MB write, then a 256 MB read that writes the dirty lines back outside the step)",
-                   "parallelism": f"sources sharded over {ws} GPU(s)"
-                   + (", records all-gathered over NCCL in 4 rounds overlapped with the kernels"
-                      if ws > 1 else "")},
+        "config": bench_config(n, g.m, te_tot, ws),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "peak_source": peak_kind,
@@ -618,17 +630,33 @@ def _next_rows(gu, g5):
         out["error"] = repr(exc)
     return out
 
-def _cpu_full_pass(O, g, thr):
-    """One pass of the oracle's C port over every source of the c5 graph:
-    (seconds, TE)."""
+def _cpu_full_pass(O, g, thr, src_end=None):
+    """One pass of the oracle's C port over sources [0, src_end) of the c5
+    graph (all of them by default): (seconds, TE)."""
+    end = g.n if src_end is None else src_end
     t0 = time.perf_counter()
-    _, _, _, sc, _ = O.partial_bfs_raw(g, K_NN, SEED, 0, g.n, nthreads=thr, work=True)
+    _, _, _, sc, _ = O.partial_bfs_raw(g, K_NN, SEED, 0, end, nthreads=thr, work=True)
     return time.perf_counter() - t0, int(sc.sum())
+
+
+def _single_core(O, g, min_seconds=4.0):
+    """The reference is single-threaded numba (_kernels.py:59-60, no prange;
+    BASELINE.md 2 plans 1 core): the same port on ONE host thread, over the
+    first quarter of the c5 sources, repeated to >= min_seconds."""
+    end = g.n // 4
+    tot, te, passes = 0.0, 0, 0
+    while tot < min_seconds or passes < 1:
+        dt, t = _cpu_full_pass(O, g, 1, end)
+        tot, te, passes = tot + dt, te + t, passes + 1
+    return {"value": round(te / tot / 1e9, 5), "unit": "GTEPS", "cores": 1, "kind": "port",
+            "sample": f"sources 0..{end - 1} of c5 ({te // passes} adjacency entries) x {passes} "
+                      "passes on one thread", "seconds": round(tot, 3)}
 
 
 def _cpu_baseline(g, min_seconds=10.0, max_passes=40):
     """The whole c5 workload on the host cores, repeated until >= min_seconds
-    of CPU work (the full workload is ~0.5 s on 16 threads, so no sampling)."""
+    of CPU work (the full workload is ~0.5 s on 16 threads, so no sampling),
+    plus the one-thread figure of the single-threaded reference."""
     from oracle import oracle as O
     O.build()
     thr = O.max_threads()
@@ -639,16 +667,21 @@ def _cpu_baseline(g, min_seconds=10.0, max_passes=40):
     return {"value": round(te / tot / 1e9, 5), "unit": "GTEPS", "cores": thr, "kind": "port",
             "sample": f"full c5 workload (all {g.n} sources, {te // passes} adjacency entries) x "
                       f"{passes} passes, oracle/oracle.c partial_bfs_all restatement",
-            "seconds": round(tot, 3)}
+            "seconds": round(tot, 3), "single_core": _single_core(O, g)}
 
 
 # ---------------------------------------------------------- reference arm
 def run_reference(args):
-    """The reference algorithm's CPU implementation (oracle C port, all host
-    threads); one step = the full c5 workload, same metric as ours."""
+    """The reference algorithm's CPU implementation (the oracle's C port of
+    _kernels.py:60-131, all host threads); one step = the full c5 workload,
+    same metric, unit and config as our arm.  No GPU is touched: CUDA is
+    hidden before torch can be imported, so the fixture's largest-component
+    pass takes the host path and libgumap.so is never loaded."""
+    os.environ["CUDA_VISIBLE_DEVICES"] = ""
     ws, rank, local = _dist_env()
     if rank != 0:
         return
+    n_gpus = max(ws, args.gpus)
     from oracle import oracle as O
     O.build()
     g, _ = build_graph("c5")
@@ -663,17 +696,84 @@ def run_reference(args):
     tot = sum(ts)
     v = te / tot / 1e9
     out = {"impl": "reference", "metric": "BFS-kNN GTEPS (partial BFS kNN, k=15)",
-           "value": round(v, 5), "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
+           "value": round(v, 5), "unit": "GTEPS", "n_gpus": n_gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
            "dtype": "int32", "data": "synthetic (seeded RGG fixture, paper datasets absent)",
-           "config": {"workload": WORKLOAD, "n": g.n, "te_per_step": te // args.steps},
+           "config": bench_config(g.n, g.m, te // args.steps, n_gpus),
            "cpu_baseline": {"value": round(v, 5), "unit": "GTEPS", "cores": thr, "kind": "port",
                             "sample": f"full c5 workload (all {g.n} sources) per step, "
-                                      "oracle/oracle.c partial_bfs_all restatement"},
+                                      "oracle/oracle.c partial_bfs_all restatement",
+                            "single_core": _single_core(O, g)},
            "e2e": {"value": round(v, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------- N-rank launch
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _spawn_ranks(args):
+    """`python bench.py --gpus N` without a torchrun launcher: re-exec this
+    script under torch.distributed.run with N ranks (one per GPU) on
+    127.0.0.1 and return its exit code; rank 0 prints the JSON line.  NCCL
+    prints its communicator-init lines (NCCL_DEBUG=INFO, subsystem INIT) so
+    the N-rank communicator is visible in the log."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def run_cpu_dry_run(args):
+    """CPU rehearsal of the N-rank path (gloo; no GPU): each rank fills its
+    interleaved source rounds with the oracle's records (the GPU kernels'
+    stand-in) through distributed.exchange_records -- the same exchange the
+    GPU step runs -- and the gathered records must equal the one-process
+    oracle result bit for bit.  Rank 0 prints a JSON line with n_gpus."""
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, _ = _dist_env()
+    dist.init_process_group("gloo")
+    from oracle import oracle as O
+    from paper_2509_19703_b200 import fixtures as F
+    from paper_2509_19703_b200.distributed import exchange_records
+
+    g = F.scale_free(20000, seed=7, m0=3)
+
+    def compute(b, e, out):
+        nbr, dd, cnt = O.partial_bfs_raw(g, K_NN, SEED, b, e, nthreads=2)
+        out[0].copy_(torch.from_numpy(nbr.reshape(-1, K_NN)))
+        out[1].copy_(torch.from_numpy(dd.reshape(-1, K_NN)))
+        out[2].copy_(torch.from_numpy(cnt))
+
+    t0 = time.perf_counter()
+    nbr, dd, cnt = exchange_records(compute, g.n, K_NN, torch.device("cpu"), chunks=4)
+    dt = time.perf_counter() - t0
+    on, od, oc = O.partial_bfs_raw(g, K_NN, SEED, nthreads=2)
+    same = (np.array_equal(nbr.numpy().reshape(-1), on) and np.array_equal(dd.numpy().reshape(-1), od)
+            and np.array_equal(cnt.numpy(), oc))
+    flags = torch.tensor([int(same)])
+    dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps({"metric": "cpu dry run of the N-rank record exchange", "n_gpus": ws,
+                          "world_size": dist.get_world_size(), "backend": "gloo",
+                          "records_identical": bool(flags.item()), "n": g.n,
+                          "seconds": round(dt, 3)}), flush=True)
+    dist.destroy_process_group()
+    if not flags.item():
+        sys.exit(1)
 
 
 def main():
@@ -686,11 +786,27 @@ def main():
     ap.add_argument("--skip-layout", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-next", action="store_true")
+    ap.add_argument("--cpu-dry-run", action="store_true",
+                    help="rehearse the N-rank exchange on CPU (gloo, oracle records)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.impl == "reference":
         run_reference(args)
+        return
+    launched = "WORLD_SIZE" in os.environ
+    if not launched and args.gpus > 1:
+        sys.exit(_spawn_ranks(args))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
+    if args.cpu_dry_run:
+        run_cpu_dry_run(args)
     else:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         run_ours(args)
 
 

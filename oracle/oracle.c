@@ -17,6 +17,8 @@
  *   or_full_knn           apsp row + knn_select_row fused per source (no n x n)
  *   or_smooth_rows        neighbors.py:261-311 (rho / sigma bisection, numpy
  *                                               pairwise row sums, libm exp)
+ *   or_fuzzy_union        neighbors.py:320-350 (dedupe, h = (a+b) - a*b over both
+ *                                               orientations, zeros dropped, (src,dst))
  *   or_sgd_sweep          _kernels.py:158-223  (sequential float64 SGD, logs the
  *                                               accepted negatives and thetas)
  *   or_sgd_replay         same arithmetic, negatives / thetas supplied
@@ -597,6 +599,167 @@ void or_smooth_rows(int64_t n, const int64_t *indptr, const int32_t *dist,
   smooth_ctx x = {indptr, dist, kmax, target, rho_out, sigma_out, w_out};
   parallel_for(nthreads, 0, n, 1024, sizeof(double) * (size_t)(2 * kmax + 2),
                smooth_range, &x);
+}
+
+/* ------------------------------------------------------- fuzzy union (C1) */
+/* neighbors.py:320-350 (and fuzzy_union, 240-242): dedupe each directed row
+ * keeping the first occurrence of a destination, then over the union of both
+ * orientations h = (a + b) - a*b (a missing orientation counts as 0), exact
+ * zeros dropped, keys in (src, dst) order.  Same arithmetic as scipy's
+ * w + w.T - w.multiply(w.T) (each entry one add, one multiply, one subtract;
+ * -ffp-contract=off), restated per vertex: a row-local sort of the forward
+ * row by destination, a counting-sort transpose (in-lists come out in source
+ * order) and a merge of the two sorted lists.  oracle.py's numpy
+ * fuzzy_union_symmetrize is the slower restatement it is pinned against. */
+typedef struct {
+  int64_t n;
+  const int64_t *indptr;
+  const int32_t *dst;
+  const double *w;
+  int64_t *fptr;   /* deduped forward rows, sorted by destination */
+  int32_t *fdst;
+  double *fw;
+  int64_t *iptr;   /* in-lists (transpose), sorted by source */
+  int32_t *isrc;
+  double *iw;
+  int64_t *optr;   /* output offsets */
+  int32_t *osrc, *odst;
+  double *ow;
+} fu_ctx;
+
+typedef struct {
+  int32_t id;
+  int64_t pos;
+} fu_pair;
+
+static int fu_cmp(const void *a, const void *b) {
+  const fu_pair *x = (const fu_pair *)a, *y = (const fu_pair *)b;
+  if (x->id != y->id) return x->id < y->id ? -1 : 1;
+  return x->pos < y->pos ? -1 : (x->pos > y->pos);
+}
+
+/* pass 1: per-row sort + dedupe into a scratch row; count kept entries */
+static void fu_rows(void *c, int64_t vb, int64_t ve, void *scratch) {
+  fu_ctx *x = (fu_ctx *)c;
+  (void)scratch;
+  for (int64_t v = vb; v < ve; v++) {
+    int64_t lo = x->indptr[v], cnt = x->indptr[v + 1] - lo;
+    fu_pair *p = (fu_pair *)malloc(sizeof(fu_pair) * (size_t)(cnt > 0 ? cnt : 1));
+    for (int64_t i = 0; i < cnt; i++) {
+      p[i].id = x->dst[lo + i];
+      p[i].pos = lo + i;
+    }
+    qsort(p, (size_t)cnt, sizeof(fu_pair), fu_cmp);
+    int64_t o = lo, kept = 0;
+    for (int64_t i = 0; i < cnt; i++) {
+      if (i > 0 && p[i].id == p[i - 1].id) continue; /* keep the first */
+      x->fdst[o + kept] = p[i].id;
+      x->fw[o + kept] = x->w[p[i].pos];
+      kept++;
+    }
+    x->fptr[v] = kept; /* count; turned into the row length below */
+    free(p);
+  }
+}
+
+static int64_t fu_merge_row(const fu_ctx *x, int64_t v, int write) {
+  int64_t a0 = x->indptr[v], an = a0 + x->fptr[v];
+  int64_t b0 = x->iptr[v], bn = x->iptr[v + 1];
+  int64_t o = write ? x->optr[v] : 0, kept = 0;
+  while (a0 < an || b0 < bn) {
+    int32_t id;
+    double a = 0.0, b = 0.0;
+    if (b0 >= bn || (a0 < an && x->fdst[a0] < x->isrc[b0])) {
+      id = x->fdst[a0];
+      a = x->fw[a0++];
+    } else if (a0 >= an || x->isrc[b0] < x->fdst[a0]) {
+      id = x->isrc[b0];
+      b = x->iw[b0++];
+    } else {
+      id = x->fdst[a0];
+      a = x->fw[a0++];
+      b = x->iw[b0++];
+    }
+    double s = a + b;
+    double pr = a * b;
+    double h = s - pr;
+    if (h != 0.0) {
+      if (write) {
+        x->osrc[o + kept] = (int32_t)v;
+        x->odst[o + kept] = id;
+        x->ow[o + kept] = h;
+      }
+      kept++;
+    }
+  }
+  return kept;
+}
+
+static void fu_count(void *c, int64_t vb, int64_t ve, void *scratch) {
+  fu_ctx *x = (fu_ctx *)c;
+  (void)scratch;
+  for (int64_t v = vb; v < ve; v++) x->optr[v + 1] = fu_merge_row(x, v, 0);
+}
+
+static void fu_write(void *c, int64_t vb, int64_t ve, void *scratch) {
+  fu_ctx *x = (fu_ctx *)c;
+  (void)scratch;
+  for (int64_t v = vb; v < ve; v++) fu_merge_row(x, v, 1);
+}
+
+/* Returns E (the number of symmetrised directed edges).  Call twice: with
+ * osrc == NULL to size, then with outputs of E entries (nbr_indptr n+1).
+ * The scratch arrays are rebuilt on each call (oracle: simplicity first). */
+int64_t or_fuzzy_union(int64_t n, const int64_t *indptr, const int32_t *dst,
+                       const double *w, int32_t *osrc, int32_t *odst, double *ow,
+                       int64_t *nbr_indptr, int nthreads) {
+  int64_t nnz = indptr[n];
+  fu_ctx x;
+  memset(&x, 0, sizeof(x));
+  x.n = n;
+  x.indptr = indptr;
+  x.dst = dst;
+  x.w = w;
+  x.fptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  x.fdst = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nnz + 1));
+  x.fw = (double *)malloc(sizeof(double) * (size_t)(nnz + 1));
+  parallel_for(nthreads, 0, n, 4096, 0, fu_rows, &x);
+  /* transpose: in-list of d gets (v, w) for every kept forward (v, d) */
+  x.iptr = (int64_t *)calloc((size_t)n + 2, sizeof(int64_t));
+  for (int64_t v = 0; v < n; v++)
+    for (int64_t i = indptr[v]; i < indptr[v] + x.fptr[v]; i++) x.iptr[x.fdst[i] + 1]++;
+  for (int64_t v = 0; v < n; v++) x.iptr[v + 1] += x.iptr[v];
+  x.isrc = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nnz + 1));
+  x.iw = (double *)malloc(sizeof(double) * (size_t)(nnz + 1));
+  int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  memcpy(fill, x.iptr, sizeof(int64_t) * (size_t)(n + 1));
+  for (int64_t v = 0; v < n; v++) /* v ascending: in-lists in source order */
+    for (int64_t i = indptr[v]; i < indptr[v] + x.fptr[v]; i++) {
+      int64_t d = x.fdst[i];
+      x.isrc[fill[d]] = (int32_t)v;
+      x.iw[fill[d]] = x.fw[i];
+      fill[d]++;
+    }
+  free(fill);
+  x.optr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  parallel_for(nthreads, 0, n, 4096, 0, fu_count, &x);
+  for (int64_t v = 0; v < n; v++) x.optr[v + 1] += x.optr[v];
+  int64_t E = x.optr[n];
+  if (osrc) {
+    x.osrc = osrc;
+    x.odst = odst;
+    x.ow = ow;
+    parallel_for(nthreads, 0, n, 4096, 0, fu_write, &x);
+    if (nbr_indptr) memcpy(nbr_indptr, x.optr, sizeof(int64_t) * (size_t)(n + 1));
+  }
+  free(x.fptr);
+  free(x.fdst);
+  free(x.fw);
+  free(x.iptr);
+  free(x.isrc);
+  free(x.iw);
+  free(x.optr);
+  return E;
 }
 
 /* ------------------------------------------------------------------- SGD */

@@ -61,6 +61,9 @@ def lib():
                                    _i32p, _f64p]
         L.or_sgd_replay.argtypes = [_f64p, _i32p, _i32p, _f64p, _i64p, i64, _i32p,
                                     _f64p, f64, f64, f64, i32]
+        L.or_fuzzy_union.argtypes = [i64, _i64p, _i32p, _f64p, _i32p, _i32p, _f64p,
+                                     _i64p, cint]
+        L.or_fuzzy_union.restype = i64
         L.or_max_threads.restype = cint
         _lib = L
     return _lib
@@ -230,11 +233,35 @@ def fuzzy_union_symmetrize(n, indptr, dst, w):
     return src, dstc, h.astype(np.float64), nbr_indptr, dstc.copy()
 
 
-def smooth_knn_weights(n, indptr, dst, dist, k, nthreads=1):
-    """neighbors.py:245-350 -> dict of the KnnGraph arrays."""
+def fuzzy_union_c(n, indptr, dst, w, nthreads=None):
+    """neighbors.py:320-350 in C (oracle.c or_fuzzy_union): the same result as
+    fuzzy_union_symmetrize (pinned against it in tests/test_oracle.py), in
+    O(nnz) per-vertex merges instead of global numpy sorts -- what makes the
+    full-size C1 parity tests (c4, c5) affordable."""
+    ip = np.ascontiguousarray(indptr, np.int64)
+    dd = np.ascontiguousarray(dst, np.int32)
+    ww = np.ascontiguousarray(w, np.float64)
+    nt = max_threads() if nthreads is None else nthreads
+    E = lib().or_fuzzy_union(n, _p(ip, _i64p), _p(dd, _i32p), _p(ww, _f64p), None, None,
+                             None, None, nt)
+    src = np.empty(E, np.int32)
+    dstc = np.empty(E, np.int32)
+    h = np.empty(E, np.float64)
+    nip = np.empty(n + 1, np.int64)
+    lib().or_fuzzy_union(n, _p(ip, _i64p), _p(dd, _i32p), _p(ww, _f64p), _p(src, _i32p),
+                         _p(dstc, _i32p), _p(h, _f64p), _p(nip, _i64p), nt)
+    return src, dstc, h, nip, dstc.copy()
+
+
+def smooth_knn_weights(n, indptr, dst, dist, k, nthreads=1, union="numpy"):
+    """neighbors.py:245-350 -> dict of the KnnGraph arrays.  union="c" takes
+    the C restatement of the fuzzy union (same arrays, much faster)."""
     rho, sigma = smooth_rho_sigma(indptr, dist, k, nthreads)
     w = directed_weights(indptr, dist, rho, sigma)
-    s, d, h, nip, nix = fuzzy_union_symmetrize(n, indptr, dst, w)
+    if union == "c":
+        s, d, h, nip, nix = fuzzy_union_c(n, indptr, dst, w, nthreads)
+    else:
+        s, d, h, nip, nix = fuzzy_union_symmetrize(n, indptr, dst, w)
     return dict(rho=rho, sigma=sigma, w=w, sym_src=s, sym_dst=d, sym_w=h,
                 nbr_indptr=nip, nbr_indices=nix)
 

@@ -57,7 +57,7 @@ def gen_partial_small():
     rng = np.random.default_rng(101)
     edges_l, n_l, k_l, seed_l, ip_l, dst_l, dist_l = [], [], [], [], [], [], []
     graphs = []
-    for trial in range(40):
+    for trial in range(100):  # all 100 graphs of criterion 1
         n, e = F.random_connected_graph(rng, n_max=200)
         k = int(rng.integers(1, 21))
         graphs.append((np.array(e, np.int64), k, trial))

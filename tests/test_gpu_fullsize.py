@@ -1,0 +1,123 @@
+"""Full-size parity on the BASELINE configs: every row, no sampling.
+
+C0 partial BFS-kNN (c3, c4, c5): every source's (nbr, dist, count) record and
+the packed DirectedKnn of the public ``partial_bfs`` against the oracle's
+restatement of ``_kernels.py:60-131`` over all sources; the per-tier source
+counts are recorded so the run shows which tiers the configs exercise.
+C0 full BFS-kNN (c2): all 20,000 rows of ``knn_from_full_distances`` against
+``neighbors.py:183-237`` restated (oracle.full_knn).
+C1 (c4, c5): rho / sigma / sym_src / sym_dst / nbr_indptr bit-exact and sym_w
+within WEIGHT_ULPS of ``neighbors.py:245-350`` restated (oracle
+smooth_knn_weights, C fuzzy union pinned in test_oracle.py).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+WEIGHT_ULPS = 4  # device exp vs numpy's SIMD exp, per weight (as test_gpu_parity.py)
+SEEDS = {"c3": 2, "c4": 3, "c5": 4}
+
+
+@pytest.fixture(scope="module")
+def gu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2509_19703_b200 as gu
+    return gu
+
+
+_graphs = {}
+
+
+def _graph(gu, name):
+    if name not in _graphs:
+        _graphs.clear()  # keep one large graph alive at a time
+        _graphs[name] = gu.config_graph(name)
+    return _graphs[name]
+
+
+def _records_with_tiers(g, k, seed):
+    """partial_bfs_records on all sources, plus the per-tier source counts
+    (gu_partial_bfs_overflow_counts: fell to tier 1a, 1b, 2)."""
+    from paper_2509_19703_b200 import _lib
+    from paper_2509_19703_b200.device import device_csr, workspace
+    from paper_2509_19703_b200.neighbors import _tier2_warps, partial_bfs_records
+
+    csr = device_csr(g)
+    t2 = _tier2_warps(g.n)
+    lib = _lib.load()
+    ws = workspace(lib.gu_partial_bfs_workspace_size(g.n, g.n, t2), csr.device)
+    nbr, dist, cnt = partial_bfs_records(csr, k, seed, 0, g.n, tier2_warps=t2, ws=ws)
+    tiers = (ctypes.c_int32 * 3)()
+    assert lib.gu_partial_bfs_overflow_counts(ctypes.c_void_p(ws.data_ptr()), g.n, tiers) == 0
+    return (nbr.cpu().numpy().reshape(-1), dist.cpu().numpy().reshape(-1), cnt.cpu().numpy(),
+            tuple(int(x) for x in tiers))
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_partial_bfs_every_row_vs_oracle(gu, oracle, name):
+    g = _graph(gu, name)
+    seed = SEEDS[name]
+    nb, dd, cnt, tiers = _records_with_tiers(g, 15, seed)
+    o_n, o_d, o_c = oracle.partial_bfs_raw(g, 15, seed, nthreads=oracle.max_threads())
+    print(f"{name}: n={g.n} sources per tier: F={g.n - tiers[0]} 1a={tiers[0] - tiers[1]} "
+          f"1b={tiers[1] - tiers[2]} 2={tiers[2]}")
+    assert np.array_equal(cnt, o_c)
+    assert np.array_equal(nb, o_n)
+    assert np.array_equal(dd, o_d)
+    if name == "c3":  # BA hubs: the big-ball tiers run at this size
+        assert tiers[1] > 0 and tiers[2] > 0
+    assert tiers[0] > 0  # tier F overflow reaches the lean warp tier on every config
+    # the public API (host path: chunked copies, uint8 distances widened on
+    # the host, packed CSR) returns the same rows
+    _, knn = gu.partial_bfs(g, 15, seed=seed)
+    ip, dst, dist = oracle._pack(g.n, 15, o_n, o_d, o_c)
+    assert np.array_equal(knn.indptr, ip)
+    assert np.array_equal(knn.dst, dst)
+    assert np.array_equal(knn.dist, dist)
+
+
+def test_full_knn_c2_every_row_vs_oracle(gu, oracle):
+    g = _graph(gu, "c2")
+    knn = gu.knn_from_full_distances(gu.all_pairs_bfs(g), 15, seed=1)
+    ip, dst, dist = oracle.full_knn(g, 15, seed=1, nthreads=oracle.max_threads())
+    assert knn.indptr.shape[0] == g.n + 1
+    assert np.array_equal(knn.indptr, ip)
+    assert np.array_equal(knn.dst, dst)
+    assert np.array_equal(knn.dist, dist)
+
+
+def _ulps(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a.view(np.int64) - b.view(np.int64))
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_c1_every_row_vs_oracle(gu, oracle, name):
+    g = _graph(gu, name)
+    seed = SEEDS[name]
+    o_n, o_d, o_c = oracle.partial_bfs_raw(g, 15, seed, nthreads=oracle.max_threads())
+    ip, dst, dist = oracle._pack(g.n, 15, o_n, o_d, o_c)
+    o = oracle.smooth_knn_weights(g.n, ip, dst, dist, 15, nthreads=oracle.max_threads(),
+                                  union="c")
+    del o_n, o_d
+    _, knn = gu.partial_bfs(g, 15, seed=seed)
+    assert np.array_equal(knn.dst, dst)
+    gk = gu.smooth_knn_weights(knn)
+    assert np.array_equal(gk.rho, o["rho"])
+    assert np.array_equal(gk.sigma, o["sigma"])
+    assert gk.edge_count == o["sym_src"].shape[0]
+    assert np.array_equal(gk.sym_src, o["sym_src"])
+    assert np.array_equal(gk.sym_dst, o["sym_dst"])
+    assert np.array_equal(gk.nbr_indptr, o["nbr_indptr"])
+    assert np.array_equal(gk.nbr_indices, o["nbr_indices"])
+    u = _ulps(gk.sym_w, o["sym_w"])
+    print(f"{name}: E={gk.edge_count} sym_w max ulps {int(u.max())}, "
+          f"{int(np.count_nonzero(u))} weights differ")
+    assert u.max() <= WEIGHT_ULPS

@@ -79,30 +79,7 @@ def test_partial_bfs_all_tiers_and_large_k(gu, oracle):
         assert np.array_equal(knn.dist, dist)
 
 
-@pytest.mark.parametrize("name", ["c4", "c5"])
-def test_partial_bfs_scale_sample_vs_oracle(gu, oracle, name):
-    """BASELINE c4 / c5 at full size: a 20k-source sample bit-exact vs the
-    oracle, plus size-independent properties over every row."""
-    import torch
-    from paper_2509_19703_b200.device import device_csr
-    from paper_2509_19703_b200.neighbors import partial_bfs_records
-
-    g = gu.config_graph(name)
-    csr = device_csr(g)
-    nbr, dist, cnt = partial_bfs_records(csr, 15, 4, 0, g.n)
-    cnt_h = cnt.cpu().numpy()
-    assert np.all(cnt_h == 15)
-    nb, dd = nbr.cpu().numpy(), dist.cpu().numpy()
-    # rows sorted by (dist, id), no self, distances >= 1
-    key = dd.astype(np.int64) * g.n + nb
-    assert np.all(np.diff(key, axis=1) > 0)
-    assert np.all(nb != np.arange(g.n)[:, None])
-    assert np.all(dd >= 1)
-    rng = np.random.default_rng(0)
-    for s0 in rng.choice(g.n - 2000, size=10, replace=False):
-        o_n, o_d, o_c = oracle.partial_bfs_raw(g, 15, 4, int(s0), int(s0) + 2000, nthreads=8)
-        assert np.array_equal(nb[s0:s0 + 2000].reshape(-1), o_n)
-        assert np.array_equal(dd[s0:s0 + 2000].reshape(-1), o_d)
+# c3 / c4 / c5 every row: tests/test_gpu_fullsize.py
 
 
 # --------------------------------------------------------------- C0 full
@@ -137,14 +114,7 @@ def test_c1_full_path_bitexact(gu):
     assert sha(dset.matrix) == str(z["apsp_sha"])
 
 
-def test_c2_full_knn_vs_oracle(gu, oracle):
-    """SS-GUMAP c2 stand-in (G' of ER(20000, 200)): fused BFS-kNN vs oracle."""
-    g = gu.config_graph("c2")
-    knn = gu.knn_from_full_distances(gu.all_pairs_bfs(g), 15, seed=1)
-    dst, dist, cnt = oracle.full_knn(g, 15, seed=1, src_begin=0, src_end=4000, nthreads=8,
-                                     packed=False)
-    assert np.array_equal(knn.dst[: 4000 * 15], dst)
-    assert np.array_equal(knn.dist[: 4000 * 15], dist)
+# c2 every row: tests/test_gpu_fullsize.py
 
 
 # --------------------------------------------------------------------- C1

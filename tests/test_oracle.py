@@ -128,3 +128,38 @@ def test_c3_scale_free_pipeline(oracle):
         if it == 1:
             assert np.array_equal(c[z["sample"]], z["after2_sample"])
     assert sha(c) == str(z["after3_sha"])
+
+
+def test_fuzzy_union_c_matches_numpy_restatement(oracle):
+    """oracle.c or_fuzzy_union (used by the full-size C1 parity tests) gives
+    the same arrays as the numpy restatement pinned above: the golden smooth
+    cases, c1, and random rows with duplicates, unsorted ids, exact-zero
+    weights and one-sided pairs."""
+    z = load_golden("smooth_cases.npz")
+    for i in range(z["n"].shape[0]):
+        n, k = int(z["n"][i]), int(z["k"][i])
+        ip = split(z["indptr"], z["indptr_off"], i)
+        dst = split(z["dst"], z["dst_off"], i)
+        dist = split(z["dist"], z["dist_off"], i)
+        a = oracle.smooth_knn_weights(n, ip, dst, dist, k)
+        b = oracle.smooth_knn_weights(n, ip, dst, dist, k, union="c")
+        for key in ("sym_src", "sym_dst", "sym_w", "nbr_indptr", "nbr_indices"):
+            assert np.array_equal(a[key], b[key]), (i, key)
+    z = load_golden("c1.npz")
+    o = oracle.smooth_knn_weights(2500, z["knn_indptr"], z["knn_dst"], z["knn_dist"], 15,
+                                  union="c")
+    for key in ("sym_src", "sym_dst", "sym_w", "nbr_indptr", "nbr_indices"):
+        assert np.array_equal(o[key], z[key]), key
+    rng = np.random.default_rng(5)
+    for trial in range(20):
+        n = int(rng.integers(2, 300))
+        counts = rng.integers(0, 12, size=n)
+        ip = np.zeros(n + 1, np.int64)
+        ip[1:] = np.cumsum(counts)
+        dst = rng.integers(0, n, size=int(ip[-1])).astype(np.int32)
+        w = rng.random(int(ip[-1]))
+        w[rng.random(w.shape[0]) < 0.2] = 0.0
+        a = oracle.fuzzy_union_symmetrize(n, ip, dst, w)
+        b = oracle.fuzzy_union_c(n, ip, dst, w, nthreads=2)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), trial
