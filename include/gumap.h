@@ -152,6 +152,21 @@ int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4
                   float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
                   int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
                   int64_t concurrency, int32_t* diverged, void* stream);
+/* Opt-in deterministic epochs (sequential by default, parallel
+ * modes only statistically reproducible -- this mode restores bitwise
+ * repeatability, acceptance criterion 9).  Same visits, draws and update
+ * rule as gu_sgd_epochs, run in batches of `batch` visits: a batch reads
+ * the positions as they stood when it started and adds its deltas as
+ * 2^-32 fixed-point integers into acc (int64[2n], zero on entry, zero on
+ * return), applied after the batch -- integer sums do not depend on the
+ * order the atomics land in.  Replaces the same _run_sgd loop as
+ * gu_sgd_epochs (layout.py:314-360). */
+int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_xy, const void* edges_int4,
+                                const int32_t* nbr_indptr, const int32_t* nbr_indices,
+                                const void* nbr_filter, float a, float b, float lr0, int32_t t,
+                                int32_t epoch_begin, int32_t epoch_end, int32_t n_neg,
+                                int64_t window, int32_t windowed, uint64_t seed, int64_t batch,
+                                int64_t* acc, int32_t* diverged, void* stream);
 /* positions visited by epoch `epoch` (visit_log): window/permutation indices
  * into the prepared edge array, length window (windowed) or E (full). */
 int gu_sgd_visit_order(int64_t E, int32_t epoch, int64_t window, int32_t windowed,

@@ -90,6 +90,10 @@ SIGNATURES = {
     "gu_sgd_epochs": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _c_f32, _c_f32,
                                      _c_f32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i64, _c_i32,
                                      _c_u64, _c_i64, _vp, _vp]),
+    "gu_sgd_epochs_deterministic": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp,
+                                                   _c_f32, _c_f32, _c_f32, _c_i32, _c_i32, _c_i32,
+                                                   _c_i32, _c_i64, _c_i32, _c_u64, _c_i64, _vp,
+                                                   _vp, _vp]),
     "gu_sgd_visit_order": (ctypes.c_int, [_c_i64, _c_i32, _c_i64, _c_i32, _c_u64, _vp, _vp]),
     "gu_replay_schedule": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _c_i32, _vp,
                                           _vp, ctypes.POINTER(_c_i64)]),

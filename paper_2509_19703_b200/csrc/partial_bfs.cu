@@ -329,14 +329,22 @@ constexpr int TF_CAP2 = 160;  // level-2 ids kept per source
 #define TF_HC 512  // hash slots per source (ball budget 3/4 of it)
 #endif
 
-__device__ unsigned long long g_magic[4097];
+// M_d = ceil(2^64 / d), 2 <= d <= 4096, for the table remainder: a constant
+// initialiser in the image (no upload, no host-side state)
+struct MagicTab {
+  unsigned long long v[4097];
+  constexpr MagicTab() : v() {
+    for (int d = 2; d <= 4096; d++) v[d] = ~0ull / (unsigned long long)d + 1ull;
+  }
+};
+__device__ const MagicTab g_magic = MagicTab();
 
 // 64-bit remainder by a small divisor (1 <= d <= 4096): q = mulhi(x, M_d) with
 // M_d = ceil(2^64 / d) is floor(x / d) or one more (Granlund-Montgomery), so a
 // single conditional correction gives the exact x % d.
 __device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
   if (d == 1) return 0;
-  const unsigned long long q = __umul64hi(x, g_magic[d]);
+  const unsigned long long q = __umul64hi(x, __ldg(&g_magic.v[d]));
   unsigned long long r = x - q * (unsigned long long)d;
   if (r > x) r += (unsigned long long)d;  // q was one too large
   return (int)r;
@@ -747,31 +755,15 @@ size_t pbfs_ws_layout(long long n, long long nsrc, int slots, char* base, PbfsWs
   return off;
 }
 
-// M_d = ceil(2^64 / d) for the table remainder (uploaded once per device)
-cudaError_t ensure_magic() {
-  static int ready_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (ready_dev == dev) return cudaSuccess;
-  static unsigned long long host_magic[4097];
-  host_magic[0] = host_magic[1] = 0;
-  for (int d = 2; d <= 4096; d++) host_magic[d] = ~0ull / (unsigned long long)d + 1ull;
-  cudaError_t e = cudaMemcpyToSymbol(g_magic, host_magic, sizeof(host_magic));
-  if (e == cudaSuccess) ready_dev = dev;
-  return e;
-}
-
 constexpr int TF_WARPS = 8;
 
 cudaError_t launch_fast(int sms, const int* indptr, const int* indices, int k,
                         unsigned long long seed, long long src_begin, long long nsrc,
                         int* out_nbr, int* out_dist, int* out_count, int* ovf_out, int* ovf_cnt,
                         unsigned long long* work, cudaStream_t st) {
-  cudaError_t e = ensure_magic();
-  if (e != cudaSuccess) return e;
   auto kern = pbfs_fast<TF_WARPS>;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TF_WARPS * 32, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TF_WARPS * 32, 0);
   if (e != cudaSuccess) return e;
   long long blocks = (nsrc + TF_WARPS - 1) / TF_WARPS;
   long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1) * 8;

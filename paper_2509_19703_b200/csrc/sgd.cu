@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(256, MINB)
                      const int* __restrict__ nip, const int* __restrict__ nix,
                      const FiltWord* __restrict__ filt, float a, float b, float lr, int epoch,
                      int n_neg, long long items, long long start, int windowed,
-                     unsigned long long seed, int* __restrict__ diverged) {
+                     unsigned long long seed, int* __restrict__ diverged,
+                     long long ibase = 0, long long* __restrict__ acc = nullptr) {
   constexpr int lanes = LANES;
   // (candidate, row begin, row end, owner lane * 8 + slot) of the warp's
   // filter hits, and each lane's bitmask of slots found to be neighbours
@@ -238,7 +239,21 @@ __global__ void __launch_bounds__(256, MINB)
   // evaluated lane-parallel for the next 32 steps and handed out by shuffle
   unsigned tile_batch = 0;
   int step = 0;
-  for (long long i0 = gwarp * lanes; i0 < items; i0 += stride, step = (step + 1) & 31) {
+  // deterministic mode (acc != nullptr): visits [ibase, items) read the
+  // positions as they stood at the start of this batch and push their deltas
+  // as 2^-32 fixed-point integers (order-free sums: bitwise reproducible);
+  // det_apply_kernel adds them after the batch
+  auto push = [&](int w, float dx, float dy) {
+    if (acc) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * (long long)w),
+                (unsigned long long)__float2ll_rn(dx * 4294967296.0f));
+      atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * (long long)w + 1),
+                (unsigned long long)__float2ll_rn(dy * 4294967296.0f));
+    } else {
+      atomicAdd(&xy[w], make_float2(dx, dy));
+    }
+  };
+  for (long long i0 = ibase + gwarp * lanes; i0 < items; i0 += stride, step = (step + 1) & 31) {
     const long long i = i0 + lane;
     bool act = lane < lanes && i < items;
     long long p = 0;
@@ -278,7 +293,7 @@ __global__ void __launch_bounds__(256, MINB)
         duy += gy;
         xu.x += gx;
         xu.y += gy;
-        atomicAdd(&xy[v], make_float2(-gx, -gy));
+        push(v, -gx, -gy);
         if (!isfinite(xv.x - gx) || !isfinite(xv.y - gy)) bad = true;
       }
     }
@@ -404,11 +419,27 @@ __global__ void __launch_bounds__(256, MINB)
       }
     }
     if (act) {
-      if (dux != 0.f || duy != 0.f) atomicAdd(&xy[u], make_float2(dux, duy));
+      if (dux != 0.f || duy != 0.f) push(u, dux, duy);
       if (!isfinite(xu.x) || !isfinite(xu.y)) bad = true;
     }
   }
   if (bad) atomicMin(diverged, epoch);
+}
+
+// deterministic mode: x += acc * 2^-32, acc = 0, finiteness check
+__global__ void det_apply_kernel(int n, float2* __restrict__ xy, long long* __restrict__ acc,
+                                 int epoch, int* __restrict__ diverged) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const long long ax = acc[2 * (long long)v], ay = acc[2 * (long long)v + 1];
+    if (ax == 0 && ay == 0) continue;
+    float2 x = xy[v];
+    x.x += (float)((double)ax * 2.3283064365386963e-10);
+    x.y += (float)((double)ay * 2.3283064365386963e-10);
+    xy[v] = x;
+    acc[2 * (long long)v] = 0;
+    acc[2 * (long long)v + 1] = 0;
+    if (!isfinite(x.x) || !isfinite(x.y)) atomicMin(diverged, epoch);
+  }
 }
 
 __global__ void visit_order_kernel(long long E, int epoch, long long items, long long start,
@@ -527,8 +558,46 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
     auto kern = lanes == 32 ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS> : sgd_epoch_kernel<16, 2>;
     kern<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr,
                             nbr_indices, (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, items,
-                            start, windowed, seed, diverged);
+                            start, windowed, seed, diverged, 0LL, nullptr);
     GU_CHECK_LAUNCH("sgd_epoch_kernel");
+  }
+  return GU_OK;
+}
+
+extern "C" int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_xy,
+                                           const void* edges_int4, const int32_t* nbr_indptr,
+                                           const int32_t* nbr_indices, const void* nbr_filter,
+                                           float a, float b, float lr0, int32_t t,
+                                           int32_t epoch_begin, int32_t epoch_end, int32_t n_neg,
+                                           int64_t window, int32_t windowed, uint64_t seed,
+                                           int64_t batch, int64_t* acc, int32_t* diverged,
+                                           void* stream) {
+  if (n <= 0 || n >= INT_MAX || E < 0 || t < 0 || epoch_begin < 0 || epoch_end > t ||
+      batch < 32 || !acc || (windowed && (window < 1 || window > E))) {
+    set_error("gu_sgd_epochs_deterministic: bad arguments");
+    return GU_ERR_ARG;
+  }
+  if (E == 0) return GU_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  batch = (batch / 32) * 32;  // warp steps never straddle a tile boundary
+  for (int e = epoch_begin; e < epoch_end; e++) {
+    const float lr = (float)((double)lr0 * (1.0 - (double)e / (double)t));
+    long long items, start;
+    epoch_range(E, e, window, windowed, &items, &start);
+    for (long long b0 = 0; b0 < items; b0 += batch) {
+      const long long b1 = b0 + batch < items ? b0 + batch : items;
+      const long long threads = b1 - b0;
+      const unsigned bs = block_for(threads);
+      const unsigned gs = bs < 256 ? 1u : grid_for(threads, threads);
+      sgd_epoch_kernel<32, SGD_MIN_BLOCKS><<<gs, bs, 0, st>>>(
+          (int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr, nbr_indices,
+          (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, b1, start, windowed, seed, diverged,
+          b0, (long long*)acc);
+      GU_CHECK_LAUNCH("sgd_epoch_kernel(deterministic)");
+      det_apply_kernel<<<grid_for(n), 256, 0, st>>>((int)n, (float2*)coords_xy,
+                                                    (long long*)acc, e, diverged);
+      GU_CHECK_LAUNCH("det_apply_kernel");
+    }
   }
   return GU_OK;
 }

@@ -114,6 +114,23 @@ class SparseDistanceSet(_LazyArrays):
     def dist(self):
         return self._get_host("dist")
 
+    def run_bfs(self, k, seed=0):
+        """Run the BFS of a lazy full set now, for a later
+        ``knn_from_full_distances(self, k, seed)``: the fused bitset BFS with
+        its per-source k-th-distance selection, records kept on the device.
+        The drivers call it inside the C0 bracket (reference layout.py:418-420
+        times all_pairs_bfs as C0), so C1 is the packing, the weights and the
+        union, as in the reference."""
+        g = self._graph
+        if not self.full or g is None or k < 1:
+            return
+        dev = require_cuda()
+        recs = full_knn_records(device_csr(g, dev), k, seed, 0, self.n)
+        self.__dict__.setdefault("_knn_records", {})[(int(k), int(seed))] = recs
+
+    def _take_records(self, k, seed):
+        return self.__dict__.get("_knn_records", {}).pop((int(k), int(seed)), None)
+
     def row(self, v):
         """(neighbor ids, hop distances) for vertex ``v``, excluding ``v``."""
         if self.full:
@@ -526,7 +543,10 @@ def knn_from_full_distances(dist_set, k, seed=0):
     dev = require_cuda()
     n = int(dist_set.n)
     g = getattr(dist_set, "_graph", None)
-    if g is not None:
+    recs = dist_set._take_records(k, seed) if isinstance(dist_set, SparseDistanceSet) else None
+    if recs is not None:  # the BFS already ran (SparseDistanceSet.run_bfs)
+        nbr, dist, cnt = recs
+    elif g is not None:
         csr = device_csr(g, dev)
         nbr, dist, cnt = full_knn_records(csr, k, seed, 0, n)
     else:
