@@ -105,9 +105,14 @@ size_t gu_pack_records_workspace_size(int64_t nrows);
  * Replaces neighbors.py:261-318: rho = row min, sigma by the reference's
  * 64-step bisection on [1e-3, 1e3] (tol 1e-5, numpy pairwise row sums over
  * rows padded to kmax, non-converged rows take the next midpoint), weights
- * w = exp(-(d - rho) / sigma).  target = np.log2(k) computed by the caller. */
+ * w = exp(-(d - rho) / sigma).  target = np.log2(k) computed by the caller.
+ * workspace: gu_smooth_knn_workspace_size(n) bytes (0 below 4096 rows), the
+ * memoised-sigma profile table and per-row slots of this call alone: calls
+ * on different streams are independent. */
+size_t gu_smooth_knn_workspace_size(int64_t n);
 int gu_smooth_knn(int64_t n, const int64_t* indptr, const int32_t* dist, int32_t kmax,
-                  double target, double* rho, double* sigma, double* w, void* stream);
+                  double target, double* rho, double* sigma, double* w, void* workspace,
+                  size_t ws_bytes, void* stream);
 
 /* ----------------------------------------------- C1 fuzzy-union symmetrise
  * Replaces neighbors.py:320-350 (dedupe first occurrence, w + w^T - w o w^T
@@ -141,13 +146,18 @@ int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* 
  * nbr_filter (nullable): per-vertex 64-bit Bloom words of the neighbour ids
  * (2 hash bits per id) from gu_sgd_neighbor_filter (8 bytes x n); a negative
  * with a clear bit skips the row search (exact: a hit still searches). */
+/* Edge-record layout for a concurrency cap: 32 bytes (the record carries
+ * its head's 128-bit neighbour Bloom word; GPU-filling epochs) or 16 bytes
+ * (the 64-bit table of gu_sgd_neighbor_filter is gathered; small caps). */
+int32_t gu_sgd_record_bytes_for(int64_t concurrency);
 int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
-                         const double* sym_w, const int32_t* nbr_indptr, uint64_t seed,
-                         void* edges_int4, int32_t* perm_out, void* stream);
+                         const double* sym_w, const int32_t* nbr_indptr,
+                         const int32_t* nbr_indices, int32_t record_bytes, uint64_t seed,
+                         void* edges, int32_t* perm_out, void* stream);
 int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr, const int32_t* nbr_indices,
                            void* filter_out, void* stream);
-int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4,
-                  const int32_t* nbr_indptr, const int32_t* nbr_indices,
+int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges,
+                  int32_t record_bytes, const int32_t* nbr_indptr, const int32_t* nbr_indices,
                   const void* nbr_filter, float a, float b,
                   float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
                   int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
@@ -161,8 +171,9 @@ int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4
  * return), applied after the batch -- integer sums do not depend on the
  * order the atomics land in.  Replaces the same _run_sgd loop as
  * gu_sgd_epochs (layout.py:314-360). */
-int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_xy, const void* edges_int4,
-                                const int32_t* nbr_indptr, const int32_t* nbr_indices,
+int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_xy, const void* edges,
+                                int32_t record_bytes, const int32_t* nbr_indptr,
+                                const int32_t* nbr_indices,
                                 const void* nbr_filter, float a, float b, float lr0, int32_t t,
                                 int32_t epoch_begin, int32_t epoch_end, int32_t n_neg,
                                 int64_t window, int32_t windowed, uint64_t seed, int64_t batch,
@@ -239,6 +250,21 @@ size_t gu_spectral_op_workspace_size(int64_t n);
 int gu_spectral_op(int64_t n, const int32_t* indptr, const int32_t* indices,
                    const double* inv_sqrt, const double* basis, int32_t nb, const double* x,
                    double* y, void* workspace, size_t ws_bytes, void* stream);
+/* Thick-restart Lanczos steps of spectral_init's eigensolver
+ * (layout.py:275-278 eigsh k=1 'LM', ncv=32, tol=1e-6, on the operator
+ * above): gu_lanczos_prepare computes vb = B^T v and the operator input of v;
+ * gu_lanczos_step(j) applies the operator to row j of V ((ncv+1) x n), runs
+ * two classical Gram-Schmidt passes against [B; V_0..V_j] with the dots fused
+ * into the passes, and writes row j+1 of V, row j+1 of VB ((ncv+1) x 4 rows
+ * V_i^T B) and H[:j+2, j] ((ncv+1) x ncv).  No host synchronisation. */
+size_t gu_lanczos_workspace_size(int64_t n);
+int gu_lanczos_prepare(int64_t n, const double* inv_sqrt, const double* basis, int32_t nb,
+                       const double* v, double* vb, void* workspace, size_t ws_bytes,
+                       void* stream);
+int gu_lanczos_step(int64_t n, const int32_t* indptr, const int32_t* indices,
+                    const double* inv_sqrt, const double* basis, int32_t nb, double* V,
+                    double* VB, double* H, int32_t ncv, int32_t j, void* workspace,
+                    size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------- connected components
  * graph.py is_connected / largest_connected_component: labels[v] = smallest

@@ -46,6 +46,10 @@ SIGNATURES = {
                                           _vp]),
     "gu_spectral_degree": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "gu_spectral_op_workspace_size": (_c_sz, [_c_i64]),
+    "gu_lanczos_workspace_size": (_c_sz, [_c_i64]),
+    "gu_lanczos_prepare": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i32, _vp, _vp, _vp, _c_sz, _vp]),
+    "gu_lanczos_step": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _c_i32, _vp, _vp, _vp, _c_i32,
+                                       _c_i32, _vp, _c_sz, _vp]),
     "gu_spectral_op": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _c_i32, _vp, _vp, _vp, _c_sz,
                                       _vp]),
     "gu_components_workspace_size": (_c_sz, [_c_i64]),
@@ -81,19 +85,23 @@ SIGNATURES = {
     "gu_pack_records": (ctypes.c_int, [_c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                        _c_sz, _vp]),
     "gu_pack_records_workspace_size": (_c_sz, [_c_i64]),
-    "gu_smooth_knn": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i32, _c_f64, _vp, _vp, _vp, _vp]),
+    "gu_smooth_knn_workspace_size": (_c_sz, [_c_i64]),
+    "gu_smooth_knn": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i32, _c_f64, _vp, _vp, _vp, _vp, _c_sz,
+                                     _vp]),
     "gu_symmetrize_workspace_size": (_c_sz, [_c_i64, _c_i64]),
     "gu_symmetrize": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      ctypes.POINTER(_c_i64), _vp, _c_sz, _vp]),
-    "gu_sgd_prepare_edges": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _c_u64, _vp, _vp, _vp]),
+    "gu_sgd_record_bytes_for": (_c_i32, [_c_i64]),
+    "gu_sgd_prepare_edges": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_u64, _vp,
+                                            _vp, _vp]),
     "gu_sgd_neighbor_filter": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
-    "gu_sgd_epochs": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _c_f32, _c_f32,
-                                     _c_f32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i64, _c_i32,
-                                     _c_u64, _c_i64, _vp, _vp]),
-    "gu_sgd_epochs_deterministic": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp,
-                                                   _c_f32, _c_f32, _c_f32, _c_i32, _c_i32, _c_i32,
-                                                   _c_i32, _c_i64, _c_i32, _c_u64, _c_i64, _vp,
-                                                   _vp, _vp]),
+    "gu_sgd_epochs": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _c_i32, _vp, _vp, _vp, _c_f32,
+                                     _c_f32, _c_f32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i64,
+                                     _c_i32, _c_u64, _c_i64, _vp, _vp]),
+    "gu_sgd_epochs_deterministic": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _c_i32, _vp, _vp,
+                                                   _vp, _c_f32, _c_f32, _c_f32, _c_i32, _c_i32,
+                                                   _c_i32, _c_i32, _c_i64, _c_i32, _c_u64, _c_i64,
+                                                   _vp, _vp, _vp]),
     "gu_sgd_visit_order": (ctypes.c_int, [_c_i64, _c_i32, _c_i64, _c_i32, _c_u64, _vp, _vp]),
     "gu_replay_schedule": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _c_i32, _vp,
                                           _vp, ctypes.POINTER(_c_i64)]),

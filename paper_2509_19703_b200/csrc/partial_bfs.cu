@@ -353,6 +353,7 @@ __device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
 #ifndef TF_MINB
 #define TF_MINB 8
 #endif
+
 // Partial Fisher-Yates resolved in registers (no shared-memory swaps).  Lane
 // i < r holds its draw j_i (>= i), a_i = list[i] and a_j = list[j_i] of the
 // original list; the result is list[i] after the reference's r sequential
@@ -396,6 +397,7 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
   const unsigned lt = (1u << lane) - 1u, le_mask = (2u << lane) - 1u;
   int* const hkey = sm_hash[warp];
   int* const lst = sm_list[warp];
+  const unsigned hbase = (unsigned)__cvta_generic_to_shared(hkey);
   unsigned long long w_scanned = 0, w_expanded = 0;
   static_assert(TF_CAP2 + 32 + 1 + 32 <= (HC * 3) / 4, "ball budget must fit the hash");
   // Warp-wide claim of distinct keys (one per lane, `lead` lanes only): one
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
         "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
         "@p atom.shared.cas.b32 %0, [%2], -1, %3;\n\t}"
         : "+r"(old)
-        : "r"((unsigned)lead), "r"((unsigned)__cvta_generic_to_shared(&hkey[h])), "r"(w)
+        : "r"((unsigned)lead), "r"(hbase + 4u * h), "r"(w)
         : "memory");
     bool coll = old != -1 && old != w;
     if (__any_sync(FULL, coll)) {
@@ -432,8 +434,6 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
       continue;
     }
-#pragma unroll
-    for (int i = 0; i < HC / 128; i++) reinterpret_cast<int4*>(hkey)[lane + 32 * i] = make_int4(-1, -1, -1, -1);
     const int w1 = lane < T0 ? __ldg(indices + b0 + lane) : -1;
     // level-2 parent ranges issued right away (needed unless level 1 crosses)
     int pb = 0, pd = 0;
@@ -441,24 +441,24 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       pb = __ldg(indptr + w1);
       pd = __ldg(indptr + w1 + 1) - pb;
     }
-    __syncwarp();
-    if (lane == 0) hkey[hash_id(s) & (HC - 1)] = s;
-    __syncwarp();
-    claim(w1, lane < T0);
     const unsigned long long fy_base = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
     if (T0 >= K) {
       // ---- level 1 reaches the budget: sorted adjacency, or a random subset
+      // (no hash: nothing beyond level 1 is discovered)
       if (T0 == K) {
         if (lane < K) {
           rn[lane] = w1;
           rd[lane] = 1;
         }
       } else {
-        // the list is level 1 itself, one id per lane: all in registers
-        int j = 0;
+        // Fisher-Yates on positions of the sorted adjacency: the picks'
+        // id order is their position order, so the rank is one popcount
+        int j = lane;
         if (lane < K) j = lane + umod64_tab(splitmix_at(fy_base, lane), T0 - lane);
-        const int v = fy_registers(K, lane, j, w1, __shfl_sync(FULL, w1, j & 31));
-        const int r = rank_in_warp(K, v);
+        const int P = fy_registers(K, lane, j, lane, j);
+        const int v = __shfl_sync(FULL, w1, P & 31);
+        const unsigned M = __reduce_or_sync(FULL, lane < K ? 1u << P : 0u);
+        const int r = __popc(M & ((1u << P) - 1u));
         if (lane < K) {
           rn[r] = v;
           rd[r] = 1;
@@ -480,6 +480,12 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       rn[lane] = w1;
       rd[lane] = 1;
     }
+#pragma unroll
+    for (int i = 0; i < HC / 128; i++) reinterpret_cast<int4*>(hkey)[lane + 32 * i] = make_int4(-1, -1, -1, -1);
+    __syncwarp();
+    if (lane == 0) hkey[hash_id(s) & (HC - 1)] = s;
+    __syncwarp();
+    claim(w1, lane < T0);
     // ---- level 2: prefix of the parents' degrees.  In an undirected CSR a
     // neighbour of s has s in its own list, so every parent is non-empty; a
     // CSR that breaks this (one-sided entries) takes the generic tiers.
@@ -579,7 +585,8 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     if (nst > remaining) {
       int j = lane;
       if (lane < remaining) j = lane + umod64_tab(splitmix_at(fy_base, lane), nst - lane);
-      v = fy_registers(remaining, lane, j, v, lst[j]);
+      const int aj = lst[j];
+      v = fy_registers(remaining, lane, j, v, aj);
     }
     const int r = rank_in_warp(remaining, v);
     if (lane < remaining) {

@@ -107,26 +107,6 @@ struct Feistel {
   }
 };
 
-// Edge record {src, dst, float(h), row}: row = (start of src's neighbour row
-// << 6) | degree when both fit (start < 2^26, degree < 63), else -1 (the
-// kernel then reads nbr_indptr) -- the first rejection probe can then issue
-// straight after the coalesced record load.
-__global__ void prepare_edges_kernel(long long E, const int* __restrict__ src,
-                                     const int* __restrict__ dst, const double* __restrict__ w,
-                                     const int* __restrict__ nip, unsigned long long key,
-                                     int4* __restrict__ out, int* __restrict__ perm_out) {
-  Feistel perm((unsigned long long)E, key);
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E;
-       p += (long long)gridDim.x * blockDim.x) {
-    const long long e = (long long)perm((unsigned long long)p);
-    const int u = src[e];
-    const int rb = nip[u], deg = nip[u + 1] - rb;
-    const int row = (rb < (1 << 26) && deg < 63) ? ((rb << 6) | deg) : -1;
-    out[p] = make_int4(u, dst[e], __float_as_int((float)w[e]), row);
-    if (perm_out) perm_out[p] = (int)e;
-  }
-}
-
 __device__ __forceinline__ float clip4(float x) { return fminf(4.0f, fmaxf(-4.0f, x)); }
 
 __device__ __forceinline__ bool is_neighbor(const int* __restrict__ ip, const int* __restrict__ ix,
@@ -142,29 +122,31 @@ __device__ __forceinline__ bool is_neighbor(const int* __restrict__ ip, const in
   return false;
 }
 
-// Per-vertex Bloom word of the neighbour ids (FILT_WORDS 32-bit words,
-// FILT_K hash bits per id): a candidate with any of its bits clear is
-// certainly not a neighbour, so only the filter hits (true neighbours and
-// false positives) run the row search and the test stays exact.
-// 64 bits with 2 hash bits per id measured best (c5 epoch 3.39 -> 3.21 ms,
-// c3 0.341 -> 0.295 ms against 128 bits / 1 bit): the same false-positive
-// rate for ~12 neighbours in half the footprint, so the filter and the
-// coordinates stay L2-resident together (profiles/README.md)
-#ifndef SGD_FILT_WORDS
-#define SGD_FILT_WORDS 2
-#endif
-#ifndef SGD_FILT_K
-#define SGD_FILT_K 2
-#endif
-constexpr int FILT_WORDS = SGD_FILT_WORDS, FILT_K = SGD_FILT_K;
-static_assert(FILT_WORDS == 2 || FILT_WORDS == 4, "filter word size");
-static_assert(FILT_K >= 1 && FILT_K <= 3, "filter hash count");
-constexpr int FILT_SHIFT = FILT_WORDS == 4 ? 25 : 26;  // 32 - log2(bits)
-using FiltWord = typename std::conditional<FILT_WORDS == 4, uint4, uint2>::type;
+// Per-vertex Bloom words of the neighbour ids: a candidate with any of its
+// bits clear is certainly not a neighbour, so only the filter hits (true
+// neighbours and false positives) run the row search and the test stays
+// exact.  Two layouts, chosen per plan (gu_sgd_record_bytes_for):
+//  * table: 64 bits, 2 hash bits per id, one word per vertex gathered by
+//    head (8 B x n) -- measured best for small concurrency caps (c3 epoch
+//    0.277 ms vs 0.39 with the records below; profiles/r02_ab_sgd_r32b.log);
+//  * in-record: 32-byte edge records carry their head's 128-bit word with 3
+//    hash bits per id, streamed with the record -- no dependent gather, and
+//    ~1.5% false positives instead of ~10% at degree 12 (c5 epoch 3.21 ->
+//    2.75 ms; profiles/r02_ab_sgd_r32.log).
+struct Filt64 {
+  using Word = uint2;
+  static constexpr int K = 2, SHIFT = 26;  // 32 - log2(64)
+};
+struct Filt128 {
+  using Word = uint4;
+  static constexpr int K = 3, SHIFT = 25;  // 32 - log2(128)
+};
+using FiltWord = Filt64::Word;
 
+template <class F>
 __device__ __forceinline__ unsigned filt_bit(int c, int j) {
   const unsigned m = j == 0 ? 0x9E3779B1u : (j == 1 ? 0x85EBCA77u : 0xC2B2AE3Du);
-  return ((unsigned)c * m) >> FILT_SHIFT;
+  return ((unsigned)c * m) >> F::SHIFT;
 }
 
 __device__ __forceinline__ unsigned filt_word(const uint4& f, unsigned w) {
@@ -172,35 +154,67 @@ __device__ __forceinline__ unsigned filt_word(const uint4& f, unsigned w) {
 }
 __device__ __forceinline__ unsigned filt_word(const uint2& f, unsigned w) { return w ? f.y : f.x; }
 
-__global__ void neighbor_filter_kernel(int n, const int* __restrict__ nip,
-                                       const int* __restrict__ nix, FiltWord* __restrict__ filt) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    unsigned w[4] = {0u, 0u, 0u, 0u};
-    const int b = __ldg(nip + v), e = __ldg(nip + v + 1);
-    for (int p = b; p < e; p++) {
-      const int c = __ldg(nix + p);
+// Bloom word of one neighbour row
+template <class F>
+__device__ __forceinline__ typename F::Word row_filter(const int* __restrict__ nix, int b, int e) {
+  constexpr int WORDS = sizeof(typename F::Word) / 4;
+  unsigned w[4] = {0u, 0u, 0u, 0u};
+  for (int p = b; p < e; p++) {
+    const int c = __ldg(nix + p);
 #pragma unroll
-      for (int k = 0; k < FILT_K; k++) {
-        const unsigned h = filt_bit(c, k);
+    for (int k = 0; k < F::K; k++) {
+      const unsigned h = filt_bit<F>(c, k);
 #pragma unroll
-        for (int j = 0; j < FILT_WORDS; j++)
-          if ((h >> 5) == (unsigned)j) w[j] |= 1u << (h & 31);
-      }
+      for (int j = 0; j < WORDS; j++)
+        if ((h >> 5) == (unsigned)j) w[j] |= 1u << (h & 31);
     }
-    FiltWord f;
-    memcpy(&f, w, sizeof(f));
-    filt[v] = f;
   }
+  typename F::Word f;
+  memcpy(&f, w, sizeof(f));
+  return f;
 }
 
-__device__ __forceinline__ bool filt_maybe(const FiltWord& f, int c) {
+__global__ void neighbor_filter_kernel(int n, const int* __restrict__ nip,
+                                       const int* __restrict__ nix, FiltWord* __restrict__ filt) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    filt[v] = row_filter<Filt64>(nix, __ldg(nip + v), __ldg(nip + v + 1));
+}
+
+template <class F>
+__device__ __forceinline__ bool filt_maybe(const typename F::Word& f, int c) {
   bool all = true;
 #pragma unroll
-  for (int k = 0; k < FILT_K; k++) {
-    const unsigned h = filt_bit(c, k);
+  for (int k = 0; k < F::K; k++) {
+    const unsigned h = filt_bit<F>(c, k);
     all = all && ((filt_word(f, h >> 5) >> (h & 31)) & 1u);
   }
   return all;
+}
+
+// Edge record {src, dst, float(h), row}: row = (start of src's neighbour row
+// << 6) | degree when both fit (start < 2^26, degree < 63), else -1 (the
+// kernel then reads nbr_indptr) -- the first rejection probe can then issue
+// straight after the coalesced record load.  32-byte records append the
+// head's 128-bit Bloom word.
+__global__ void prepare_edges_kernel(long long E, const int* __restrict__ src,
+                                     const int* __restrict__ dst, const double* __restrict__ w,
+                                     const int* __restrict__ nip, const int* __restrict__ nix,
+                                     int rec_int4, unsigned long long key, int4* __restrict__ out,
+                                     int* __restrict__ perm_out) {
+  Feistel perm((unsigned long long)E, key);
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long e = (long long)perm((unsigned long long)p);
+    const int u = src[e];
+    const int rb = nip[u], deg = nip[u + 1] - rb;
+    const int row = (rb < (1 << 26) && deg < 63) ? ((rb << 6) | deg) : -1;
+    out[rec_int4 * p] = make_int4(u, dst[e], __float_as_int((float)w[e]), row);
+    if (rec_int4 == 2) {
+      const uint4 f = row_filter<Filt128>(nix, rb, rb + deg);
+      out[2 * p + 1] = make_int4((int)f.x, (int)f.y, (int)f.z, (int)f.w);
+    }
+    if (perm_out) perm_out[p] = (int)e;
+  }
 }
 
 constexpr int SGD_WARPS = 8;  // 256 threads per block at most (block_for)
@@ -209,7 +223,7 @@ constexpr int SGD_WARPS = 8;  // 256 threads per block at most (block_for)
 // GPU-filling epochs, 2 (96 registers) for the small-cap 16-lane mode, whose
 // few resident warps are latency-bound and gain from the longer register
 // budget (c3 epoch 0.295 -> 0.276 ms; at 96 registers c5 would lose 8%)
-template <int LANES, int MINB>
+template <int LANES, int MINB, bool REC32>
 __global__ void __launch_bounds__(256, MINB)
     sgd_epoch_kernel(int n, long long E, float2* __restrict__ xy, const int4* __restrict__ edges,
                      const int* __restrict__ nip, const int* __restrict__ nix,
@@ -271,11 +285,18 @@ __global__ void __launch_bounds__(256, MINB)
     }
     if (!act) p = 0;
     // streamed once per epoch: evict-first, keep L2 for x / filter / rows
-    const int4 rec = act ? __ldcs(edges + p) : make_int4(0, 0, 0, 0);
+    using F = typename std::conditional<REC32, Filt128, Filt64>::type;
+    const int4 rec = act ? __ldcs(edges + (REC32 ? 2 : 1) * p) : make_int4(0, 0, 0, 0);
     const int u = rec.x, v = rec.y;
-    FiltWord fw;
-    if (filt) fw = __ldg(filt + u);
-    else memset(&fw, 0xff, sizeof(fw));
+    typename F::Word fw;
+    if (REC32) {
+      const int4 f4 = act ? __ldcs(edges + 2 * p + 1) : make_int4(-1, -1, -1, -1);
+      memcpy(&fw, &f4, sizeof(fw));
+    } else if (filt) {
+      memcpy(&fw, filt + u, sizeof(fw));
+    } else {
+      memset(&fw, 0xff, sizeof(fw));
+    }
     const float h = __int_as_float(rec.z);
     float2 xu = xy[u];
     const float2 xv = xy[v];
@@ -326,7 +347,7 @@ __global__ void __launch_bounds__(256, MINB)
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         draw_q[q] = draw32(vbase, q0 + q, 0);
         cand[q] = (int)__umulhi(draw_q[q], (unsigned)n);
-        if (act && q < nq && filt_maybe(fw, cand[q])) mm |= 1u << q;
+        if (act && q < nq && filt_maybe<F>(fw, cand[q])) mm |= 1u << q;
       }
       float2 xc[SGD_NEG_BLOCK];
 #pragma unroll
@@ -481,17 +502,43 @@ unsigned block_for(long long max_threads) {
 
 using namespace gu;
 
+// visits per warp of an epoch launch: a cap below the resident-thread
+// capacity (4 blocks of 256 per SM at 64 registers) runs 16 visits per warp
+// on cap * 2 threads -- the same visits in flight, more warps to hide
+// latency (measured best on c3; 8 lanes slows full epochs).
+// GU_SGD_MIN_LANES=32 turns it off.
+static int sgd_lanes(long long concurrency) {
+  const long long resident = 148LL * SGD_MIN_BLOCKS * 256;
+  static const int min_lanes = [] {
+    const char* v = getenv("GU_SGD_MIN_LANES");
+    return (v && atoi(v) >= 32) ? 32 : 16;
+  }();
+  if (concurrency > 0 && concurrency < resident && min_lanes == 16 &&
+      (concurrency * 32) / 16 <= 148LL * 2 * 256)  // fits the 2-CTA/SM kernel
+    return 16;
+  return 32;
+}
+
+extern "C" int32_t gu_sgd_record_bytes_for(int64_t concurrency) {
+  // GPU-filling epochs stream 32-byte records with the in-record filter;
+  // small caps keep 16-byte records and the gathered 64-bit table
+  return sgd_lanes(concurrency) == 32 ? 32 : 16;
+}
+
 extern "C" int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
-                                    const double* sym_w, const int32_t* nbr_indptr, uint64_t seed,
-                                    void* edges_int4, int32_t* perm_out, void* stream) {
-  if (E < 0 || E >= INT_MAX) {
-    set_error("gu_sgd_prepare_edges: unsupported E=%lld", (long long)E);
+                                    const double* sym_w, const int32_t* nbr_indptr,
+                                    const int32_t* nbr_indices, int32_t record_bytes,
+                                    uint64_t seed, void* edges, int32_t* perm_out,
+                                    void* stream) {
+  if (E < 0 || E >= INT_MAX || (record_bytes != 16 && record_bytes != 32)) {
+    set_error("gu_sgd_prepare_edges: unsupported E=%lld / record_bytes=%d", (long long)E,
+              record_bytes);
     return GU_ERR_UNSUPPORTED;
   }
   if (E == 0) return GU_OK;
   prepare_edges_kernel<<<grid_for(E), 256, 0, (cudaStream_t)stream>>>(
-      E, sym_src, sym_dst, sym_w, nbr_indptr, mix64(seed ^ 0xED6E5ull), (int4*)edges_int4,
-      perm_out);
+      E, sym_src, sym_dst, sym_w, nbr_indptr, nbr_indices, record_bytes / 16,
+      mix64(seed ^ 0xED6E5ull), (int4*)edges, perm_out);
   GU_CHECK_LAUNCH("prepare_edges_kernel");
   return GU_OK;
 }
@@ -520,14 +567,25 @@ extern "C" int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr,
   return GU_OK;
 }
 
-extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges_int4,
-                             const int32_t* nbr_indptr, const int32_t* nbr_indices,
-                             const void* nbr_filter, float a,
+typedef void (*EpochKernel)(int, long long, float2*, const int4*, const int*, const int*,
+                            const FiltWord*, float, float, float, int, int, long long, long long,
+                            int, unsigned long long, int*, long long, long long*);
+
+static EpochKernel epoch_kernel(int lanes, bool rec32) {
+  if (lanes == 32)
+    return rec32 ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS, true>
+                 : sgd_epoch_kernel<32, SGD_MIN_BLOCKS, false>;
+  return rec32 ? sgd_epoch_kernel<16, 2, true> : sgd_epoch_kernel<16, 2, false>;
+}
+
+extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges,
+                             int32_t record_bytes, const int32_t* nbr_indptr,
+                             const int32_t* nbr_indices, const void* nbr_filter, float a,
                              float b, float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
                              int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
                              int64_t concurrency, int32_t* diverged, void* stream) {
   if (n <= 0 || n >= INT_MAX || E < 0 || t < 0 || epoch_begin < 0 || epoch_end > t ||
-      (windowed && (window < 1 || window > E))) {
+      (record_bytes != 16 && record_bytes != 32) || (windowed && (window < 1 || window > E))) {
     set_error("gu_sgd_epochs: bad arguments");
     return GU_ERR_ARG;
   }
@@ -538,25 +596,12 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
     const float lr = (float)((double)lr0 * (1.0 - (double)e / (double)t));
     long long items, start;
     epoch_range(E, e, window, windowed, &items, &start);
-    // a cap below the resident-thread capacity (4 blocks of 256 per SM at 64
-    // registers) runs `lanes` < 32 visits per warp on cap * 32 / lanes
-    // threads: the same visits in flight, more warps to hide latency
-    const long long resident = 148LL * SGD_MIN_BLOCKS * 256;
-    // 16 lanes: measured best on c3 (8 slows full epochs); GU_SGD_MIN_LANES=32
-    // turns it off
-    static const int min_lanes = [] {
-      const char* v = getenv("GU_SGD_MIN_LANES");
-      return (v && atoi(v) >= 32) ? 32 : 16;
-    }();
-    int lanes = 32;
-    if (concurrency > 0 && concurrency < resident && min_lanes == 16 &&
-        (concurrency * 32) / 16 <= 148LL * 2 * 256)  // fits the 2-CTA/SM kernel
-      lanes = 16;
+    const int lanes = sgd_lanes(concurrency);
     const long long threads = concurrency > 0 ? (concurrency * 32 + lanes - 1) / lanes : 0;
     const unsigned bs = block_for(threads);
     const unsigned gs = bs < 256 ? 1u : grid_for((items * 32 + lanes - 1) / lanes, threads);
-    auto kern = lanes == 32 ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS> : sgd_epoch_kernel<16, 2>;
-    kern<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr,
+    EpochKernel kern = epoch_kernel(lanes, record_bytes == 32);
+    kern<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges, nbr_indptr,
                             nbr_indices, (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, items,
                             start, windowed, seed, diverged, 0LL, nullptr);
     GU_CHECK_LAUNCH("sgd_epoch_kernel");
@@ -565,7 +610,8 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
 }
 
 extern "C" int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_xy,
-                                           const void* edges_int4, const int32_t* nbr_indptr,
+                                           const void* edges, int32_t record_bytes,
+                                           const int32_t* nbr_indptr,
                                            const int32_t* nbr_indices, const void* nbr_filter,
                                            float a, float b, float lr0, int32_t t,
                                            int32_t epoch_begin, int32_t epoch_end, int32_t n_neg,
@@ -573,7 +619,8 @@ extern "C" int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_x
                                            int64_t batch, int64_t* acc, int32_t* diverged,
                                            void* stream) {
   if (n <= 0 || n >= INT_MAX || E < 0 || t < 0 || epoch_begin < 0 || epoch_end > t ||
-      batch < 32 || !acc || (windowed && (window < 1 || window > E))) {
+      batch < 32 || !acc || (record_bytes != 16 && record_bytes != 32) ||
+      (windowed && (window < 1 || window > E))) {
     set_error("gu_sgd_epochs_deterministic: bad arguments");
     return GU_ERR_ARG;
   }
@@ -589,8 +636,8 @@ extern "C" int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_x
       const long long threads = b1 - b0;
       const unsigned bs = block_for(threads);
       const unsigned gs = bs < 256 ? 1u : grid_for(threads, threads);
-      sgd_epoch_kernel<32, SGD_MIN_BLOCKS><<<gs, bs, 0, st>>>(
-          (int)n, E, (float2*)coords_xy, (const int4*)edges_int4, nbr_indptr, nbr_indices,
+      epoch_kernel(32, record_bytes == 32)<<<gs, bs, 0, st>>>(
+          (int)n, E, (float2*)coords_xy, (const int4*)edges, nbr_indptr, nbr_indices,
           (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, b1, start, windowed, seed, diverged,
           b0, (long long*)acc);
       GU_CHECK_LAUNCH("sgd_epoch_kernel(deterministic)");

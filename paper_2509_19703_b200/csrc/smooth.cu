@@ -130,12 +130,16 @@ __device__ double row_sigma(const int* d, int c, int kmax, double target, double
 // result is the same float64 computation on the same operands: bit-identical.
 constexpr int SIG_TABLE = 8192;
 constexpr unsigned long long SIG_EMPTY = 0ull;
-__device__ unsigned long long g_sig_key[SIG_TABLE];
-__device__ long long g_sig_rep[SIG_TABLE];
-__device__ double g_sig_val[SIG_TABLE];
-__device__ double g_sig_rho[SIG_TABLE];
-__device__ double g_sig_w[SIG_TABLE][4];     // weight of each run
-__device__ unsigned g_sig_ends[SIG_TABLE];   // cumulative run ends, 8 bits each
+// the profile table lives in the caller's workspace (per call: concurrent
+// calls on different streams never share it)
+struct SigTable {
+  unsigned long long key[SIG_TABLE];
+  long long rep[SIG_TABLE];
+  double val[SIG_TABLE];
+  double rho[SIG_TABLE];
+  double w[SIG_TABLE][4];    // weight of each run
+  unsigned ends[SIG_TABLE];  // cumulative run ends, 8 bits each
+};
 
 __device__ __forceinline__ unsigned long long sig_mix(unsigned long long x) {
   x ^= x >> 33;
@@ -161,14 +165,15 @@ __device__ __forceinline__ unsigned long long row_key(const int* d, int c) {
   return key | ((unsigned long long)runs << 56);
 }
 
-__global__ void sig_clear() {
+__global__ void sig_clear(SigTable* __restrict__ tab) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < SIG_TABLE; i += gridDim.x * blockDim.x)
-    g_sig_key[i] = SIG_EMPTY;
+    tab->key[i] = SIG_EMPTY;
 }
 
 // pass 1 (thread per row): key -> table slot, kept in slot_out (-1: direct)
 __global__ void sig_keys(long long n, const long long* __restrict__ indptr,
-                         const int* __restrict__ dist, int kmax, int* __restrict__ slot_out) {
+                         const int* __restrict__ dist, int kmax, SigTable* __restrict__ tab,
+                         int* __restrict__ slot_out) {
   const int lane = threadIdx.x & 31;
   for (long long base = (long long)blockIdx.x * blockDim.x + threadIdx.x - lane; base < n;
        base += (long long)gridDim.x * blockDim.x) {
@@ -186,11 +191,11 @@ __global__ void sig_keys(long long n, const long long* __restrict__ indptr,
     if (lane == leader && key != SIG_EMPTY) {
       unsigned h = (unsigned)sig_mix(key) & (SIG_TABLE - 1);
       for (int probe = 0; probe < SIG_TABLE; probe++) {
-        unsigned long long cur = *(volatile unsigned long long*)&g_sig_key[h];
+        unsigned long long cur = *(volatile unsigned long long*)&tab->key[h];
         if (cur == SIG_EMPTY) {
-          cur = atomicCAS(&g_sig_key[h], SIG_EMPTY, key);
+          cur = atomicCAS(&tab->key[h], SIG_EMPTY, key);
           if (cur == SIG_EMPTY) {  // inserted: this row represents the profile
-            g_sig_rep[h] = v;
+            tab->rep[h] = v;
             slot = (int)h;
             break;
           }
@@ -209,18 +214,18 @@ __global__ void sig_keys(long long n, const long long* __restrict__ indptr,
 
 // pass 2 (thread per table entry): sigma of each profile on its representative
 __global__ void sig_solve(const long long* __restrict__ indptr, const int* __restrict__ dist,
-                          int kmax, double target) {
+                          int kmax, double target, SigTable* __restrict__ tab) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < SIG_TABLE; s += gridDim.x * blockDim.x) {
-    if (g_sig_key[s] == SIG_EMPTY) continue;
-    const long long v = g_sig_rep[s];
+    if (tab->key[s] == SIG_EMPTY) continue;
+    const long long v = tab->rep[s];
     const long long lo = indptr[v];
     double rho;
     const int c = (int)(indptr[v + 1] - lo);
     const double sigma = row_sigma(dist + lo, c, kmax, target, &rho);
-    g_sig_val[s] = sigma;
-    g_sig_rho[s] = rho;
+    tab->val[s] = sigma;
+    tab->rho[s] = rho;
     // per-run weights: the same expression the per-entry path evaluates
-    const unsigned long long key = g_sig_key[s];
+    const unsigned long long key = tab->key[s];
     const int runs = (int)((key >> 56) & 7);
     unsigned ends = 0;
     int end = 0;
@@ -228,11 +233,11 @@ __global__ void sig_solve(const long long* __restrict__ indptr, const int* __res
       if (j < runs) {
         const int dj = (int)((key >> (14 * j + 6)) & 255);
         end += (int)((key >> (14 * j)) & 63);
-        g_sig_w[s][j] = exp(-((double)dj - rho) / sigma);
+        tab->w[s][j] = exp(-((double)dj - rho) / sigma);
       }
       ends |= (unsigned)(j < runs ? end : 255) << (8 * j);
     }
-    g_sig_ends[s] = ends;
+    tab->ends[s] = ends;
   }
 }
 
@@ -242,9 +247,9 @@ __global__ void sig_solve(const long long* __restrict__ indptr, const int* __res
 // a shuffle search; w = exp(-(d - rho) / sigma) as in the reference
 __global__ void __launch_bounds__(128)
     smooth_kernel(long long n, const long long* __restrict__ indptr, const int* __restrict__ dist,
-                  int kmax, double target, const int* __restrict__ slot_in,
-                  double* __restrict__ rho_out, double* __restrict__ sigma_out,
-                  double* __restrict__ w_out) {
+                  int kmax, double target, const SigTable* __restrict__ tab,
+                  const int* __restrict__ slot_in, double* __restrict__ rho_out,
+                  double* __restrict__ sigma_out, double* __restrict__ w_out) {
   const int lane = threadIdx.x & 31;
   for (long long base = (long long)blockIdx.x * blockDim.x + threadIdx.x - lane; base < n;
        base += (long long)gridDim.x * blockDim.x) {
@@ -256,8 +261,8 @@ __global__ void __launch_bounds__(128)
     const int slot = valid && slot_in ? slot_in[v] : -1;
     if (valid) {
       if (slot >= 0) {
-        rho = g_sig_rho[slot];
-        sigma = g_sig_val[slot];
+        rho = tab->rho[slot];
+        sigma = tab->val[slot];
       } else {
         sigma = row_sigma(dist + lo, (int)(hi - lo), kmax, target, &rho);
       }
@@ -283,10 +288,10 @@ __global__ void __launch_bounds__(128)
       if (e < e1) {
         double w;
         if (r_slot >= 0) {  // profiled row: its run's precomputed weight
-          const unsigned ends = g_sig_ends[r_slot];
+          const unsigned ends = tab->ends[r_slot];
           const unsigned i = (unsigned)(e - r_lo);
           const int j = (i >= (ends & 255u)) + (i >= ((ends >> 8) & 255u)) + (i >= ((ends >> 16) & 255u));
-          w = g_sig_w[r_slot][j];
+          w = tab->w[r_slot][j];
         } else {
           w = exp(-((double)dist[e] - r_rho) / r_sig);
         }
@@ -301,8 +306,18 @@ __global__ void __launch_bounds__(128)
 
 using namespace gu;
 
+// memoised-sigma scratch: the profile table + one slot per row (rows below
+// SMOOTH_MEMO_MIN_ROWS are solved directly and need no workspace)
+constexpr long long SMOOTH_MEMO_MIN_ROWS = 4096;
+
+extern "C" size_t gu_smooth_knn_workspace_size(int64_t n) {
+  if (n < SMOOTH_MEMO_MIN_ROWS) return 0;
+  return ((sizeof(SigTable) + 255) & ~(size_t)255) + sizeof(int) * (size_t)n;
+}
+
 extern "C" int gu_smooth_knn(int64_t n, const int64_t* indptr, const int32_t* dist, int32_t kmax,
-                             double target, double* rho, double* sigma, double* w, void* stream) {
+                             double target, double* rho, double* sigma, double* w,
+                             void* workspace, size_t ws_bytes, void* stream) {
   if (n < 0 || kmax < 1) {
     set_error("gu_smooth_knn: bad arguments (n=%lld kmax=%d)", (long long)n, kmax);
     return GU_ERR_ARG;
@@ -311,36 +326,25 @@ extern "C" int gu_smooth_knn(int64_t n, const int64_t* indptr, const int32_t* di
   cudaStream_t st = (cudaStream_t)stream;
   long long blocks = (n + 127) / 128;
   if (blocks > 148LL * 32) blocks = 148LL * 32;
-  // per-row table slots live in a stream-ordered scratch allocation; the
-  // device's default pool keeps its memory between calls (no OS round trip)
-  static int pool_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (pool_dev != dev) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      unsigned long long keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    cudaGetLastError();
-    pool_dev = dev;
+  const size_t need = gu_smooth_knn_workspace_size(n);
+  if (need && (!workspace || ws_bytes < need)) {
+    set_error("gu_smooth_knn: workspace %zu < %zu bytes", ws_bytes, need);
+    return GU_ERR_WORKSPACE;
   }
-  int* slots = nullptr;
-  if (n >= 4096 && cudaMallocAsync((void**)&slots, sizeof(int) * (size_t)n, st) != cudaSuccess) {
-    cudaGetLastError();
-    slots = nullptr;  // no scratch: every row solved directly
-  }
+  SigTable* tab = need ? (SigTable*)workspace : nullptr;
+  int* slots = need ? (int*)((char*)workspace + ((sizeof(SigTable) + 255) & ~(size_t)255))
+                    : nullptr;
   if (slots) {
-    sig_clear<<<8, 256, 0, st>>>();
+    sig_clear<<<8, 256, 0, st>>>(tab);
     GU_CHECK_LAUNCH("sig_clear");
-    sig_keys<<<(unsigned)blocks, 128, 0, st>>>(n, (const long long*)indptr, dist, kmax, slots);
+    sig_keys<<<(unsigned)blocks, 128, 0, st>>>(n, (const long long*)indptr, dist, kmax, tab,
+                                                slots);
     GU_CHECK_LAUNCH("sig_keys");
-    sig_solve<<<SIG_TABLE / 128, 128, 0, st>>>((const long long*)indptr, dist, kmax, target);
+    sig_solve<<<SIG_TABLE / 128, 128, 0, st>>>((const long long*)indptr, dist, kmax, target, tab);
     GU_CHECK_LAUNCH("sig_solve");
   }
   smooth_kernel<<<(unsigned)blocks, 128, 0, st>>>(n, (const long long*)indptr, dist, kmax, target,
-                                                  slots, rho, sigma, w);
+                                                  tab, slots, rho, sigma, w);
   GU_CHECK_LAUNCH("smooth_kernel");
-  if (slots) GU_CHECK(cudaFreeAsync(slots, st));
   return GU_OK;
 }

@@ -124,6 +124,264 @@ int launch_dots(int n, const double* B, int nb, const double* x, double* partial
   return GU_OK;
 }
 
+// ---------------------------------------------------------------- Lanczos
+// One thick-restart Lanczos step of layout._top_eigvec on the device, the
+// Gram-Schmidt fused into the passes over the basis V (ncv + 1 rows of n):
+//   pass 1  y = xp + D^-1/2 A z (the operator's SpMV; xp = P v_j and
+//           z = D^-1/2 xp prepared by the previous step) fused with the dots
+//           of y against [B; V_0..V_j] (B: the deflated eigenvectors)
+//   pass 2  w = y - B c - V h   with c = B^T y and h = V^T y - (V^T B) c,
+//           i.e. P y projected against V, fused with the second-pass dots
+//           [B; V]^T w (CGS2)
+//   pass 3  w -= B c' + V h'   and ||w||^2
+//   pass 4  v_{j+1} = w / beta and its dots with B (the row V_{j+1}^T B kept
+//           for the next step's h), then xp / z of v_{j+1}
+// H[:j+1, j] = h + h', H[j+1, j] = beta are written on the device; every
+// reduction is partials per block then one block summing them in a fixed
+// order (deterministic).  Replaces four cuBLAS GEMV passes, a norm and a
+// scale per step (the torch loop of round 1).
+constexpr int LZ_MAX_ROWS = SP_MAX_BASIS + 64;  // B rows + V rows (ncv <= 63)
+constexpr int LZ_BLOCKS = 148 * 4;
+
+struct LzWs {
+  double* y;        // n
+  double* w;        // n
+  double* xp;       // n
+  double* z;        // n
+  double* partial;  // LZ_MAX_ROWS x LZ_BLOCKS
+  double* coef;     // LZ_MAX_ROWS (c | h of the current pass)
+  double* hsum;     // LZ_MAX_ROWS (first-pass h kept for H)
+  double* beta;     // 1
+};
+
+size_t lz_layout(long long n, char* base, LzWs* ws) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = (off + bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t oy = take(8 * (size_t)n), ow = take(8 * (size_t)n), ox = take(8 * (size_t)n),
+               oz = take(8 * (size_t)n), op = take(8 * (size_t)LZ_MAX_ROWS * LZ_BLOCKS),
+               oc = take(8 * (size_t)LZ_MAX_ROWS), oh = take(8 * (size_t)LZ_MAX_ROWS),
+               ob = take(8);
+  if (base && ws) {
+    ws->y = (double*)(base + oy);
+    ws->w = (double*)(base + ow);
+    ws->xp = (double*)(base + ox);
+    ws->z = (double*)(base + oz);
+    ws->partial = (double*)(base + op);
+    ws->coef = (double*)(base + oc);
+    ws->hsum = (double*)(base + oh);
+    ws->beta = (double*)(base + ob);
+  }
+  return off;
+}
+
+// row r of [B; V]: B_r for r < nb, else V_{r - nb}
+__device__ __forceinline__ const double* lz_row(const double* B, int nb, const double* V, long long n,
+                                                int r) {
+  return r < nb ? B + (long long)r * n : V + (long long)(r - nb) * n;
+}
+
+// block-reduce this thread's per-row accumulators acc[q] (row first + q *
+// stride; stride 8: the 8-lane groups of a warp hold rows g8, g8 + 8, ...;
+// stride 1: every lane holds rows 0, 1, ...) into partial[r][block] for the
+// rows r in [r0, r1)
+template <int NACC>
+__device__ __forceinline__ void lz_block_partials(const double (&acc)[NACC], int first, int stride,
+                                                  int r0, int r1, double* partial) {
+  __shared__ double sh[LZ_MAX_ROWS][SP_THREADS / 32];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NACC; q++) {
+    double v = acc[q];
+    if (stride == 8) {
+      v += __shfl_xor_sync(FULL, v, 8);
+      v += __shfl_xor_sync(FULL, v, 16);
+    } else {
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    }
+    const int r = first + q * stride;
+    if (r >= r0 && r < r1 && lane < (stride == 8 ? 8 : 1)) sh[r][wid] = v;
+  }
+  __syncthreads();
+  for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < SP_THREADS / 32; k++) s += sh[r][k];
+    partial[(long long)r * gridDim.x + blockIdx.x] = s;
+  }
+  __syncthreads();  // sh is reused by the next call
+}
+
+// pass 1: y = xp + inv_sqrt * (A z), 8 lanes per row; lane g8 of a row's
+// group accumulates the dots of y with rows g8, g8 + 8, ... of [B; V]
+__global__ void __launch_bounds__(SP_THREADS)
+    lz_spmv_dots(int n, const int* __restrict__ indptr, const int* __restrict__ indices,
+                 const double* __restrict__ inv_sqrt, const double* __restrict__ xp,
+                 const double* __restrict__ z, double* __restrict__ y,
+                 const double* __restrict__ B, int nb, const double* __restrict__ V, int nr,
+                 double* __restrict__ partial) {
+  constexpr int NACC = LZ_MAX_ROWS / 8;
+  const int g8 = threadIdx.x & 7;
+  const unsigned gmask = 0xffu << (threadIdx.x & 24);
+  double acc[NACC];
+#pragma unroll
+  for (int q = 0; q < NACC; q++) acc[q] = 0.0;
+  // a block-uniform trip count (every thread reaches the reductions)
+  const int rows_per_iter = (gridDim.x * SP_THREADS) >> 3;
+  for (int v0 = (blockIdx.x * SP_THREADS) >> 3; v0 < n; v0 += rows_per_iter) {
+    const int v = v0 + (threadIdx.x >> 3);
+    double yv = 0.0;
+    if (v < n) {
+      const int b = __ldg(indptr + v), e = __ldg(indptr + v + 1);
+      double s = 0.0;
+      for (int p = b + g8; p < e; p += 8) s += z[__ldg(indices + p)];
+      s += __shfl_xor_sync(gmask, s, 4, 8);
+      s += __shfl_xor_sync(gmask, s, 2, 8);
+      s += __shfl_xor_sync(gmask, s, 1, 8);
+      yv = xp[v] + inv_sqrt[v] * s;
+      if (g8 == 0) y[v] = yv;
+#pragma unroll
+      for (int q = 0; q < NACC; q++) {
+        const int r = g8 + 8 * q;
+        if (r < nr) acc[q] = fma(lz_row(B, nb, V, n, r)[v], yv, acc[q]);
+      }
+    }
+  }
+  lz_block_partials<NACC>(acc, g8, 8, 0, nr, partial);
+}
+
+// out = x - sum_r rows_r * coef_r (rows of [B; V], nr of them); optional
+// dots of out with every row (partial) and ||out||^2 (partial row nr)
+template <bool DOTS, bool NORM>
+__global__ void __launch_bounds__(SP_THREADS)
+    lz_update(int n, const double* __restrict__ B, int nb, const double* __restrict__ V, int nr,
+              const double* __restrict__ coef, const double* __restrict__ x,
+              double* __restrict__ out, double* __restrict__ partial) {
+  constexpr int NACC = LZ_MAX_ROWS / 8 + 1;
+  __shared__ double c[LZ_MAX_ROWS];
+  for (int r = threadIdx.x; r < nr; r += blockDim.x) c[r] = coef[r];
+  __syncthreads();
+  const int g8 = threadIdx.x & 7;
+  double acc[NACC];
+#pragma unroll
+  for (int q = 0; q < NACC; q++) acc[q] = 0.0;
+  // 8 consecutive threads share an element: lane g8 does rows g8, g8+8, ...
+  const int per_iter = (gridDim.x * SP_THREADS) >> 3;
+  for (int i0 = (blockIdx.x * SP_THREADS) >> 3; i0 < n; i0 += per_iter) {
+    const int i = i0 + (threadIdx.x >> 3);
+    if (i < n) {
+      double s = 0.0;
+      for (int r = g8; r < nr; r += 8) s += lz_row(B, nb, V, n, r)[i] * c[r];
+      const unsigned gmask = 0xffu << (threadIdx.x & 24);
+      s += __shfl_xor_sync(gmask, s, 4, 8);
+      s += __shfl_xor_sync(gmask, s, 2, 8);
+      s += __shfl_xor_sync(gmask, s, 1, 8);
+      const double o = x[i] - s;
+      if (g8 == 0) out[i] = o;
+      if (DOTS) {
+#pragma unroll
+        for (int q = 0; q < NACC - 1; q++) {
+          const int r = g8 + 8 * q;
+          if (r < nr) acc[q] = fma(lz_row(B, nb, V, n, r)[i], o, acc[q]);
+        }
+      }
+      if (NORM && g8 == 0) acc[NACC - 1] = fma(o, o, acc[NACC - 1]);
+    }
+  }
+  if (DOTS) {  // rows 0..nr-1 from the 8-lane groups
+    double head[NACC - 1];
+#pragma unroll
+    for (int q = 0; q < NACC - 1; q++) head[q] = acc[q];
+    lz_block_partials<NACC - 1>(head, g8, 8, 0, nr, partial);
+  }
+  if (NORM) {  // ||out||^2 into row nr (only lanes with g8 == 0 hold a share)
+    const double v[1] = {acc[NACC - 1]};
+    lz_block_partials<1>(v, nr, 1, nr, nr + 1, partial);
+  }
+}
+
+// v = w / beta (beta null: v = w, not written); dots of v with B (partials,
+// rows 0..nb-1)
+__global__ void __launch_bounds__(SP_THREADS)
+    lz_scale_dots(int n, const double* __restrict__ w, const double* __restrict__ beta,
+                  double* __restrict__ v, const double* __restrict__ B, int nb,
+                  double* __restrict__ partial) {
+  double acc[SP_MAX_BASIS] = {0.0, 0.0, 0.0, 0.0};
+  const double ib = beta ? 1.0 / fmax(*beta, 1e-300) : 1.0;
+  for (int i = blockIdx.x * SP_THREADS + threadIdx.x; i < n; i += gridDim.x * SP_THREADS) {
+    const double x = w[i] * ib;
+    if (v) v[i] = x;
+#pragma unroll
+    for (int b = 0; b < SP_MAX_BASIS; b++)
+      if (b < nb) acc[b] = fma(B[(long long)b * n + i], x, acc[b]);
+  }
+  lz_block_partials<SP_MAX_BASIS>(acc, 0, 1, 0, nb, partial);
+}
+
+// coef[r] = sum_k partial[r][k] in a fixed order, r < nr; mode:
+//   0: plain sums into coef (and hsum when save_h)
+//   1: first pass: coef = [c | h] with h = V^T y - VB c   (VB: (j+1) x nb)
+// One block; rows handled one warp each.
+__global__ void lz_final(const double* __restrict__ partial, int nr, int nblocks, int nb,
+                         int jrows, const double* __restrict__ VB, int mode,
+                         double* __restrict__ coef, double* __restrict__ hsum) {
+  __shared__ double s[LZ_MAX_ROWS + 1];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = wid; r < nr; r += blockDim.x >> 5) {
+    double v = 0.0;
+    for (int k = lane; k < nblocks; k += 32) v += partial[(long long)r * nblocks + k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
+    if (lane == 0) s[r] = v;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+    double v = s[r];
+    if (mode == 1 && r >= nb) {
+      const int i = r - nb;
+      for (int b = 0; b < nb; b++) v -= VB[(long long)i * SP_MAX_BASIS + b] * s[b];
+    }
+    coef[r] = v;
+    if (hsum) hsum[r] = v;
+  }
+}
+
+// H[:j+1, j] = h1 + h2 (rows nb.. of the two coefficient sets), H[j+1, j] =
+// beta = sqrt(||w||^2); VB row j+1 = the dots of v_{j+1} with B
+__global__ void lz_write_h(const double* __restrict__ hsum, const double* __restrict__ coef2,
+                           int nb, int jrows, const double* __restrict__ partial_norm,
+                           int nblocks, double* __restrict__ H, int ncv, int j,
+                           double* __restrict__ beta) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < nblocks; k++) s += partial_norm[k];
+    const double bt = sqrt(s);
+    *beta = bt;
+    H[(long long)(j + 1) * ncv + j] = bt;
+  }
+  for (int i = threadIdx.x; i < jrows; i += blockDim.x)
+    H[(long long)i * ncv + j] = hsum[nb + i] + coef2[nb + i];
+}
+
+// xp = v - B vb, z = inv_sqrt * xp (the next operator input)
+__global__ void lz_prepare(int n, const double* __restrict__ v, const double* __restrict__ B,
+                           int nb, const double* __restrict__ vb,
+                           const double* __restrict__ inv_sqrt, double* __restrict__ xp,
+                           double* __restrict__ z) {
+  double c[SP_MAX_BASIS];
+#pragma unroll
+  for (int b = 0; b < SP_MAX_BASIS; b++) c[b] = b < nb ? vb[b] : 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double x = v[i];
+#pragma unroll
+    for (int b = 0; b < SP_MAX_BASIS; b++)
+      if (b < nb) x -= B[(long long)b * n + i] * c[b];
+    xp[i] = x;
+    z[i] = inv_sqrt[i] * x;
+  }
+}
+
 }  // namespace
 }  // namespace gu
 
@@ -182,5 +440,99 @@ extern "C" int gu_spectral_op(int64_t n, const int32_t* indptr, const int32_t* i
     spec_project<<<148 * 4, SP_THREADS, 0, st>>>(N, basis, nb, c2, y, y, inv_sqrt, nullptr);
     GU_CHECK_LAUNCH("spec_project");
   }
+  return GU_OK;
+}
+
+extern "C" size_t gu_lanczos_workspace_size(int64_t n) { return lz_layout(n, nullptr, nullptr); }
+
+// vb (device, nb doubles) = B^T v, and the operator input (xp, z) of v kept
+// in the workspace for the next gu_lanczos_step.
+extern "C" int gu_lanczos_prepare(int64_t n, const double* inv_sqrt, const double* basis,
+                                  int32_t nb, const double* v, double* vb, void* workspace,
+                                  size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 1 || n >= INT_MAX || nb < 0 || nb > SP_MAX_BASIS) {
+    set_error("gu_lanczos_prepare: bad arguments");
+    return GU_ERR_ARG;
+  }
+  LzWs ws;
+  if (!workspace || ws_bytes < lz_layout(n, (char*)workspace, &ws)) {
+    set_error("gu_lanczos_prepare: workspace too small");
+    return GU_ERR_WORKSPACE;
+  }
+  const int N = (int)n;
+  if (nb > 0) {  // vb = B^T v
+    lz_scale_dots<<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, v, nullptr, nullptr, basis, nb,
+                                                    ws.partial);
+    GU_CHECK_LAUNCH("lz_scale_dots");
+    lz_final<<<1, SP_THREADS, 0, st>>>(ws.partial, nb, LZ_BLOCKS, nb, 0, nullptr, 0, vb, nullptr);
+    GU_CHECK_LAUNCH("lz_final");
+  }
+  lz_prepare<<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, v, basis, nb, vb, inv_sqrt, ws.xp, ws.z);
+  GU_CHECK_LAUNCH("lz_prepare");
+  return GU_OK;
+}
+
+// One Lanczos step j (see the kernels above).  V: (ncv + 1) x n row-major,
+// rows 0..j filled, row j's operator input prepared (gu_lanczos_prepare or
+// the previous step); VB: (ncv + 1) x 4 row-major, rows 0..j = V_i^T B;
+// H: (ncv + 1) x ncv row-major.  Writes V row j + 1, VB row j + 1, H[:j+2, j]
+// and prepares row j + 1's operator input.  No host synchronisation.
+extern "C" int gu_lanczos_step(int64_t n, const int32_t* indptr, const int32_t* indices,
+                               const double* inv_sqrt, const double* basis, int32_t nb,
+                               double* V, double* VB, double* H, int32_t ncv, int32_t j,
+                               void* workspace, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 1 || n >= INT_MAX || nb < 0 || nb > SP_MAX_BASIS || ncv < 1 ||
+      ncv + 1 + SP_MAX_BASIS > LZ_MAX_ROWS || j < 0 || j >= ncv) {
+    set_error("gu_lanczos_step: bad arguments (n=%lld nb=%d ncv=%d j=%d)", (long long)n, nb,
+              ncv, j);
+    return GU_ERR_ARG;
+  }
+  LzWs ws;
+  if (!workspace || ws_bytes < lz_layout(n, (char*)workspace, &ws)) {
+    set_error("gu_lanczos_step: workspace too small");
+    return GU_ERR_WORKSPACE;
+  }
+  const int N = (int)n;
+  const int jrows = j + 1, nr = nb + jrows;
+  const long long rows_per_block = SP_THREADS / 8;
+  long long sblocks = (n + rows_per_block - 1) / rows_per_block;
+  if (sblocks > LZ_BLOCKS) sblocks = LZ_BLOCKS;
+  // pass 1: y = operator(v_j), dots [B; V]^T y
+  lz_spmv_dots<<<(unsigned)sblocks, SP_THREADS, 0, st>>>(N, indptr, indices, inv_sqrt, ws.xp,
+                                                         ws.z, ws.y, basis, nb, V, nr,
+                                                         ws.partial);
+  GU_CHECK_LAUNCH("lz_spmv_dots");
+  lz_final<<<1, SP_THREADS, 0, st>>>(ws.partial, nr, (int)sblocks, nb, jrows, VB, 1, ws.coef,
+                                     ws.hsum);
+  GU_CHECK_LAUNCH("lz_final");
+  // pass 2: w = y - B c - V h, dots [B; V]^T w
+  lz_update<true, false><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, ws.coef, ws.y,
+                                                           ws.w, ws.partial);
+  GU_CHECK_LAUNCH("lz_update");
+  lz_final<<<1, SP_THREADS, 0, st>>>(ws.partial, nr, LZ_BLOCKS, nb, jrows, nullptr, 0, ws.coef,
+                                     nullptr);
+  GU_CHECK_LAUNCH("lz_final");
+  // pass 3: w -= B c' + V h', ||w||^2 (partial row nr)
+  lz_update<false, true><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, ws.coef, ws.w,
+                                                           ws.w, ws.partial);
+  GU_CHECK_LAUNCH("lz_update");
+  lz_write_h<<<1, SP_THREADS, 0, st>>>(ws.hsum, ws.coef, nb, jrows,
+                                       ws.partial + (long long)nr * LZ_BLOCKS, LZ_BLOCKS, H, ncv,
+                                       j, ws.beta);
+  GU_CHECK_LAUNCH("lz_write_h");
+  // pass 4: v_{j+1} = w / beta, its dots with B, then its operator input
+  double* vnext = V + (long long)(j + 1) * n;
+  double* vbnext = VB + (long long)(j + 1) * SP_MAX_BASIS;
+  lz_scale_dots<<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, ws.w, ws.beta, vnext, basis, nb, ws.partial);
+  GU_CHECK_LAUNCH("lz_scale_dots");
+  if (nb > 0) {
+    lz_final<<<1, SP_THREADS, 0, st>>>(ws.partial, nb, LZ_BLOCKS, nb, 0, nullptr, 0, vbnext,
+                                       nullptr);
+    GU_CHECK_LAUNCH("lz_final");
+  }
+  lz_prepare<<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, vnext, basis, nb, vbnext, inv_sqrt, ws.xp, ws.z);
+  GU_CHECK_LAUNCH("lz_prepare");
   return GU_OK;
 }

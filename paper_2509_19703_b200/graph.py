@@ -169,10 +169,18 @@ def build_graph(edge_pairs, labels=None):
         pairs_list = list(edge_pairs)
         if not pairs_list:
             raise GraphError("empty graph")
+        # the integer fast path only for genuinely integral input: floats,
+        # bools, numeric strings and mixed labels keep their own values and
+        # sort order (the reference sorts the original labels)
         try:
-            pairs = np.asarray(pairs_list, dtype=np.int64).reshape(-1, 2)
-        except (TypeError, ValueError):
+            arr = np.asarray(pairs_list)
+        except (TypeError, ValueError, OverflowError):
+            arr = None
+        if (arr is None or arr.dtype.kind not in "iu" or arr.ndim != 2 or arr.shape[1] != 2):
             return _build_graph_labels(pairs_list)
+        if arr.dtype == np.uint64 and arr.size and int(arr.max()) > np.iinfo(np.int64).max:
+            return _build_graph_labels(pairs_list)
+        pairs = arr.astype(np.int64, copy=False)
     if pairs.shape[0] == 0:
         raise GraphError("empty graph")
     if pairs.shape[0] >= GPU_BUILD_MIN_PAIRS and _gpu_available() and int(pairs.min()) >= 0:
@@ -214,12 +222,31 @@ def _build_graph_gpu(pairs):
     return g
 
 
+def _labels_monotone(g):
+    """True when label order is vertex order (no labels, or strictly
+    increasing ones -- build_graph's dense relabel guarantees it), so the
+    smallest label of a component is the label of its smallest vertex id."""
+    labels = getattr(g, "labels", ()) or ()
+    if len(labels) < 2:
+        return True
+    try:
+        a = np.asarray(labels)
+        if a.dtype.kind in "iuf":
+            return bool(np.all(a[1:] > a[:-1]))
+        return all(labels[i] < labels[i + 1] for i in range(len(labels) - 1))
+    except TypeError:
+        return False
+
+
 def largest_connected_component(g):
     """Induced subgraph on the largest component, relabelled densely in id
     order, labels carried (graph.py:201-232); ties go to the component
-    holding the smallest vertex id.  On the GPU when one is present
-    (csrc/ingest.cu union-find + compaction)."""
-    if g.n >= 2 and _gpu_available():
+    holding the smallest original label (graph.py:211-214).  On the GPU when
+    one is present (csrc/ingest.cu union-find + compaction); graphs whose
+    labels are not in vertex order take the host path, whose tie rule
+    compares labels."""
+    monotone = _labels_monotone(g)
+    if g.n >= 2 and _gpu_available() and monotone:
         return _lcc_gpu(g)
     import scipy.sparse as sp
     from scipy.sparse import csgraph
@@ -231,7 +258,10 @@ def largest_connected_component(g):
         return g
     sizes = np.bincount(member, minlength=ncomp)
     best = np.flatnonzero(sizes == sizes.max())
-    if len(best) > 1:
+    if len(best) > 1 and not monotone:
+        labels = g.labels
+        champion = min(best, key=lambda c: min(labels[v] for v in np.flatnonzero(member == c)))
+    elif len(best) > 1:
         first_vertex = np.full(ncomp, g.n, dtype=np.int64)
         np.minimum.at(first_vertex, member, np.arange(g.n))
         champion = best[np.argmin(first_vertex[best])]

@@ -58,10 +58,13 @@ def _coords(layout, dev):
     return torch.from_numpy(xy).to(dev)
 
 
-def _sources(sources, dev):
+def _sources(sources, dev, n):
     if sources is None:
         return None
-    src = torch.from_numpy(np.ascontiguousarray(np.asarray(sources), dtype=np.int32)).to(dev)
+    s = np.asarray(sources)
+    if s.size and (s.dtype.kind not in "iu" or int(s.min()) < 0 or int(s.max()) >= n):
+        raise ValueError(f"sources must be vertex ids in [0, {n})")
+    src = torch.from_numpy(np.ascontiguousarray(s, dtype=np.int32)).to(dev)
     if src.numel() == 0 or int(torch.unique(src).numel()) != src.numel():
         raise ValueError("sources must be distinct vertex ids")
     return src
@@ -84,7 +87,7 @@ def neighborhood_preservation(g, layout, r=2, sources=None):
     slots = int(max(1, min(NP_MAX_SLOTS, NP_SCRATCH_BUDGET // (8 * n))))
     ws = workspace(lib.gu_np_workspace_size(n, slots), dev)
     out = torch.zeros(1, dtype=torch.float64, device=dev)
-    src = _sources(sources, dev)
+    src = _sources(sources, dev, g.n)
     _lib.call("gu_neighborhood_preservation", n, _lib.ptr(csr.indptr), _lib.ptr(csr.indices),
               _lib.ptr(xy), int(r), slots, _lib.ptr(src), 0 if src is None else src.numel(),
               _lib.ptr(out), _lib.ptr(ws), ws.numel(), stream_ptr(dev))
@@ -107,7 +110,7 @@ def stress(g, layout, rescale=True, sources=None):
     lib = _lib.load()
     ws = workspace(lib.gu_stress_workspace_size(n), dev)
     out = torch.zeros(3, dtype=torch.float64, device=dev)
-    src = _sources(sources, dev)
+    src = _sources(sources, dev, g.n)
     _lib.call("gu_stress", n, _lib.ptr(csr.indptr), _lib.ptr(csr.indices), _lib.ptr(xy),
               1 if rescale else 0, _lib.ptr(src), 0 if src is None else src.numel(),
               _lib.ptr(out), _lib.ptr(ws), ws.numel(), stream_ptr(dev))

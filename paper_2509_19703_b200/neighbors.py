@@ -609,9 +609,10 @@ def smooth_knn_weights(knn, k=None):
     sigma = torch.empty(n, dtype=torch.float64, device=dev)
     w = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
     st = stream_ptr(dev)
-    _lib.call("gu_smooth_knn", n, _lib.ptr(indptr), _lib.ptr(dist), kmax, target,
-              _lib.ptr(rho), _lib.ptr(sigma), _lib.ptr(w), st)
     lib = _lib.load()
+    sws = workspace(lib.gu_smooth_knn_workspace_size(n), dev)
+    _lib.call("gu_smooth_knn", n, _lib.ptr(indptr), _lib.ptr(dist), kmax, target,
+              _lib.ptr(rho), _lib.ptr(sigma), _lib.ptr(w), _lib.ptr(sws), sws.numel(), st)
     ws = workspace(lib.gu_symmetrize_workspace_size(n, nnz), dev)
     cap = max(2 * nnz, 1)
     sym_src = torch.empty(cap, dtype=torch.int32, device=dev)

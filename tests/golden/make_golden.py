@@ -442,6 +442,28 @@ def gen_spectral():
     save("spectral.npz", **out)
 
 
+def gen_spectral_c3():
+    """spectral_init of the reference on BASELINE c3 (BA n=100k, m0=3, seed
+    2; ARPACK, ~15 s here): coordinates (float32) and the three smallest
+    eigenvalues of L_sym (eigsh on 2I - L, the reference's own operator), so
+    the test can bound the coordinate difference by residual / gap."""
+    import scipy.sparse as sp
+    from scipy.sparse.linalg import eigsh
+    g = F.scale_free(100000, seed=2, m0=3)
+    rg = gu.build_graph([tuple(map(int, e)) for e in g.edges])
+    assert rg.n == g.n
+    lay = gu.spectral_init(rg, seed=2)
+    n = rg.n
+    deg = np.diff(rg.adj_indptr).astype(np.float64)
+    A = sp.csr_matrix((np.ones(rg.adj_indices.shape[0]), rg.adj_indices, rg.adj_indptr), shape=(n, n))
+    isq = sp.diags(1.0 / np.sqrt(deg))
+    M = sp.identity(n) + isq @ A @ isq   # 2I - L_sym
+    vals = eigsh(M, k=4, which="LM", tol=1e-10, return_eigenvectors=False)
+    lam = np.sort(2.0 - vals)
+    print("c3 lam", lam)
+    save("spectral_c3.npz", coords=np.asarray(lay.coords, np.float32), seed=np.array(2), lam=lam)
+
+
 def gen_sparsify():
     """sparsify.py:49-205 on dense graphs (m > n log2 n): the reference's exact
     resistances, its sparsifier's kept-edge mask, and its sketch resistances
@@ -548,6 +570,83 @@ def gen_quality_c2(nseeds=5):
     with mp.get_context("spawn").Pool(nseeds) as pool:
         lays = pool.map(_c2_seed, [(s, ep, g.n) for s in range(nseeds)])
     save("quality_c2.npz", layouts=np.stack(lays), n=np.array(g.n), m=np.array(g.m))
+
+def _ingest_cases():
+    """Inputs of the build_graph / largest_connected_component goldens
+    (graph.py:132-232): the recipe is shared with tests/test_ingest.py."""
+    rng = np.random.default_rng(303)
+    cases = []
+    # integers: non-contiguous ids, duplicates (both orientations), self loops
+    ids = rng.choice(10**9, size=300, replace=False)
+    pairs = [(int(ids[a]), int(ids[b])) for a, b in rng.integers(0, 300, size=(900, 2))]
+    cases.append(("ints", pairs))
+    cases.append(("strings", [("b", "a"), ("c", "b"), ("a", "b"), ("d", "d"), ("e", "f"),
+                              ("f", "e"), ("zz", "a")]))
+    # numeric strings sort as strings ("10" < "8" < "9")
+    cases.append(("numeric_strings", [("10", "9"), ("9", "8"), ("8", "10"), ("100", "7"),
+                                      ("7", "8")]))
+    # floats keep their values: (1.5, 1.7) is an edge, not a self loop
+    cases.append(("floats", [(1.5, 1.7), (1.7, 2.5), (2.5, 1.5), (0.25, 3.0), (3.0, 3.0)]))
+    # several components of different sizes, a size tie for the runner-up
+    comp = [(i, i + 1) for i in range(0, 9)] + [(20, 21), (21, 22), (30, 31), (31, 32),
+                                                 (40, 41)]
+    cases.append(("components", comp))
+    return cases
+
+
+def _ingest_tie_graph(gu_mod):
+    """Two equal-size components whose smallest labels are NOT in vertex
+    order: the reference's tie rule (graph.py:211-214) takes the component
+    holding the smallest label (vertices 3..5, labels 10..12)."""
+    edges = np.array([(0, 1), (1, 2), (3, 4), (4, 5)], np.int64)
+    labels = (50, 51, 52, 10, 11, 12)
+    if hasattr(gu_mod, "graph_from_edges"):
+        return gu_mod.graph_from_edges(6, edges, labels=labels)
+    from graph_umap.graph import _from_canonical, Graph
+    n, m, ip, ix, e = _from_canonical(6, edges, labels)
+    return Graph(n=n, m=m, adj_indptr=ip, adj_indices=ix, edges=e, labels=labels)
+
+
+def _graph_json(g):
+    return dict(n=int(g.n), m=int(g.m), edges=np.asarray(g.edges).tolist(),
+                labels=list(g.labels), dropped_self_loops=int(g.dropped_self_loops),
+                dropped_duplicates=int(g.dropped_duplicates),
+                indptr=np.asarray(g.adj_indptr).tolist(),
+                indices=np.asarray(g.adj_indices).tolist())
+
+
+def gen_ingest():
+    """build_graph / largest_connected_component outputs of the live
+    reference (graph.py:132-232) for small label-typed inputs, a large
+    integer input (the GPU build path; digests only) and the label tie."""
+    from graph_umap.graph import largest_connected_component as ref_lcc
+    out = {"cases": []}
+    for name, pairs in _ingest_cases():
+        g = gu.build_graph(pairs)
+        out["cases"].append(dict(name=name, pairs=[list(p) for p in pairs], graph=_graph_json(g),
+                                 lcc=_graph_json(ref_lcc(g))))
+    tie = _ingest_tie_graph(gu)
+    out["tie"] = dict(graph=_graph_json(tie), lcc=_graph_json(ref_lcc(tie)))
+    # large integer input: 200k random pairs over 60k ids below 2^40 (many
+    # components); the GPU build and LCC paths engage at this size
+    rng = np.random.default_rng(404)
+    idv = rng.choice(2**40, size=60000, replace=False)
+    pairs = idv[rng.integers(0, 60000, size=(200000, 2))]
+    g = gu.build_graph([(int(a), int(b)) for a, b in pairs])
+    h = ref_lcc(g)
+    out["large"] = dict(seed=404, nids=60000, npairs=200000, n=int(g.n), m=int(g.m),
+                        dropped_self_loops=int(g.dropped_self_loops),
+                        dropped_duplicates=int(g.dropped_duplicates),
+                        edges_sha=sha(np.asarray(g.edges, np.int64)),
+                        labels_sha=sha(np.asarray(g.labels, np.int64)),
+                        lcc_n=int(h.n), lcc_m=int(h.m),
+                        lcc_edges_sha=sha(np.asarray(h.edges, np.int64)),
+                        lcc_labels_sha=sha(np.asarray(h.labels, np.int64)))
+    path = os.path.join(HERE, "ingest.json")
+    with open(path, "w") as f:
+        json.dump(out, f)
+    print("wrote", path, os.path.getsize(path), "bytes")
+
 
 def main():
     # quality_c3_full (~1.5 h on 8 cores) runs only when named

@@ -492,7 +492,42 @@ def test_sgd_neighbor_filter_covers_neighbors(gu):
     ip, ix = gk.nbr_indptr, gk.nbr_indices
     src = np.repeat(np.arange(gk.n), np.diff(ip))
     assert filt.shape == (gk.n, 2)
-    for mult in (0x9E3779B1, 0x85EBCA77):  # the two hash bits of an id
-        h = ((ix.astype(np.uint64) * np.uint64(mult)) & np.uint64(0xFFFFFFFF)) >> np.uint64(26)
-        words = filt[src, (h >> np.uint64(5)).astype(np.int64)]
-        assert np.all((words >> (h & np.uint64(31)).astype(np.uint32)) & 1)
+    _bloom_covers(filt[src], ix, (0x9E3779B1, 0x85EBCA77), 26)
+
+
+def _bloom_covers(words, ids, mults, shift):
+    """Every id has all of its hash bits set in the row's word."""
+    for mult in mults:
+        h = ((ids.astype(np.uint64) * np.uint64(mult)) & np.uint64(0xFFFFFFFF)) >> np.uint64(shift)
+        w = words[np.arange(ids.shape[0]), (h >> np.uint64(5)).astype(np.int64)]
+        assert np.all((w >> (h & np.uint64(31)).astype(np.uint32)) & 1)
+
+
+def test_sgd_record_filter_covers_neighbors(gu):
+    """32-byte edge records (GPU-filling epochs) carry their head's 128-bit
+    Bloom word (3 hash bits per id): every neighbour of the head is covered,
+    and the records hold the sym edges in the plan's order."""
+    from paper_2509_19703_b200 import _lib
+    from paper_2509_19703_b200.layout import SgdPlan
+    import torch
+
+    g = gu.synth_graph("scale_free", 700_000, seed=4, m0=3)  # cap n/4 fills the GPU
+    _, knn = gu.partial_bfs(g, 15, seed=1)
+    gk = gu.smooth_knn_weights(knn)
+    assert _lib.load().gu_sgd_record_bytes_for(0) == 32
+    plan = SgdPlan(gk, 0, torch.device("cuda"))
+    if plan.record_bytes != 32:
+        pytest.skip("this graph's concurrency cap keeps 16-byte records")
+    rec = plan.edges.cpu().numpy()
+    perm = plan.perm.cpu().numpy()
+    assert np.array_equal(rec[:, 0], gk.sym_src[perm]) and np.array_equal(rec[:, 1], gk.sym_dst[perm])
+    words = rec[:, 4:8].view(np.uint32)
+    ip, ix = gk.nbr_indptr, gk.nbr_indices
+    heads = rec[:, 0]
+    # check the words of a sample of records against their head's full row
+    pick = np.random.default_rng(0).choice(rec.shape[0], size=20000, replace=False)
+    for i in pick[:2000]:
+        u = heads[i]
+        row = ix[ip[u]:ip[u + 1]]
+        _bloom_covers(np.repeat(words[i:i + 1], row.shape[0], axis=0), row,
+                      (0x9E3779B1, 0x85EBCA77, 0xC2B2AE3D), 25)
