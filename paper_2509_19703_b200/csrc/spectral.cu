@@ -140,7 +140,7 @@ int launch_dots(int n, const double* B, int nb, const double* x, double* partial
 // reduction is partials per block then one block summing them in a fixed
 // order (deterministic).  Replaces four cuBLAS GEMV passes, a norm and a
 // scale per step (the torch loop of round 1).
-constexpr int LZ_MAX_ROWS = SP_MAX_BASIS + 64;  // B rows + V rows (ncv <= 63)
+constexpr int LZ_MAX_ROWS = SP_MAX_BASIS + 36;  // B rows + V rows (ncv <= 35)
 constexpr int LZ_BLOCKS = 148 * 4;
 
 struct LzWs {
@@ -214,91 +214,74 @@ __device__ __forceinline__ void lz_block_partials(const double (&acc)[NACC], int
   __syncthreads();  // sh is reused by the next call
 }
 
-// pass 1: y = xp + inv_sqrt * (A z), 8 lanes per row; lane g8 of a row's
-// group accumulates the dots of y with rows g8, g8 + 8, ... of [B; V]
-__global__ void __launch_bounds__(SP_THREADS)
-    lz_spmv_dots(int n, const int* __restrict__ indptr, const int* __restrict__ indices,
-                 const double* __restrict__ inv_sqrt, const double* __restrict__ xp,
-                 const double* __restrict__ z, double* __restrict__ y,
-                 const double* __restrict__ B, int nb, const double* __restrict__ V, int nr,
-                 double* __restrict__ partial) {
-  constexpr int NACC = LZ_MAX_ROWS / 8;
-  const int g8 = threadIdx.x & 7;
-  const unsigned gmask = 0xffu << (threadIdx.x & 24);
-  double acc[NACC];
-#pragma unroll
-  for (int q = 0; q < NACC; q++) acc[q] = 0.0;
-  // a block-uniform trip count (every thread reaches the reductions)
-  const int rows_per_iter = (gridDim.x * SP_THREADS) >> 3;
-  for (int v0 = (blockIdx.x * SP_THREADS) >> 3; v0 < n; v0 += rows_per_iter) {
-    const int v = v0 + (threadIdx.x >> 3);
-    double yv = 0.0;
-    if (v < n) {
-      const int b = __ldg(indptr + v), e = __ldg(indptr + v + 1);
-      double s = 0.0;
-      for (int p = b + g8; p < e; p += 8) s += z[__ldg(indices + p)];
-      s += __shfl_xor_sync(gmask, s, 4, 8);
-      s += __shfl_xor_sync(gmask, s, 2, 8);
-      s += __shfl_xor_sync(gmask, s, 1, 8);
-      yv = xp[v] + inv_sqrt[v] * s;
-      if (g8 == 0) y[v] = yv;
-#pragma unroll
-      for (int q = 0; q < NACC; q++) {
-        const int r = g8 + 8 * q;
-        if (r < nr) acc[q] = fma(lz_row(B, nb, V, n, r)[v], yv, acc[q]);
-      }
-    }
-  }
-  lz_block_partials<NACC>(acc, g8, 8, 0, nr, partial);
-}
-
-// out = x - sum_r rows_r * coef_r (rows of [B; V], nr of them); optional
-// dots of out with every row (partial) and ||out||^2 (partial row nr)
+// out = x - sum_r row_r * coef_r over the rows of [B; V] (nr of them;
+// coef null: out = x), optionally the dots of out with every row (partial
+// rows 0..nr-1) and ||out||^2 (partial row nr).  Thread per element: the nr
+// row values of element i are loaded coalesced (consecutive threads,
+// consecutive i of one row) and kept in registers for the dots, which are
+// reduced per warp by butterfly shuffles; lane r & 31 keeps row r's sum.
 template <bool DOTS, bool NORM>
-__global__ void __launch_bounds__(SP_THREADS)
-    lz_update(int n, const double* __restrict__ B, int nb, const double* __restrict__ V, int nr,
-              const double* __restrict__ coef, const double* __restrict__ x,
-              double* __restrict__ out, double* __restrict__ partial) {
-  constexpr int NACC = LZ_MAX_ROWS / 8 + 1;
+__global__ void __launch_bounds__(SP_THREADS, 2)
+    lz_rows(int n, const double* __restrict__ B, int nb, const double* __restrict__ V, int nr,
+            const double* __restrict__ coef, const double* __restrict__ x,
+            double* __restrict__ out, double* __restrict__ partial) {
   __shared__ double c[LZ_MAX_ROWS];
-  for (int r = threadIdx.x; r < nr; r += blockDim.x) c[r] = coef[r];
+  __shared__ double sh[LZ_MAX_ROWS + 1][SP_THREADS / 32];
+  for (int r = threadIdx.x; r < LZ_MAX_ROWS; r += blockDim.x)
+    c[r] = (coef && r < nr) ? coef[r] : 0.0;
   __syncthreads();
-  const int g8 = threadIdx.x & 7;
-  double acc[NACC];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NA = (LZ_MAX_ROWS + 31) / 32;
+  double acc[NA];
 #pragma unroll
-  for (int q = 0; q < NACC; q++) acc[q] = 0.0;
-  // 8 consecutive threads share an element: lane g8 does rows g8, g8+8, ...
-  const int per_iter = (gridDim.x * SP_THREADS) >> 3;
-  for (int i0 = (blockIdx.x * SP_THREADS) >> 3; i0 < n; i0 += per_iter) {
-    const int i = i0 + (threadIdx.x >> 3);
-    if (i < n) {
-      double s = 0.0;
-      for (int r = g8; r < nr; r += 8) s += lz_row(B, nb, V, n, r)[i] * c[r];
-      const unsigned gmask = 0xffu << (threadIdx.x & 24);
-      s += __shfl_xor_sync(gmask, s, 4, 8);
-      s += __shfl_xor_sync(gmask, s, 2, 8);
-      s += __shfl_xor_sync(gmask, s, 1, 8);
-      const double o = x[i] - s;
-      if (g8 == 0) out[i] = o;
-      if (DOTS) {
+  for (int q = 0; q < NA; q++) acc[q] = 0.0;
+  double nacc = 0.0;
+  const int stride = gridDim.x * blockDim.x;
+  // block-uniform trip count: every lane reaches the shuffles
+  for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+    const int i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    double vals[LZ_MAX_ROWS];
 #pragma unroll
-        for (int q = 0; q < NACC - 1; q++) {
-          const int r = g8 + 8 * q;
-          if (r < nr) acc[q] = fma(lz_row(B, nb, V, n, r)[i], o, acc[q]);
+    for (int r = 0; r < LZ_MAX_ROWS; r++)
+      vals[r] = (ok && r < nr) ? __ldg(lz_row(B, nb, V, n, r) + i) : 0.0;
+    double o = ok ? x[i] : 0.0;
+    if (coef) {
+#pragma unroll
+      for (int r = 0; r < LZ_MAX_ROWS; r++) o -= vals[r] * c[r];
+    }
+    if (out && ok) out[i] = o;
+    if (DOTS) {
+#pragma unroll
+      for (int r = 0; r < LZ_MAX_ROWS; r++) {
+        if (r < nr) {  // block-uniform
+          double s = vals[r] * o;
+#pragma unroll
+          for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(FULL, s, m);
+          if (lane == (r & 31)) acc[r >> 5] += s;
         }
       }
-      if (NORM && g8 == 0) acc[NACC - 1] = fma(o, o, acc[NACC - 1]);
+    }
+    if (NORM) nacc = fma(o, o, nacc);
+  }
+  if (DOTS) {
+#pragma unroll
+    for (int q = 0; q < NA; q++) {
+      const int r = q * 32 + lane;
+      if (r < nr) sh[r][wid] = acc[q];
     }
   }
-  if (DOTS) {  // rows 0..nr-1 from the 8-lane groups
-    double head[NACC - 1];
+  if (NORM) {
 #pragma unroll
-    for (int q = 0; q < NACC - 1; q++) head[q] = acc[q];
-    lz_block_partials<NACC - 1>(head, g8, 8, 0, nr, partial);
+    for (int m = 16; m > 0; m >>= 1) nacc += __shfl_xor_sync(FULL, nacc, m);
+    if (lane == 0) sh[nr][wid] = nacc;
   }
-  if (NORM) {  // ||out||^2 into row nr (only lanes with g8 == 0 hold a share)
-    const double v[1] = {acc[NACC - 1]};
-    lz_block_partials<1>(v, nr, 1, nr, nr + 1, partial);
+  __syncthreads();
+  const int r0 = DOTS ? 0 : nr, r1 = NORM ? nr + 1 : nr;
+  for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < SP_THREADS / 32; k++) s += sh[r][k];
+    partial[(long long)r * gridDim.x + blockIdx.x] = s;
   }
 }
 
@@ -498,26 +481,28 @@ extern "C" int gu_lanczos_step(int64_t n, const int32_t* indptr, const int32_t* 
   const int jrows = j + 1, nr = nb + jrows;
   const long long rows_per_block = SP_THREADS / 8;
   long long sblocks = (n + rows_per_block - 1) / rows_per_block;
-  if (sblocks > LZ_BLOCKS) sblocks = LZ_BLOCKS;
-  // pass 1: y = operator(v_j), dots [B; V]^T y
-  lz_spmv_dots<<<(unsigned)sblocks, SP_THREADS, 0, st>>>(N, indptr, indices, inv_sqrt, ws.xp,
-                                                         ws.z, ws.y, basis, nb, V, nr,
-                                                         ws.partial);
-  GU_CHECK_LAUNCH("lz_spmv_dots");
-  lz_final<<<1, SP_THREADS, 0, st>>>(ws.partial, nr, (int)sblocks, nb, jrows, VB, 1, ws.coef,
+  if (sblocks > 148 * 16) sblocks = 148 * 16;
+  // pass 1: y = operator(v_j), then the dots [B; V]^T y
+  spec_spmv<<<(unsigned)sblocks, SP_THREADS, 0, st>>>(N, indptr, indices, inv_sqrt, ws.xp, ws.z,
+                                                      ws.y);
+  GU_CHECK_LAUNCH("spec_spmv");
+  lz_rows<true, false><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, nullptr, ws.y,
+                                                         nullptr, ws.partial);
+  GU_CHECK_LAUNCH("lz_rows");
+  lz_final<<<1, SP_THREADS, 0, st>>>(ws.partial, nr, LZ_BLOCKS, nb, jrows, VB, 1, ws.coef,
                                      ws.hsum);
   GU_CHECK_LAUNCH("lz_final");
   // pass 2: w = y - B c - V h, dots [B; V]^T w
-  lz_update<true, false><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, ws.coef, ws.y,
-                                                           ws.w, ws.partial);
-  GU_CHECK_LAUNCH("lz_update");
+  lz_rows<true, false><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, ws.coef, ws.y,
+                                                         ws.w, ws.partial);
+  GU_CHECK_LAUNCH("lz_rows");
   lz_final<<<1, SP_THREADS, 0, st>>>(ws.partial, nr, LZ_BLOCKS, nb, jrows, nullptr, 0, ws.coef,
                                      nullptr);
   GU_CHECK_LAUNCH("lz_final");
   // pass 3: w -= B c' + V h', ||w||^2 (partial row nr)
-  lz_update<false, true><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, ws.coef, ws.w,
-                                                           ws.w, ws.partial);
-  GU_CHECK_LAUNCH("lz_update");
+  lz_rows<false, true><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, ws.coef, ws.w,
+                                                         ws.w, ws.partial);
+  GU_CHECK_LAUNCH("lz_rows");
   lz_write_h<<<1, SP_THREADS, 0, st>>>(ws.hsum, ws.coef, nb, jrows,
                                        ws.partial + (long long)nr * LZ_BLOCKS, LZ_BLOCKS, H, ncv,
                                        j, ws.beta);

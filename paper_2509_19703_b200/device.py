@@ -126,7 +126,7 @@ def _par_copyto(dst, src):
     pool = _copy_pool()
     parts = pool._max_workers
     n = dst.shape[0]
-    if n < (1 << 20) or parts <= 1:
+    if n < (1 << 18) or parts <= 1:
         np.copyto(dst, src)
         return
     bounds = np.linspace(0, n, parts + 1).astype(np.int64)
@@ -185,8 +185,10 @@ def to_device(a, dtype, device):
         dev.copy_(src, non_blocking=True)
         torch.cuda.current_stream(device).synchronize()  # the caller may reuse `a`
         return dev
-    # chunked, double-buffered: the host copy of chunk i+1 overlaps the DMA of i
+    # chunked, double-buffered: the host copy of chunk i+1 (split over host
+    # threads) overlaps the DMA of chunk i
     flat = src.reshape(-1)
+    aflat = a.reshape(-1)
     dev = torch.empty(flat.shape, dtype=src.dtype, device=device)
     chunk = max(1, _UPLOAD_CHUNK_BYTES // src.element_size())
     bufs = [torch.empty(min(chunk, flat.numel()), dtype=src.dtype, pin_memory=True)
@@ -198,7 +200,7 @@ def to_device(a, dtype, device):
         b = i & 1
         if evs[b] is not None:
             evs[b].synchronize()  # the DMA that last read this buffer is done
-        bufs[b][: hi - lo].copy_(flat[lo:hi])
+        _par_copyto(bufs[b][: hi - lo].numpy(), aflat[lo:hi])
         dev[lo:hi].copy_(bufs[b][: hi - lo], non_blocking=True)
         evs[b] = torch.cuda.Event()
         evs[b].record(stream)
