@@ -475,9 +475,10 @@ def _sgd_bench(gu, g, args, dev, peak):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": _profile_traffic("sgd_epoch_kernel"),
                          "alg_bytes_per_update": 88,
-                         "limiter": "per-visit dependent chain (record -> endpoints and filter -> "
-                                    "row test) at 48% occupancy (64 registers); 49% long-scoreboard "
-                                    "stalls (profiles/r01_ncu_sgd.txt, DESIGN.md K7)"},
+                         "limiter": "per-visit latency and issue: 47% occupancy (64 registers), "
+                                    "57% issue active; stalls long-scoreboard 34%, wait 23%; the "
+                                    "128-bit filter test is ~27% of the instructions; DRAM at 10% "
+                                    "of peak (profiles/r02_ncu_sgd_rec32.txt, DESIGN.md K7)"},
             "diverged": int(div.item()) != INT32_MAX}
 
 
