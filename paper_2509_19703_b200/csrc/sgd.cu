@@ -137,9 +137,12 @@ struct Filt64 {
   using Word = uint2;
   static constexpr int K = 2, SHIFT = 26;  // 32 - log2(64)
 };
+#ifndef SGD_F128_K
+#define SGD_F128_K 3
+#endif
 struct Filt128 {
   using Word = uint4;
-  static constexpr int K = 3, SHIFT = 25;  // 32 - log2(128)
+  static constexpr int K = SGD_F128_K, SHIFT = 25;  // 32 - log2(128)
 };
 using FiltWord = Filt64::Word;
 

@@ -116,7 +116,8 @@ def _copy_pool():
     if _COPY_POOL is None:
         import concurrent.futures
         import os
-        _COPY_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+        nt = int(os.environ.get("GU_COPY_THREADS", "0")) or min(8, os.cpu_count() or 1)
+        _COPY_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=nt)
     return _COPY_POOL
 
 
