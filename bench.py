@@ -442,7 +442,11 @@ def _sgd_bench(gu, g, args, dev, peak):
     gk = gu.smooth_knn_weights(knn)
     E = gk.edge_count
     a, b = gu.fit_ab(0.1, 1.0)
+    torch.cuda.synchronize()
+    tp0 = time.perf_counter()
     plan = _plan_for(gk, SEED, dev)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - tp0
     init = np.random.default_rng(SEED).uniform(-10, 10, size=(g.n, 2)).astype(np.float32)
     xy = torch.from_numpy(init).to(dev)
     div = torch.full((1,), INT32_MAX, dtype=torch.int32, device=dev)
@@ -450,7 +454,7 @@ def _sgd_bench(gu, g, args, dev, peak):
     st = torch.cuda.current_stream()
 
     def epochs(e0, e1):
-        _lib.call("gu_sgd_epochs", plan.n, plan.E, _lib.ptr(xy), _lib.ptr(plan.edges), plan.record_bytes,
+        _lib.call("gu_sgd_epochs", plan.n, plan.E, _lib.ptr(xy), _lib.ptr(plan.edges), plan.record_mode,
                   _lib.ptr(plan.nbr_indptr), _lib.ptr(plan.nbr_indices), _lib.ptr(plan.filter), float(a), float(b),
                   1.0, T, e0, e1, 5, E, 0, plan.seed, sgd_concurrency(plan.n), _lib.ptr(div),
                   stream_ptr(dev))
@@ -472,6 +476,10 @@ def _sgd_bench(gu, g, args, dev, peak):
     achieved = 88.0 * E / (ms / 1e3) / 1e9
     return {"metric": "SGD edge-updates/s (full epoch, 5 negatives, fp32 Hogwild)",
             "value": round(ups, 1), "unit": "updates/s", "E": E, "ms_per_epoch": round(ms, 4),
+            "records": {0: "16-byte + gathered 64-bit filter", 1: "32-byte with 128-bit filter",
+                        2: "32-byte with neighbour-id window (BFS locality order)"}[plan.record_mode],
+            "mean_window_frac": getattr(plan, "mean_window", None),
+            "plan_seconds": round(plan_s, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": _profile_traffic("sgd_epoch_kernel"),

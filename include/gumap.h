@@ -147,17 +147,41 @@ int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* 
  * (2 hash bits per id) from gu_sgd_neighbor_filter (8 bytes x n); a negative
  * with a clear bit skips the row search (exact: a hit still searches). */
 /* Edge-record layout for a concurrency cap: 32 bytes (the record carries
- * its head's 128-bit neighbour Bloom word; GPU-filling epochs) or 16 bytes
- * (the 64-bit table of gu_sgd_neighbor_filter is gathered; small caps). */
+ * its head's filter; GPU-filling epochs) or 16 bytes (the 64-bit table of
+ * gu_sgd_neighbor_filter is gathered; small caps). */
 int32_t gu_sgd_record_bytes_for(int64_t concurrency);
+/* record_mode: 0 = 16-byte records + table, 1 = 32-byte records with the
+ * head's 128-bit Bloom word, 2 = 32-byte records with [min, max] of the
+ * head's neighbour ids and its 64-bit word (for ids in a locality order,
+ * gu_bfs_order).  relabel (nullable): old id -> new id; nbr_indptr /
+ * nbr_indices are then the neighbour CSR in the new ids. */
 int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
                          const double* sym_w, const int32_t* nbr_indptr,
-                         const int32_t* nbr_indices, int32_t record_bytes, uint64_t seed,
-                         void* edges, int32_t* perm_out, void* stream);
+                         const int32_t* nbr_indices, const int32_t* relabel, int32_t record_mode,
+                         uint64_t seed, void* edges, int32_t* perm_out, void* stream);
+/* REC_RANGE records (record_mode 2) in a local stored order: the edges in
+ * the order of the relabelled neighbour CSR (new_indptr / new_indices from
+ * gu_bfs_order), shuffled inside blocks of `block` consecutive edges, so an
+ * epoch tile touches nearby vertices; perm_out maps positions to the sym edge
+ * ids of the caller's CSR (nbr_indptr / nbr_indices, rows sorted). */
+int gu_sgd_prepare_edges_local(int64_t n, int64_t E, const double* sym_w,
+                               const int32_t* new_indptr, const int32_t* new_indices,
+                               const int32_t* order, const int32_t* nbr_indptr,
+                               const int32_t* nbr_indices, int64_t block, uint64_t seed,
+                               void* edges, int32_t* perm_out, void* stream);
+/* Locality order of a symmetric graph for the SGD epochs (csrc/order.cu):
+ * vertices sorted by (BFS level from a pseudo-peripheral vertex, id), the
+ * unreached last.  order[new] = old, perm[old] = new; new_indptr /
+ * new_indices (nullable) receive the graph in the new ids (rows sorted);
+ * host_levels[2] the depths of the two BFS sweeps.  Synchronous. */
+size_t gu_bfs_order_workspace_size(int64_t n, int64_t m);
+int gu_bfs_order(int64_t n, const int32_t* indptr, const int32_t* indices, int32_t* order,
+                 int32_t* perm, int32_t* new_indptr, int32_t* new_indices, int32_t* host_levels,
+                 void* workspace, size_t ws_bytes, void* stream);
 int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr, const int32_t* nbr_indices,
                            void* filter_out, void* stream);
 int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges,
-                  int32_t record_bytes, const int32_t* nbr_indptr, const int32_t* nbr_indices,
+                  int32_t record_mode, const int32_t* nbr_indptr, const int32_t* nbr_indices,
                   const void* nbr_filter, float a, float b,
                   float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
                   int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
@@ -172,7 +196,7 @@ int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges,
  * order the atomics land in.  Replaces the same _run_sgd loop as
  * gu_sgd_epochs (layout.py:314-360). */
 int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_xy, const void* edges,
-                                int32_t record_bytes, const int32_t* nbr_indptr,
+                                int32_t record_mode, const int32_t* nbr_indptr,
                                 const int32_t* nbr_indices,
                                 const void* nbr_filter, float a, float b, float lr0, int32_t t,
                                 int32_t epoch_begin, int32_t epoch_end, int32_t n_neg,

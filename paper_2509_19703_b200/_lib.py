@@ -92,8 +92,12 @@ SIGNATURES = {
     "gu_symmetrize": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      ctypes.POINTER(_c_i64), _vp, _c_sz, _vp]),
     "gu_sgd_record_bytes_for": (_c_i32, [_c_i64]),
-    "gu_sgd_prepare_edges": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_u64, _vp,
-                                            _vp, _vp]),
+    "gu_sgd_prepare_edges": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_u64,
+                                            _vp, _vp, _vp]),
+    "gu_sgd_prepare_edges_local": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                                  _c_i64, _c_u64, _vp, _vp, _vp]),
+    "gu_bfs_order_workspace_size": (_c_sz, [_c_i64, _c_i64]),
+    "gu_bfs_order": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_sz, _vp]),
     "gu_sgd_neighbor_filter": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
     "gu_sgd_epochs": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _c_i32, _vp, _vp, _vp, _c_f32,
                                      _c_f32, _c_f32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i64,

@@ -146,6 +146,14 @@ struct Filt128 {
 };
 using FiltWord = Filt64::Word;
 
+// edge-record layouts (gu_sgd_prepare_edges / gu_sgd_epochs `record_mode`)
+enum RecMode : int {
+  REC_TABLE = 0,  // 16 bytes; the head's 64-bit word gathered from the per-vertex table
+  REC_BLOOM = 1,  // 32 bytes; + the head's 128-bit / 3-hash Bloom word
+  REC_RANGE = 2,  // 32 bytes; + [min, max] of the head's neighbour ids and its
+                  // 64-bit / 2-hash word (ids in a locality order, csrc/order.cu)
+};
+
 template <class F>
 __device__ __forceinline__ unsigned filt_bit(int c, int j) {
   const unsigned m = j == 0 ? 0x9E3779B1u : (j == 1 ? 0x85EBCA77u : 0xC2B2AE3Du);
@@ -198,24 +206,77 @@ __device__ __forceinline__ bool filt_maybe(const typename F::Word& f, int c) {
 // << 6) | degree when both fit (start < 2^26, degree < 63), else -1 (the
 // kernel then reads nbr_indptr) -- the first rejection probe can then issue
 // straight after the coalesced record load.  32-byte records append the
-// head's 128-bit Bloom word.
+// head's filter (REC_BLOOM: 128-bit word; REC_RANGE: min / max neighbour id
+// and the 64-bit word).  relabel (nullable): old id -> new id; nip / nix are
+// then the graph in the new ids, and src / dst are mapped through it.
 __global__ void prepare_edges_kernel(long long E, const int* __restrict__ src,
                                      const int* __restrict__ dst, const double* __restrict__ w,
                                      const int* __restrict__ nip, const int* __restrict__ nix,
-                                     int rec_int4, unsigned long long key, int4* __restrict__ out,
+                                     const int* __restrict__ relabel, int mode,
+                                     unsigned long long key, int4* __restrict__ out,
                                      int* __restrict__ perm_out) {
   Feistel perm((unsigned long long)E, key);
+  const int rw = mode == REC_TABLE ? 1 : 2;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E;
        p += (long long)gridDim.x * blockDim.x) {
     const long long e = (long long)perm((unsigned long long)p);
-    const int u = src[e];
+    const int u = relabel ? relabel[src[e]] : src[e];
+    const int v = relabel ? relabel[dst[e]] : dst[e];
     const int rb = nip[u], deg = nip[u + 1] - rb;
     const int row = (rb < (1 << 26) && deg < 63) ? ((rb << 6) | deg) : -1;
-    out[rec_int4 * p] = make_int4(u, dst[e], __float_as_int((float)w[e]), row);
-    if (rec_int4 == 2) {
+    out[rw * p] = make_int4(u, v, __float_as_int((float)w[e]), row);
+    if (mode == REC_BLOOM) {
       const uint4 f = row_filter<Filt128>(nix, rb, rb + deg);
       out[2 * p + 1] = make_int4((int)f.x, (int)f.y, (int)f.z, (int)f.w);
+    } else if (mode == REC_RANGE) {
+      const uint2 f = row_filter<Filt64>(nix, rb, rb + deg);
+      const int lo = deg > 0 ? nix[rb] : INT_MAX, hi = deg > 0 ? nix[rb + deg - 1] : -1;
+      out[2 * p + 1] = make_int4(lo, hi, (int)f.x, (int)f.y);
     }
+    if (perm_out) perm_out[p] = (int)e;
+  }
+}
+
+// REC_RANGE records in a local stored order: the edges in the order of the
+// relabelled neighbour CSR (heads ascending in the BFS locality order), then
+// shuffled inside blocks of `block` consecutive edges.  A 1024-edge epoch tile
+// then touches the coordinates of a few thousand nearby vertices (~22 KB at
+// c5) instead of ~1024 scattered ones; tiles still run in a fresh random
+// order every epoch.  order: new id -> old id; nip_old / nix_old: the
+// caller's neighbour CSR, whose entry index is the sym edge id (rows sorted).
+__global__ void prepare_edges_local(long long E, const double* __restrict__ w, int n,
+                                    const int* __restrict__ nip, const int* __restrict__ nix,
+                                    const int* __restrict__ order,
+                                    const int* __restrict__ nip_old,
+                                    const int* __restrict__ nix_old, long long block,
+                                    unsigned long long key, int4* __restrict__ out,
+                                    int* __restrict__ perm_out) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long blk = p / block, b0 = blk * block;
+    const long long bsize = (E - b0) < block ? (E - b0) : block;
+    Feistel fp((unsigned long long)bsize, mix64(key ^ (0x9E3779B97F4A7C15ull * (blk + 1))));
+    const long long q = b0 + (long long)fp((unsigned long long)(p - b0));
+    // head: the row holding entry q (upper bound in the new offsets)
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (nip[mid] <= q) lo = mid; else hi = mid;
+    }
+    const int u = lo, v = nix[q];
+    const int ou = order[u], ov = order[v];
+    int a = nip_old[ou], b = nip_old[ou + 1];
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (nix_old[mid] < ov) a = mid + 1; else b = mid;
+    }
+    const long long e = a;
+    const int rb = nip[u], deg = nip[u + 1] - rb;
+    const int row = (rb < (1 << 26) && deg < 63) ? ((rb << 6) | deg) : -1;
+    out[2 * p] = make_int4(u, v, __float_as_int((float)w[e]), row);
+    const uint2 f = row_filter<Filt64>(nix, rb, rb + deg);
+    out[2 * p + 1] = make_int4(deg > 0 ? nix[rb] : INT_MAX, deg > 0 ? nix[rb + deg - 1] : -1,
+                               (int)f.x, (int)f.y);
     if (perm_out) perm_out[p] = (int)e;
   }
 }
@@ -226,7 +287,7 @@ constexpr int SGD_WARPS = 8;  // 256 threads per block at most (block_for)
 // GPU-filling epochs, 2 (96 registers) for the small-cap 16-lane mode, whose
 // few resident warps are latency-bound and gain from the longer register
 // budget (c3 epoch 0.295 -> 0.276 ms; at 96 registers c5 would lose 8%)
-template <int LANES, int MINB, bool REC32>
+template <int LANES, int MINB, int MODE>
 __global__ void __launch_bounds__(256, MINB)
     sgd_epoch_kernel(int n, long long E, float2* __restrict__ xy, const int4* __restrict__ edges,
                      const int* __restrict__ nip, const int* __restrict__ nix,
@@ -288,13 +349,20 @@ __global__ void __launch_bounds__(256, MINB)
     }
     if (!act) p = 0;
     // streamed once per epoch: evict-first, keep L2 for x / filter / rows
-    using F = typename std::conditional<REC32, Filt128, Filt64>::type;
-    const int4 rec = act ? __ldcs(edges + (REC32 ? 2 : 1) * p) : make_int4(0, 0, 0, 0);
+    using F = typename std::conditional<MODE == REC_BLOOM, Filt128, Filt64>::type;
+    const int4 rec = act ? __ldcs(edges + (MODE == REC_TABLE ? 1 : 2) * p) : make_int4(0, 0, 0, 0);
     const int u = rec.x, v = rec.y;
     typename F::Word fw;
-    if (REC32) {
+    int rlo = INT_MIN, rhi = INT_MAX;  // REC_RANGE: the head's neighbour-id window
+    if (MODE == REC_BLOOM) {
       const int4 f4 = act ? __ldcs(edges + 2 * p + 1) : make_int4(-1, -1, -1, -1);
       memcpy(&fw, &f4, sizeof(fw));
+    } else if (MODE == REC_RANGE) {
+      const int4 f4 = act ? __ldcs(edges + 2 * p + 1) : make_int4(INT_MIN, INT_MAX, -1, -1);
+      rlo = f4.x;
+      rhi = f4.y;
+      const uint2 f2 = make_uint2((unsigned)f4.z, (unsigned)f4.w);
+      memcpy(&fw, &f2, sizeof(fw));
     } else if (filt) {
       memcpy(&fw, filt + u, sizeof(fw));
     } else {
@@ -350,7 +418,8 @@ __global__ void __launch_bounds__(256, MINB)
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         draw_q[q] = draw32(vbase, q0 + q, 0);
         cand[q] = (int)__umulhi(draw_q[q], (unsigned)n);
-        if (act && q < nq && filt_maybe<F>(fw, cand[q])) mm |= 1u << q;
+        if (act && q < nq && cand[q] >= rlo && cand[q] <= rhi && filt_maybe<F>(fw, cand[q]))
+          mm |= 1u << q;
       }
       float2 xc[SGD_NEG_BLOCK];
 #pragma unroll
@@ -530,19 +599,37 @@ extern "C" int32_t gu_sgd_record_bytes_for(int64_t concurrency) {
 
 extern "C" int gu_sgd_prepare_edges(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
                                     const double* sym_w, const int32_t* nbr_indptr,
-                                    const int32_t* nbr_indices, int32_t record_bytes,
-                                    uint64_t seed, void* edges, int32_t* perm_out,
-                                    void* stream) {
-  if (E < 0 || E >= INT_MAX || (record_bytes != 16 && record_bytes != 32)) {
-    set_error("gu_sgd_prepare_edges: unsupported E=%lld / record_bytes=%d", (long long)E,
-              record_bytes);
+                                    const int32_t* nbr_indices, const int32_t* relabel,
+                                    int32_t record_mode, uint64_t seed, void* edges,
+                                    int32_t* perm_out, void* stream) {
+  if (E < 0 || E >= INT_MAX || record_mode < REC_TABLE || record_mode > REC_RANGE) {
+    set_error("gu_sgd_prepare_edges: unsupported E=%lld / record_mode=%d", (long long)E,
+              record_mode);
     return GU_ERR_UNSUPPORTED;
   }
   if (E == 0) return GU_OK;
   prepare_edges_kernel<<<grid_for(E), 256, 0, (cudaStream_t)stream>>>(
-      E, sym_src, sym_dst, sym_w, nbr_indptr, nbr_indices, record_bytes / 16,
+      E, sym_src, sym_dst, sym_w, nbr_indptr, nbr_indices, relabel, record_mode,
       mix64(seed ^ 0xED6E5ull), (int4*)edges, perm_out);
   GU_CHECK_LAUNCH("prepare_edges_kernel");
+  return GU_OK;
+}
+
+extern "C" int gu_sgd_prepare_edges_local(int64_t n, int64_t E, const double* sym_w,
+                                          const int32_t* new_indptr, const int32_t* new_indices,
+                                          const int32_t* order, const int32_t* nbr_indptr,
+                                          const int32_t* nbr_indices, int64_t block,
+                                          uint64_t seed, void* edges, int32_t* perm_out,
+                                          void* stream) {
+  if (n < 1 || n >= INT_MAX || E < 0 || E >= INT_MAX || block < 1) {
+    set_error("gu_sgd_prepare_edges_local: bad arguments");
+    return GU_ERR_ARG;
+  }
+  if (E == 0) return GU_OK;
+  prepare_edges_local<<<grid_for(E), 256, 0, (cudaStream_t)stream>>>(
+      E, sym_w, (int)n, new_indptr, new_indices, order, nbr_indptr, nbr_indices, block,
+      mix64(seed ^ 0xED6E5ull), (int4*)edges, perm_out);
+  GU_CHECK_LAUNCH("prepare_edges_local");
   return GU_OK;
 }
 
@@ -574,21 +661,24 @@ typedef void (*EpochKernel)(int, long long, float2*, const int4*, const int*, co
                             const FiltWord*, float, float, float, int, int, long long, long long,
                             int, unsigned long long, int*, long long, long long*);
 
-static EpochKernel epoch_kernel(int lanes, bool rec32) {
+static EpochKernel epoch_kernel(int lanes, int mode) {
   if (lanes == 32)
-    return rec32 ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS, true>
-                 : sgd_epoch_kernel<32, SGD_MIN_BLOCKS, false>;
-  return rec32 ? sgd_epoch_kernel<16, 2, true> : sgd_epoch_kernel<16, 2, false>;
+    return mode == REC_RANGE   ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_RANGE>
+           : mode == REC_BLOOM ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_BLOOM>
+                               : sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_TABLE>;
+  return mode == REC_RANGE   ? sgd_epoch_kernel<16, 2, REC_RANGE>
+         : mode == REC_BLOOM ? sgd_epoch_kernel<16, 2, REC_BLOOM>
+                             : sgd_epoch_kernel<16, 2, REC_TABLE>;
 }
 
 extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges,
-                             int32_t record_bytes, const int32_t* nbr_indptr,
+                             int32_t record_mode, const int32_t* nbr_indptr,
                              const int32_t* nbr_indices, const void* nbr_filter, float a,
                              float b, float lr0, int32_t t, int32_t epoch_begin, int32_t epoch_end,
                              int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
                              int64_t concurrency, int32_t* diverged, void* stream) {
   if (n <= 0 || n >= INT_MAX || E < 0 || t < 0 || epoch_begin < 0 || epoch_end > t ||
-      (record_bytes != 16 && record_bytes != 32) || (windowed && (window < 1 || window > E))) {
+      record_mode < REC_TABLE || record_mode > REC_RANGE || (windowed && (window < 1 || window > E))) {
     set_error("gu_sgd_epochs: bad arguments");
     return GU_ERR_ARG;
   }
@@ -603,7 +693,7 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
     const long long threads = concurrency > 0 ? (concurrency * 32 + lanes - 1) / lanes : 0;
     const unsigned bs = block_for(threads);
     const unsigned gs = bs < 256 ? 1u : grid_for((items * 32 + lanes - 1) / lanes, threads);
-    EpochKernel kern = epoch_kernel(lanes, record_bytes == 32);
+    EpochKernel kern = epoch_kernel(lanes, record_mode);
     kern<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges, nbr_indptr,
                             nbr_indices, (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, items,
                             start, windowed, seed, diverged, 0LL, nullptr);
@@ -613,7 +703,7 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
 }
 
 extern "C" int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_xy,
-                                           const void* edges, int32_t record_bytes,
+                                           const void* edges, int32_t record_mode,
                                            const int32_t* nbr_indptr,
                                            const int32_t* nbr_indices, const void* nbr_filter,
                                            float a, float b, float lr0, int32_t t,
@@ -622,7 +712,7 @@ extern "C" int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_x
                                            int64_t batch, int64_t* acc, int32_t* diverged,
                                            void* stream) {
   if (n <= 0 || n >= INT_MAX || E < 0 || t < 0 || epoch_begin < 0 || epoch_end > t ||
-      batch < 32 || !acc || (record_bytes != 16 && record_bytes != 32) ||
+      batch < 32 || !acc || record_mode < REC_TABLE || record_mode > REC_RANGE ||
       (windowed && (window < 1 || window > E))) {
     set_error("gu_sgd_epochs_deterministic: bad arguments");
     return GU_ERR_ARG;
@@ -639,7 +729,7 @@ extern "C" int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_x
       const long long threads = b1 - b0;
       const unsigned bs = block_for(threads);
       const unsigned gs = bs < 256 ? 1u : grid_for(threads, threads);
-      epoch_kernel(32, record_bytes == 32)<<<gs, bs, 0, st>>>(
+      epoch_kernel(32, record_mode)<<<gs, bs, 0, st>>>(
           (int)n, E, (float2*)coords_xy, (const int4*)edges, nbr_indptr, nbr_indices,
           (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, b1, start, windowed, seed, diverged,
           b0, (long long*)acc);

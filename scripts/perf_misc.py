@@ -63,7 +63,7 @@ for name in ("c3", "c4", "c5"):
         def run(mode=mode):
             e = ep[0] % 200
             ep[0] += 1
-            _lib.call("gu_sgd_epochs", plan.n, plan.E, _lib.ptr(xy), _lib.ptr(plan.edges), plan.record_bytes,
+            _lib.call("gu_sgd_epochs", plan.n, plan.E, _lib.ptr(xy), _lib.ptr(plan.edges), plan.record_mode,
                       _lib.ptr(plan.nbr_indptr), _lib.ptr(plan.nbr_indices), _lib.ptr(plan.filter), float(a), float(b), 1.0,
                       200, e, e + 1, 5, window if mode != "full" else E, 0 if mode == "full" else 1,
                       plan.seed, sgd_concurrency(plan.n), _lib.ptr(div), stream_ptr(dev))

@@ -22,9 +22,9 @@ conc = int(os.environ.get("CONC", sgd_concurrency(plan.n)))
 for ep in range(6):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    _lib.call("gu_sgd_epochs", plan.n, plan.E, _lib.ptr(xy), _lib.ptr(plan.edges), plan.record_bytes,
+    _lib.call("gu_sgd_epochs", plan.n, plan.E, _lib.ptr(xy), _lib.ptr(plan.edges), plan.record_mode,
               _lib.ptr(plan.nbr_indptr), _lib.ptr(plan.nbr_indices), _lib.ptr(plan.filter), float(a), float(b), 1.0,
               200, ep, ep + 1, 5, E, 0, plan.seed, conc, _lib.ptr(div), stream_ptr(dev))
     e1.record(); e1.synchronize()
     ms = e0.elapsed_time(e1)
-print(f"{name}: E={E} conc={conc} full epoch {ms:.3f} ms  {E/ms/1e6:.2f} G upd/s", flush=True)
+print(f"{name}: E={E} conc={conc} mode={plan.record_mode} window={getattr(plan, 'mean_window', None)} full epoch {ms:.3f} ms  {E/ms/1e6:.2f} G upd/s", flush=True)
