@@ -53,6 +53,7 @@ struct FbShared {
   int tk[64];
   int lastlvl[64];
   unsigned keep[2];
+  int anynew;  // MODE_APSP: a vertex was discovered in the level just finished
   unsigned long long active;
   double2 sxy[64];
   double red[2][FB_WARPS];
@@ -130,12 +131,10 @@ __global__ void __launch_bounds__(FB_THREADS)
       vis[v] = 0ull;
       l1[v] = 0ull;
     }
-    if (MODE == MODE_APSP) {
-      for (int b = 0; b < nb; b++) {
-        int* row = out_rows + (s0 - src_begin + b) * (long long)n;
-        for (int v = tid; v < n; v += FB_THREADS) row[v] = (v == (int)(s0 + b)) ? 0 : GU_INF32;
-      }
-    }
+    // APSP rows: every (source, vertex) entry is written exactly once -- 0 for
+    // the source itself here, its level when it is discovered, GU_INF32 by
+    // the unreached pass after the levels (no full-row initialisation pass)
+    if (MODE == MODE_APSP && tid < nb) out_rows[(s0 - src_begin + tid) * (long long)n + s0 + tid] = 0;
     // source id of bit b: s0 + b, or the listed source in stress mode
     auto src_of = [&](int b) -> int {
       return (MODE == MODE_STRESS && sa.sources) ? sa.sources[s0 + b] : (int)(s0 + b);
@@ -149,7 +148,10 @@ __global__ void __launch_bounds__(FB_THREADS)
       sh.tk[tid] = 0;
       sh.lastlvl[tid] = 0;
     }
-    if (tid == 0) sh.active = nb == 64 ? ~0ull : ((1ull << nb) - 1ull);
+    if (tid == 0) {
+      sh.active = nb == 64 ? ~0ull : ((1ull << nb) - 1ull);
+      sh.anynew = 0;
+    }
     __syncthreads();
     // ---- level 0 / level 1 (push from the sources' sorted adjacency)
     for (int b = warp; b < nb; b += FB_WARPS) {
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(FB_THREADS)
       if (lane == 0) {
         atomicOr(&vis[s], 1ull << b);
         sh.cnt[b] = end - beg;
+        if (MODE == MODE_APSP && end > beg) sh.anynew = 1;
       }
       te += (lane == 0) ? (unsigned long long)(end - beg) : 0ull;
       int* row = MODE == MODE_APSP ? out_rows + (s0 - src_begin + b) * (long long)n : nullptr;
@@ -177,6 +180,13 @@ __global__ void __launch_bounds__(FB_THREADS)
         const int b = tid;
         bool act = (sh.active >> b) & 1ull;
         bool keep = act;
+        if (MODE == MODE_APSP) {
+          // no per-source counts in APSP mode: every source runs until a level
+          // discovers nothing for any of them
+          keep = act && sh.anynew != 0;
+          sh.cnt[b] = 0;
+          act = false;  // skip the count bookkeeping below
+        }
         if (act) {
           int c = sh.cnt[b];
           if (c == 0) {
@@ -202,6 +212,7 @@ __global__ void __launch_bounds__(FB_THREADS)
       const unsigned long long active = sh.active;
       if (active == 0ull) break;
       levels_run++;
+      if (MODE == MODE_APSP && tid == 0) sh.anynew = 0;  // read by the retire step above
       // ---- fold the level just finished into vis
       {
         unsigned long long* prev = level(l);
@@ -219,12 +230,27 @@ __global__ void __launch_bounds__(FB_THREADS)
         unsigned long long nw = 0ull;
         if (v < n) {
           const unsigned long long vv = vis[v];
-          if ((~vv & active) != 0ull) {
+          const unsigned long long need = ~vv & active;
+          if (need != 0ull) {
             const int beg = __ldg(indptr + v), end = __ldg(indptr + v + 1);
             unsigned long long acc = 0ull;
-            for (int p = beg; p < end; p++) acc |= prev[__ldg(indices + p)];
-            te += (unsigned long long)(end - beg);
-            nw = acc & ~vv & active;
+            int p = beg;
+            // bottom-up early exit: stop once every source still looking for
+            // v has found it (dense late levels touch a few neighbours); the
+            // new bits are the same as with the full OR
+            for (; p + 4 <= end; p += 4) {
+              const int i0 = __ldg(indices + p), i1 = __ldg(indices + p + 1),
+                        i2 = __ldg(indices + p + 2), i3 = __ldg(indices + p + 3);
+              acc |= prev[i0] | prev[i1] | prev[i2] | prev[i3];
+              if ((acc & need) == need) {
+                p += 4;
+                break;
+              }
+            }
+            if ((acc & need) != need)
+              for (; p < end; p++) acc |= prev[__ldg(indices + p)];
+            te += (unsigned long long)(p - beg);  // entries actually read
+            nw = acc & need;
             if (nw) vis[v] = vv | nw;
           }
           next[v] = nw;
@@ -232,7 +258,16 @@ __global__ void __launch_bounds__(FB_THREADS)
         unsigned long long any = nw;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) any |= __shfl_xor_sync(FULL, any, o);
-        while (any) {
+        if (MODE == MODE_APSP) {
+          // rows written coalesced, one source bit at a time; no counts
+          if (any && lane == 0) sh.anynew = 1;
+          while (any) {
+            const int b = __ffsll((long long)any) - 1;
+            any &= any - 1ull;
+            if ((nw >> b) & 1ull) out_rows[(s0 - src_begin + b) * (long long)n + v] = nl;
+          }
+        }
+        while (MODE != MODE_APSP && any) {
           const int b = __ffsll((long long)any) - 1;
           any &= any - 1ull;
           const int c = __popc(__ballot_sync(FULL, (nw >> b) & 1ull));
@@ -252,6 +287,18 @@ __global__ void __launch_bounds__(FB_THREADS)
       if (MODE == MODE_KNN && l >= L) break;  // unreachable by construction
     }
     if (MODE == MODE_STRESS && tid < nb && sh.cum[tid] + 1 < n) atomicOr(sa.flag, 1);
+    if (MODE == MODE_APSP) {
+      // unreached (source, vertex) pairs: GU_INF32 (none on a connected graph)
+      const unsigned long long mine = nb == 64 ? ~0ull : ((1ull << nb) - 1ull);
+      for (int v = tid; v < n; v += FB_THREADS) {
+        unsigned long long miss = ~vis[v] & mine;
+        while (miss) {
+          const int b = __ffsll((long long)miss) - 1;
+          miss &= miss - 1ull;
+          if (v != (int)(s0 + b)) out_rows[(s0 - src_begin + b) * (long long)n + v] = GU_INF32;
+        }
+      }
+    }
     if (MODE == MODE_KNN) {
       // ---- selection, one warp per source
       int* perm = perm_base + (size_t)warp * n;
