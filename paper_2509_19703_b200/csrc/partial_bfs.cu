@@ -35,6 +35,16 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ unsigned hash_id(int w) { return (unsigned)w * 0x9E3779B1u; }
+#ifndef PB_HASH_HIGH
+#define PB_HASH_HIGH 1
+#endif
+// home slot of id w in a table of HC (a power of two) slots: the top bits of
+// the Fibonacci product (PB_HASH_HIGH) or its low bits
+template <int HC>
+__device__ __forceinline__ unsigned hash_slot(int w) {
+  constexpr int B = __builtin_ctz(HC);
+  return PB_HASH_HIGH ? (hash_id(w) >> (32 - B)) : (hash_id(w) & (HC - 1));
+}
 
 // Tier-1 geometry: G lanes per source (32 / G sources per warp), at most CAP
 // vertices discovered (hash of 2*CAP slots), PCAP frontier parents and TCAP
@@ -118,7 +128,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   // claim w in the hash; true iff it was not there (table never fills: the
   // callers stop inserting once a source is known to overflow CAP)
   auto claim = [&](int w) -> bool {
-    unsigned h = hash_id(w) & (HC - 1);
+    unsigned h = hash_slot<HC>(w);
     for (;;) {
       const int old = atomicCAS(&hkey[h], -1, w);
       if (old == -1) return true;
@@ -148,7 +158,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     unsigned long long scanned = T0, expanded = 1;
     if (!ovf) {
       // ---- level 1: adjacency of s, already in discovery (= id) order
-      if (lane == 0) hkey[hash_id(s) & (HC - 1)] = s;
+      if (lane == 0) hkey[hash_slot<HC>(s)] = s;
       __syncwarp();
       for (int t0 = 0; t0 < T0; t0 += 32) {
         const int t = t0 + lane;
@@ -404,7 +414,7 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
   // predicated CAS for everybody; the linear-probe loop runs only when some
   // lane hit an occupied slot, so the common case has no divergence.
   auto claim = [&](int w, bool lead) -> bool {
-    unsigned h = hash_id(w) & (HC - 1);
+    unsigned h = hash_slot<HC>(w);
     int old = w;  // predicated CAS (no branch): lanes with !lead keep old == w
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
 #pragma unroll
     for (int i = 0; i < HC / 128; i++) reinterpret_cast<int4*>(hkey)[lane + 32 * i] = make_int4(-1, -1, -1, -1);
     __syncwarp();
-    if (lane == 0) hkey[hash_id(s) & (HC - 1)] = s;
+    if (lane == 0) hkey[hash_slot<HC>(s)] = s;
     __syncwarp();
     claim(w1, lane < T0);
     // ---- level 2: prefix of the parents' degrees.  In an undirected CSR a
