@@ -294,17 +294,17 @@ __global__ void __launch_bounds__(256, MINB)
                      const FiltWord* __restrict__ filt, float a, float b, float lr, int epoch,
                      int n_neg, long long items, long long start, int windowed,
                      unsigned long long seed, int* __restrict__ diverged,
-                     long long ibase = 0, long long* __restrict__ acc = nullptr, int epochs = 1,
-                     double lr0 = 0.0, int t = 1, long long window = 0) {
+                     long long ibase = 0, long long* __restrict__ acc = nullptr) {
   constexpr int lanes = LANES;
   // (candidate, row begin, row end, owner lane * 8 + slot) of the warp's
   // filter hits, and each lane's bitmask of slots found to be neighbours
   __shared__ int4 sh_pairs[SGD_WARPS][32 * SGD_NEG_BLOCK];
   __shared__ unsigned sh_hit[SGD_WARPS][32];
   const long long ntiles = (E + TILE - 1) / TILE;
+  Feistel tperm((unsigned long long)ntiles, mix64(seed ^ (0x51ED27ull + (unsigned long long)epoch)));
+  const unsigned long long rkey = mix64(seed ^ (0xA5A5A5A5ull * (unsigned long long)(epoch + 1)));
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   bool bad = false;
-  int bad_epoch = INT_MAX;
   // warp-uniform loop (every lane reaches the collectives below).  Each warp
   // takes `lanes` visits per step (lanes < 32 when the concurrency cap is
   // small: the same visits in flight spread over more warps, i.e. more
@@ -331,23 +331,6 @@ __global__ void __launch_bounds__(256, MINB)
       atomicAdd(&xy[w], make_float2(dx, dy));
     }
   };
-  // `epochs` consecutive epochs in one launch (small concurrency caps): the
-  // same threads -- the cap -- walk epoch after epoch with no grid-wide
-  // barrier in between, each visit with its own epoch's learning rate, order
-  // and draws; a lane that finishes an epoch early starts the next
-  for (int ep = 0; ep < epochs; ep++) {
-  const int e_cur = epoch + ep;
-  if (ep > 0) {
-    lr = (float)(lr0 * (1.0 - (double)e_cur / (double)t));
-    if (windowed) start = (long long)(((unsigned long long)e_cur * (unsigned long long)window) %
-                                      (unsigned long long)E);
-    if (bad && bad_epoch == INT_MAX) bad_epoch = e_cur - 1;
-  }
-  const Feistel tperm((unsigned long long)ntiles,
-                      mix64(seed ^ (0x51ED27ull + (unsigned long long)e_cur)));
-  const unsigned long long rkey = mix64(seed ^ (0xA5A5A5A5ull * (unsigned long long)(e_cur + 1)));
-  tile_batch = 0;
-  step = 0;
   for (long long i0 = ibase + gwarp * lanes; i0 < items; i0 += stride, step = (step + 1) & 31) {
     const long long i = i0 + lane;
     bool act = lane < lanes && i < items;
@@ -533,8 +516,7 @@ __global__ void __launch_bounds__(256, MINB)
       if (!isfinite(xu.x) || !isfinite(xu.y)) bad = true;
     }
   }
-  }  // epochs
-  if (bad) atomicMin(diverged, bad_epoch == INT_MAX ? epoch + epochs - 1 : bad_epoch);
+  if (bad) atomicMin(diverged, epoch);
 }
 
 // deterministic mode: x += acc * 2^-32, acc = 0, finiteness check
@@ -677,8 +659,7 @@ extern "C" int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr,
 
 typedef void (*EpochKernel)(int, long long, float2*, const int4*, const int*, const int*,
                             const FiltWord*, float, float, float, int, int, long long, long long,
-                            int, unsigned long long, int*, long long, long long*, int, double, int,
-                            long long);
+                            int, unsigned long long, int*, long long, long long*);
 
 static EpochKernel epoch_kernel(int lanes, int mode) {
   if (lanes == 32)
@@ -703,29 +684,19 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
   }
   if (E == 0) return GU_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const int lanes = sgd_lanes(concurrency);
-  // small caps (16 visits per warp): the whole range of epochs in one launch
-  // (no launch gap or grid tail between epochs); GPU-filling epochs: one
-  // launch each
-  static const bool multi_env = [] {
-    const char* v = getenv("GU_SGD_MULTI_EPOCH");
-    return !(v && v[0] == '0');
-  }();
-  const int per_launch = (lanes == 16 && multi_env) ? (epoch_end - epoch_begin) : 1;
-  for (int e = epoch_begin; e < epoch_end; e += per_launch) {
+  for (int e = epoch_begin; e < epoch_end; e++) {
     // lr = learning_rate * (1 - it / t), layout.py:334 (float64 on host)
     const float lr = (float)((double)lr0 * (1.0 - (double)e / (double)t));
     long long items, start;
     epoch_range(E, e, window, windowed, &items, &start);
+    const int lanes = sgd_lanes(concurrency);
     const long long threads = concurrency > 0 ? (concurrency * 32 + lanes - 1) / lanes : 0;
     const unsigned bs = block_for(threads);
     const unsigned gs = bs < 256 ? 1u : grid_for((items * 32 + lanes - 1) / lanes, threads);
-    const int ne = e + per_launch <= epoch_end ? per_launch : epoch_end - e;
     EpochKernel kern = epoch_kernel(lanes, record_mode);
     kern<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges, nbr_indptr,
                             nbr_indices, (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, items,
-                            start, windowed, seed, diverged, 0LL, nullptr, ne, (double)lr0, t,
-                            window);
+                            start, windowed, seed, diverged, 0LL, nullptr);
     GU_CHECK_LAUNCH("sgd_epoch_kernel");
   }
   return GU_OK;
@@ -761,7 +732,7 @@ extern "C" int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_x
       epoch_kernel(32, record_mode)<<<gs, bs, 0, st>>>(
           (int)n, E, (float2*)coords_xy, (const int4*)edges, nbr_indptr, nbr_indices,
           (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, b1, start, windowed, seed, diverged,
-          b0, (long long*)acc, 1, (double)lr0, t, window);
+          b0, (long long*)acc);
       GU_CHECK_LAUNCH("sgd_epoch_kernel(deterministic)");
       det_apply_kernel<<<grid_for(n), 256, 0, st>>>((int)n, (float2*)coords_xy,
                                                     (long long*)acc, e, diverged);
