@@ -391,7 +391,13 @@ __device__ __forceinline__ int rank_in_warp(int r, int v) {
   return rk;
 }
 
-template <int WARPS>
+// PACKED (n < 2^24 - 1): hash slots hold (tag << 24 | id) and duplicates
+// inside a chunk pair are resolved by a shared-memory atomicMin on the tag
+// (the flattened position t + 1): no MATCH.  A MATCH.ANY occupies the ADU one
+// slot per DISTINCT value among the lanes (~64 SM cycles for 32 distinct ids,
+// profiles/r02_micro_adu.log), and the ADU was the most-used pipe of this
+// kernel (73%).  !PACKED keeps the MATCH election for larger graphs.
+template <int WARPS, bool PACKED>
 __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     pbfs_fast(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
               unsigned long long seed, long long src_begin, long long nsrc,
@@ -463,14 +469,15 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       } else {
         // Fisher-Yates on positions of the sorted adjacency: the picks'
         // id order is their position order, so the rank is one popcount
+        // (lane p holds position p: it stores its own id at rank
+        // popc(picked positions below p))
         int j = lane;
         if (lane < K) j = lane + umod64_tab(splitmix_at(fy_base, lane), T0 - lane);
         const int P = fy_registers(K, lane, j, lane, j);
-        const int v = __shfl_sync(FULL, w1, P & 31);
         const unsigned M = __reduce_or_sync(FULL, lane < K ? 1u << P : 0u);
-        const int r = __popc(M & ((1u << P) - 1u));
-        if (lane < K) {
-          rn[r] = v;
+        if ((M >> lane) & 1u) {
+          const int r = __popc(M & lt);
+          rn[r] = w1;
           rd[r] = 1;
         }
       }
@@ -508,6 +515,10 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     const int inc = warp_incl_scan(cdv);
     const int cpre = inc - cdv;
     const int T = __shfl_sync(FULL, inc, 31);
+    if (PACKED && T > 254) {  // tags t + 1 must fit in 8 bits
+      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+      continue;
+    }
     int nst = 0, pcount = 0;
     // candidate of chunk t0 for this lane (parent count of earlier chunks: pc);
     // cbase = adjacency start - flattened start of the lane's parent, so a
@@ -530,7 +541,63 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     // (the hash holds it: static_assert).  Both MATCHes are issued before the
     // claims, and the second chunk's claims follow the first's, so each pair
     // costs one dependent round trip instead of two.
+    // PACKED: insert one tagged key per lane (valid lanes only); h is the
+    // slot holding the id, mine is true when the id was not in the hash
+    // before this chunk pair (then the smallest tag of the pair wins the slot)
+    auto insert_tagged = [&](int w, unsigned key, bool valid, unsigned base_tag, unsigned& h,
+                             bool& mine) {
+      // Predicated CAS (an unconditional one with a never-matching compare
+      // value was 20% slower: lanes past T all hold the same id, so their
+      // CASes serialise on one slot); the probe loop runs only when some lane
+      // hit another id's slot.
+      h = hash_slot<HC>(w);
+      unsigned old = key;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+          "@p atom.shared.cas.b32 %0, [%2], -1, %3;\n\t}"
+          : "+r"(old)
+          : "r"((unsigned)valid), "r"(hbase + 4u * h), "r"(key)
+          : "memory");
+      bool coll = valid && old != 0xffffffffu && (old & 0xffffffu) != (unsigned)w;
+      if (__any_sync(FULL, coll)) {
+        while (coll) {
+          h = (h + 1) & (HC - 1);
+          old = (unsigned)atomicCAS(&hkey[h], -1, (int)key);
+          coll = old != 0xffffffffu && (old & 0xffffffu) != (unsigned)w;
+        }
+        __syncwarp();
+      }
+      mine = valid && (old == 0xffffffffu || (old >> 24) >= base_tag);
+      // unconditional (a predicated RED becomes a branch): min with all ones
+      // is a no-op
+      atomicMin(reinterpret_cast<unsigned*>(&hkey[h]),
+                (mine && old != 0xffffffffu) ? key : 0xffffffffu);
+    };
+    auto process2p = [&](int t0, int xa, int xb) -> bool {
+      const bool two = t0 + 32 < T;  // warp-uniform
+      const unsigned base_tag = (unsigned)(t0 + 1);
+      const unsigned ka = ((unsigned)(t0 + lane + 1) << 24) | (unsigned)xa;
+      const unsigned kb = ((unsigned)(t0 + 33 + lane) << 24) | (unsigned)xb;
+      unsigned ha, hb;
+      bool ma, mb;
+      insert_tagged(xa, ka, t0 + lane < T, base_tag, ha, ma);
+      insert_tagged(xb, kb, two && t0 + 32 + lane < T, base_tag, hb, mb);
+      __syncwarp();
+      const bool na = ma && (unsigned)hkey[ha] == ka;
+      const bool nb = mb && (unsigned)hkey[hb] == kb;
+      const unsigned ba = __ballot_sync(FULL, na);
+      const unsigned bb = __ballot_sync(FULL, nb);
+      // nst <= TF_CAP2 on entry: a's entries end below TF_CAP2 + 32, b's
+      // below TF_CAP2 + 64 (past TF_CAP2 only when overflowing, which
+      // discards the list); lanes with nothing new hit their sink
+      lst[na ? nst + __popc(ba & lt) : TF_CAP2 + 32 + lane] = xa;
+      nst += __popc(ba);
+      lst[nb ? nst + __popc(bb & lt) : TF_CAP2 + 32 + lane] = xb;
+      nst += __popc(bb);
+      return nst > TF_CAP2;
+    };
     auto process2 = [&](int t0, int xa, int xb) -> bool {
+      if (PACKED) return process2p(t0, xa, xb);
       const bool two = t0 + 32 < T;  // warp-uniform
       const unsigned ga = __match_any_sync(FULL, xa);
       const unsigned gb = two ? __match_any_sync(FULL, xb) : 0u;
@@ -553,13 +620,13 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     // move or select touches an in-flight load result
     int x0 = 0, x1 = 0, x2 = 0, x3 = 0;
     unsigned m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    bool ovf = false;
     load_chunk(0, 0, x0, m0);
     pcount = __popc(m0);
     if (32 < T) {
       load_chunk(32, pcount, x1, m1);
       pcount += __popc(m1);
     }
-    bool ovf = false;
     for (int t0 = 0;;) {
       if (t0 + 64 < T) {
         load_chunk(t0 + 64, pcount, x2, m2);
@@ -591,13 +658,11 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       continue;
     }
     __syncwarp();
+    int pos = lane;
+    if (nst > remaining && lane < remaining)
+      pos = lane + umod64_tab(splitmix_at(fy_base, lane), nst - lane);
     int v = lst[lane];
-    if (nst > remaining) {
-      int j = lane;
-      if (lane < remaining) j = lane + umod64_tab(splitmix_at(fy_base, lane), nst - lane);
-      const int aj = lst[j];
-      v = fy_registers(remaining, lane, j, v, aj);
-    }
+    if (nst > remaining) v = fy_registers(remaining, lane, pos, v, lst[pos]);
     const int r = rank_in_warp(remaining, v);
     if (lane < remaining) {
       rn[T0 + r] = v;
@@ -774,11 +839,12 @@ size_t pbfs_ws_layout(long long n, long long nsrc, int slots, char* base, PbfsWs
 
 constexpr int TF_WARPS = 8;
 
-cudaError_t launch_fast(int sms, const int* indptr, const int* indices, int k,
+cudaError_t launch_fast(int sms, long long n, const int* indptr, const int* indices, int k,
                         unsigned long long seed, long long src_begin, long long nsrc,
                         int* out_nbr, int* out_dist, int* out_count, int* ovf_out, int* ovf_cnt,
                         unsigned long long* work, cudaStream_t st) {
-  auto kern = pbfs_fast<TF_WARPS>;
+  // packed tags need ids below 2^24 - 1 (the empty key is all ones)
+  auto kern = n < (1 << 24) - 1 ? pbfs_fast<TF_WARPS, true> : pbfs_fast<TF_WARPS, false>;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TF_WARPS * 32, 0);
   if (e != cudaSuccess) return e;
@@ -890,7 +956,7 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
     // (comparison only; every path is exact).
     static const char* env_mode = getenv("GU_PBFS_MODE");
     if (!env_mode || strcmp(env_mode, "lean")) {
-      GU_CHECK(launch_fast(sms, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
+      GU_CHECK(launch_fast(sms, n, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
                            out_count, ws.ovf0, ws.counts + 2, work, st));
       GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0, ws.counts + 2,
                            out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));

@@ -588,3 +588,31 @@ def test_sgd_range_records_rgg(gu):
     print("NP relabelled / plain:", vals, ratio)
     # Hogwild runs of one seed differ by ~1-2% NP between repeats at this size
     assert abs(ratio - 1.0) < 0.025
+
+
+def test_partial_bfs_large_ids_unpacked_path(gu, oracle):
+    """n >= 2^24 - 1: tier F switches from packed (tag << 24 | id) hash keys
+    to the MATCH election.  A scale-free graph relabelled onto the top ids of
+    a 2^24 + 7 vertex space (the rest isolated); the range of its sources
+    must equal the oracle's rows (_kernels.py:60-131)."""
+    import torch
+
+    from paper_2509_19703_b200.device import device_csr
+    from paper_2509_19703_b200.fixtures import canonical_edges, graph_from_edges
+    from paper_2509_19703_b200.neighbors import partial_bfs_records
+
+    n = (1 << 24) + 7
+    base = gu.synth_graph("scale_free", 20000, seed=5, m0=3)
+    off = n - base.n
+    src = np.repeat(np.arange(base.n), np.diff(base.adj_indptr))
+    pairs = np.stack([src + off, base.adj_indices.astype(np.int64) + off], axis=1)
+    pairs = pairs[pairs[:, 0] < pairs[:, 1]]
+    g = graph_from_edges(n, canonical_edges(n, pairs))
+    csr = device_csr(g)
+    nb, dd, cnt = partial_bfs_records(csr, 15, 9, off, n, tier2_warps=1)
+    torch.cuda.synchronize()
+    o_n, o_d, o_c = oracle.partial_bfs_raw(g, 15, 9, src_begin=off, src_end=n,
+                                           nthreads=oracle.max_threads())
+    assert np.array_equal(cnt.cpu().numpy(), o_c)
+    assert np.array_equal(nb.cpu().numpy().reshape(-1), o_n)
+    assert np.array_equal(dd.cpu().numpy().reshape(-1), o_d)
