@@ -364,24 +364,35 @@ __device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
 #define TF_MINB 8
 #endif
 
-// Partial Fisher-Yates resolved in registers (no shared-memory swaps).  Lane
-// i < r holds its draw j_i (>= i), a_i = list[i] and a_j = list[j_i] of the
-// original list; the result is list[i] after the reference's r sequential
-// swaps swap(list[i], list[j_i]), i = 0..r-1.  Step k sends u_k -- the value
-// position k held just before it -- to position j_k; a later lane picks it up
-// as its own u when j_k is its position, and as the value it will take when
-// j_k is its draw (the last such step wins, as in the sequential loop).
-__device__ __forceinline__ int fy_registers(int r, int lane, int j, int a_i, int a_j) {
-  int u = a_i, take = a_j;
-  for (int k = 0; k + 1 < r; k++) {
-    const int jk = __shfl_sync(FULL, j, k);
-    const int uk = __shfl_sync(FULL, u, k);
-    if (lane > k) {
-      if (lane == jk) u = uk;
-      if (j == jk) take = uk;
-    }
+// Partial Fisher-Yates in closed form.  Lane i < r holds its draw j_i (>= i)
+// of the reference's sequential swaps swap(a[i], a[j_i]), i = 0..r-1
+// (_kernels.py:98-105); returns the ORIGINAL position whose value ends in
+// slot i.  Slot i is never touched after step i, so it receives what position
+// j_i held just before step i: the value the last earlier step with the same
+// draw moved there (lanes of equal draws: one MATCH; inactive lanes share
+// one key, so it costs at most r + 1 ADU slots), else a[j_i] itself.  What a
+// position k < r held just before step k is, likewise, what the last earlier
+// step drawing k moved there: a chain k -> W(k) -> ... ending at an original
+// position, resolved by pointer jumping (draws rarely collide).  wsc: 32
+// ints of per-warp scratch.
+__device__ __forceinline__ int fy_positions(int r, int lane, int j, int* wsc) {
+  const bool act = lane < r;
+  const unsigned grp = __match_any_sync(FULL, act ? j : -1);
+  wsc[lane] = lane;
+  __syncwarp();
+  // W(d) = the last step i < d with j_i == d: the member of d's draw group
+  // with no other member strictly between it and d
+  if (act && j < r && j > lane && (grp & ~((2u << lane) - 1u) & ((1u << j) - 1u)) == 0) wsc[j] = lane;
+  __syncwarp();
+  int nxt = wsc[lane];
+  for (;;) {
+    const int n2 = __shfl_sync(FULL, nxt, nxt);
+    if (!__any_sync(FULL, n2 != nxt)) break;
+    nxt = n2;
   }
-  return j == lane ? u : take;
+  const unsigned prev = act ? grp & ((1u << lane) - 1u) : 0u;
+  const int vL = __shfl_sync(FULL, nxt, (31 - __clz(prev)) & 31);
+  return prev ? vL : j;
 }
 
 // rank of v among the (distinct) values of lanes 0..r-1
@@ -473,7 +484,7 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
         // popc(picked positions below p))
         int j = lane;
         if (lane < K) j = lane + umod64_tab(splitmix_at(fy_base, lane), T0 - lane);
-        const int P = fy_registers(K, lane, j, lane, j);
+        const int P = fy_positions(K, lane, j, lst + TF_CAP2 + 32);
         const unsigned M = __reduce_or_sync(FULL, lane < K ? 1u << P : 0u);
         if ((M >> lane) & 1u) {
           const int r = __popc(M & lt);
@@ -661,8 +672,8 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     int pos = lane;
     if (nst > remaining && lane < remaining)
       pos = lane + umod64_tab(splitmix_at(fy_base, lane), nst - lane);
-    int v = lst[lane];
-    if (nst > remaining) v = fy_registers(remaining, lane, pos, v, lst[pos]);
+    if (nst > remaining) pos = fy_positions(remaining, lane, pos, lst + TF_CAP2 + 32);
+    const int v = lst[pos];
     const int r = rank_in_warp(remaining, v);
     if (lane < remaining) {
       rn[T0 + r] = v;
