@@ -105,7 +105,7 @@ __device__ __forceinline__ int umod64_small(unsigned long long x, int d) {
 //   * a level's entries are written to the output row as soon as the level is
 //     settled (rank by id inside the level; levels are in distance order);
 //   * overflow is detected before the hash can fill, so probing is unbounded.
-template <int CAP, int PCAP, int TCAP, int WARPS, int MINB>
+template <int CAP, int PCAP, int TCAP, int WARPS, int MINB, bool PACKED>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     pbfs_warp(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
               unsigned long long seed, long long src_begin, long long nsrc,
@@ -264,8 +264,35 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
           }
           pb += __popc(m1);
         }
-        const unsigned grp = __match_any_sync(FULL, w);
-        const bool isnew = t0 + lane < T && lane == __ffs(grp) - 1 && claim(w);
+        bool isnew;
+        if (PACKED) {
+          // ids below 2^24 - 1: the chunk inserts (lane + 1) << 24 | id, equal
+          // ids keep the lowest lane (atomicMin), settled ids hold tag 0; the
+          // chunk's first occurrences then retag their slot to 0.  No MATCH
+          // (one ADU slot per distinct id, see tier F).
+          const bool valid = t0 + lane < T;
+          const unsigned key = ((unsigned)(lane + 1) << 24) | (unsigned)w;
+          unsigned h = hash_slot<HC>(w);
+          unsigned old = valid ? (unsigned)atomicCAS(&hkey[h], -1, (int)key) : 0u;
+          bool coll = valid && old != 0xffffffffu && (old & 0xffffffu) != (unsigned)w;
+          if (__any_sync(FULL, coll)) {
+            while (coll) {
+              h = (h + 1) & (HC - 1);
+              old = (unsigned)atomicCAS(&hkey[h], -1, (int)key);
+              coll = old != 0xffffffffu && (old & 0xffffffu) != (unsigned)w;
+            }
+          }
+          const bool mine = valid && (old == 0xffffffffu || (old >> 24) != 0u);
+          atomicMin(reinterpret_cast<unsigned*>(&hkey[h]),
+                    (mine && old != 0xffffffffu) ? key : 0xffffffffu);
+          __syncwarp();
+          isnew = mine && (unsigned)hkey[h] == key;
+          __syncwarp();
+          if (isnew) hkey[h] = w;
+        } else {
+          const unsigned grp = __match_any_sync(FULL, w);
+          isnew = t0 + lane < T && lane == __ffs(grp) - 1 && claim(w);
+        }
         const unsigned bal = __ballot_sync(FULL, isnew);
         if (isnew) {
           const int pos = nst + __popc(bal & lt);
@@ -334,7 +361,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 // fetched by shuffle; the next chunk's loads are issued before the current
 // chunk's hash work.  Sources of any other shape (deg(s) > 32, a level 2 that
 // does not reach k, a ball above the budget) go to the generic tiers.
-constexpr int TF_CAP2 = 160;  // level-2 ids kept per source
+#ifndef TF_CAP2
+#define TF_CAP2 160  // level-2 ids kept per source
+#endif
 #ifndef TF_HC
 #define TF_HC 512  // hash slots per source (ball budget 3/4 of it)
 #endif
@@ -869,14 +898,15 @@ cudaError_t launch_fast(int sms, long long n, const int* indptr, const int* indi
 }
 
 template <int CAP, int PCAP, int TCAP, int W, int MINB>
-cudaError_t launch_warp_tier(int sms, const int* indptr, const int* indices, int k,
+cudaError_t launch_warp_tier(int sms, long long n, const int* indptr, const int* indices, int k,
                              unsigned long long seed, long long src_begin, long long nsrc,
                              const int* list, const int* list_count, int* out_nbr, int* out_dist,
                              int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
                              cudaStream_t st) {
   using LA = Tier1<32, CAP, PCAP, TCAP>;
   constexpr size_t smem = sizeof(int) * LA::WORDS * W;
-  auto kern = pbfs_warp<CAP, PCAP, TCAP, W, MINB>;
+  auto kern = n < (1 << 24) - 1 ? pbfs_warp<CAP, PCAP, TCAP, W, MINB, true>
+                                : pbfs_warp<CAP, PCAP, TCAP, W, MINB, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -892,24 +922,24 @@ cudaError_t launch_warp_tier(int sms, const int* indptr, const int* indices, int
 }
 
 // tier 1a: lean warp, CAP 128
-cudaError_t launch_lean(int sms, const int* indptr, const int* indices, int k,
+cudaError_t launch_lean(int sms, long long n, const int* indptr, const int* indices, int k,
                         unsigned long long seed, long long src_begin, long long nsrc,
                         const int* list, const int* list_count, int* out_nbr, int* out_dist,
                         int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
                         cudaStream_t st) {
   return launch_warp_tier<T1A_CAP, T1A_PCAP, T1A_TCAP, 8, GU_LEAN_MINB>(
-      sms, indptr, indices, k, seed, src_begin, nsrc, list, list_count, out_nbr, out_dist, out_count,
+      sms, n, indptr, indices, k, seed, src_begin, nsrc, list, list_count, out_nbr, out_dist, out_count,
       ovf_out, ovf_cnt, work, st);
 }
 
 // tier 1b: the same lean warp kernel with CAP 1024 (hub-adjacent balls)
-cudaError_t launch_lean_big(int sms, const int* indptr, const int* indices, int k,
+cudaError_t launch_lean_big(int sms, long long n, const int* indptr, const int* indices, int k,
                             unsigned long long seed, long long src_begin, long long nsrc,
                             const int* list, const int* list_count, int* out_nbr, int* out_dist,
                             int* out_count, int* ovf_out, int* ovf_cnt, unsigned long long* work,
                             cudaStream_t st) {
   return launch_warp_tier<T1B_CAP, T1B_PCAP, T1B_TCAP, 2, 1>(
-      sms, indptr, indices, k, seed, src_begin, nsrc, list, list_count, out_nbr, out_dist, out_count,
+      sms, n, indptr, indices, k, seed, src_begin, nsrc, list, list_count, out_nbr, out_dist, out_count,
       ovf_out, ovf_cnt, work, st);
 }
 
@@ -969,13 +999,13 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
     if (!env_mode || strcmp(env_mode, "lean")) {
       GU_CHECK(launch_fast(sms, n, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
                            out_count, ws.ovf0, ws.counts + 2, work, st));
-      GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0, ws.counts + 2,
+      GU_CHECK(launch_lean(sms, n, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0, ws.counts + 2,
                            out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
     } else {
-      GU_CHECK(launch_lean(sms, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
+      GU_CHECK(launch_lean(sms, n, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
                            out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
     }
-    GU_CHECK(launch_lean_big(sms, indptr, indices, k, seed, src_begin, nsrc, ws.ovfA, ws.counts + 0,
+    GU_CHECK(launch_lean_big(sms, n, indptr, indices, k, seed, src_begin, nsrc, ws.ovfA, ws.counts + 0,
                              out_nbr, out_dist, out_count, ws.ovfB, ws.counts + 1, work, st));
   } else {
     // k > group size: every source goes straight to the exact tier-2 path
