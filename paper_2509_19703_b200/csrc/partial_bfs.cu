@@ -719,6 +719,241 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
   }
 }
 
+// ------------------------------------------------------------ tier C (CTA)
+// Big balls (hub-adjacent sources of scale-free graphs: a level of thousands
+// of ids): one CTA of 256 threads per source, the ball hash (HC slots), the
+// discovered list and the level's parent ranges in shared memory.  A level is
+// expanded 256 flattened entries at a time, one entry per thread; the parent
+// of entry t comes from a bitmap of adjacency starts and per-word prefix
+// counts.  First occurrences without MATCH: each entry inserts
+// (t - t0 + 1) << 23 | id, equal ids keep the smallest tag (atomicMin), ids
+// of earlier chunks and levels hold tag 0; after a barrier the entries whose
+// slot holds their own key are the chunk's first occurrences, compacted in t
+// order by warp ballots and a prefix over the 8 warp counts, and their slots
+// retagged to 0.  Needs ids below 2^23 - 1; larger graphs keep the warp
+// tier.  Replaces a 2-warp CTA with a 1024-id cap (12 warps per SM).
+constexpr int TC_THREADS = 256, TC_HC = 4096, TC_CAP = 3072, TC_PCAP = 1024, TC_TCAP = 8192;
+struct TierC {
+  static constexpr int TW = TC_TCAP / 32;
+  // hkey[HC] disc[CAP] ppre[PCAP] pbeg[PCAP] bmap[TW] pcnt[TW] jdraw[32] wcnt[8]
+  static constexpr int WORDS = TC_HC + TC_CAP + 2 * TC_PCAP + 2 * TW + 32 + 8;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    pbfs_cta(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
+             unsigned long long seed, long long src_begin, const int* __restrict__ list,
+             const int* __restrict__ list_count, int* __restrict__ out_nbr,
+             int* __restrict__ out_dist, int* __restrict__ out_cnt, int* __restrict__ ovf_list,
+             int* __restrict__ ovf_count, unsigned long long* __restrict__ work) {
+  constexpr int HC = TC_HC, CAP = TC_CAP, PCAP = TC_PCAP, TCAP = TC_TCAP, TW = TierC::TW;
+  constexpr unsigned EMPTY = 0xffffffffu, IDM = (1u << 23) - 1u;
+  extern __shared__ __align__(16) int smem[];
+  unsigned* const hkey = reinterpret_cast<unsigned*>(smem);
+  int* const disc = smem + HC;
+  int* const ppre = disc + CAP;
+  int* const pbeg = ppre + PCAP;
+  unsigned* const bmap = reinterpret_cast<unsigned*>(pbeg + PCAP);
+  int* const pcnt = reinterpret_cast<int*>(bmap + TW);
+  int* const jdraw = pcnt + TW;
+  int* const wcnt = jdraw + 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned long long w_scanned = 0, w_expanded = 0;
+  // insert an id of a settled level (tag 0); true iff it was not there
+  auto put0 = [&](int w) {
+    unsigned h = hash_slot<HC>(w);
+    for (;;) {
+      const unsigned old = atomicCAS(&hkey[h], EMPTY, (unsigned)w);
+      if (old == EMPTY || old == (unsigned)w) return;
+      h = (h + 1) & (HC - 1);
+    }
+  };
+  // block-wide exclusive prefix of one int per thread (+ total)
+  auto block_scan = [&](int v, int& total) -> int {
+    const int inc = warp_incl_scan(v);
+    if (lane == 31) wcnt[warp] = inc;
+    __syncthreads();
+    int before = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < TC_THREADS / 32; q++) {
+      const int c = wcnt[q];
+      before += q < warp ? c : 0;
+      tot += c;
+    }
+    __syncthreads();
+    total = tot;
+    return before + inc - v;
+  };
+  const int total_items = *list_count;
+  for (int it = blockIdx.x; it < total_items; it += gridDim.x) {
+    const int s = list[it];
+    const long long item = (long long)s - src_begin;
+    int* const rn = out_nbr + item * K;
+    int* const rd = out_dist + item * K;
+    const unsigned long long fy_base = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
+    for (int i = tid; i < HC / 4; i += TC_THREADS)
+      reinterpret_cast<uint4*>(hkey)[i] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+    const int b0 = __ldg(indptr + s);
+    const int T0 = __ldg(indptr + s + 1) - b0;
+    __syncthreads();
+    bool ovf = T0 > CAP - 2;
+    int count = 0, nst = 0, lb = 1, le = 1, depth = 1;
+    if (!ovf) {
+      // ---- level 1: the sorted adjacency of s
+      if (tid == 0) put0(s);
+      for (int t = tid; t < T0; t += TC_THREADS) {
+        const int w = __ldg(indices + b0 + t);
+        disc[1 + t] = w;
+        put0(w);
+      }
+      w_scanned += tid == 0 ? (unsigned long long)T0 : 0ull;
+      w_expanded += tid == 0 ? 1ull : 0ull;
+      nst = T0;
+      le = 1 + T0;
+      __syncthreads();
+    }
+    // ---- levels: level `depth` is disc[lb, le) with nst ids; output it
+    // (whole, or the Fisher-Yates subsample when it crosses K), expand it
+    while (!ovf) {
+      const int remaining = K - count;
+      int take = nst;
+      if (nst > remaining) {
+        // crossing level: draws in parallel, the r swaps by one thread
+        if (tid < remaining) jdraw[tid] = tid + umod64_tab(splitmix_at(fy_base, tid), nst - tid);
+        __syncthreads();
+        if (tid == 0) {
+          for (int i = 0; i < remaining; i++) {
+            const int j = jdraw[i];
+            const int a = disc[le - nst + i];
+            disc[le - nst + i] = disc[le - nst + j];
+            disc[le - nst + j] = a;
+          }
+        }
+        __syncthreads();
+        take = remaining;
+      }
+      // rows: this level's picks ranked by id (levels come in distance order)
+      if (tid < take) {
+        const int v = disc[le - nst + tid];
+        int r = 0;
+        for (int q = 0; q < take; q++) r += disc[le - nst + q] < v;
+        rn[count + r] = v;
+        rd[count + r] = depth;
+      }
+      count += take;
+      if (count >= K || nst == 0) break;
+      // ---- expand: parents disc[lb, le) (nonzero degrees compacted)
+      const int f = nst;
+      if (f > PCAP) {
+        ovf = true;
+        break;
+      }
+      for (int w = tid; w < TW; w += TC_THREADS) bmap[w] = 0u;
+      __syncthreads();
+      int carry = 0, nne = 0;
+      for (int i0 = 0; i0 < f; i0 += TC_THREADS) {
+        const int i = i0 + tid;
+        int d = 0, b = 0;
+        if (i < f) {
+          const int u = disc[lb + i];
+          b = __ldg(indptr + u);
+          d = __ldg(indptr + u + 1) - b;
+        }
+        int dtot, ntot;
+        const int dex = block_scan(d, dtot);
+        const int rex = block_scan(d > 0 ? 1 : 0, ntot);
+        if (d > 0) {
+          const int r = nne + rex;
+          const int p0 = carry + dex;
+          ppre[r] = p0;
+          pbeg[r] = b;
+          if (p0 < TCAP) atomicOr(&bmap[p0 >> 5], 1u << (p0 & 31));
+        }
+        carry += dtot;
+        nne += ntot;
+      }
+      const int T = carry;
+      w_scanned += tid == 0 ? (unsigned long long)T : 0ull;
+      w_expanded += tid == 0 ? (unsigned long long)f : 0ull;
+      if (T > TCAP) {
+        ovf = true;
+        break;
+      }
+      __syncthreads();
+      // prefix popcounts of the start bitmap (one word per thread)
+      {
+        int ptot, pcarry = 0;
+        for (int w0 = 0; w0 < TW; w0 += TC_THREADS) {
+          const int w = w0 + tid;
+          const int c = w < TW ? __popc(bmap[w]) : 0;
+          const int ex = block_scan(c, ptot);
+          if (w < TW) pcnt[w] = pcarry + ex;
+          pcarry += ptot;
+        }
+        __syncthreads();
+      }
+      lb = le;
+      nst = 0;
+      depth++;
+      for (int t0 = 0; t0 < T; t0 += TC_THREADS) {
+        const int t = t0 + tid;
+        const bool valid = t < T;
+        int w = 0;
+        if (valid) {
+          const int p = pcnt[t >> 5] + __popc(bmap[t >> 5] & ((2u << (t & 31)) - 1u)) - 1;
+          w = __ldg(indices + pbeg[p] + (t - ppre[p]));
+        }
+        const unsigned key = ((unsigned)(tid + 1) << 23) | (unsigned)w;
+        unsigned h = hash_slot<HC>(w), old = 0u;
+        if (valid) {
+          for (;;) {
+            old = atomicCAS(&hkey[h], EMPTY, key);
+            if (old == EMPTY || (old & IDM) == (unsigned)w) break;
+            h = (h + 1) & (HC - 1);
+          }
+        }
+        const bool mine = valid && (old == EMPTY || (old >> 23) != 0u);
+        if (mine && old != EMPTY) atomicMin(&hkey[h], key);
+        __syncthreads();
+        const bool isnew = mine && hkey[h] == key;
+        const unsigned bal = __ballot_sync(FULL, isnew);
+        if (lane == 0) wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int before = 0, tot = 0;
+#pragma unroll
+        for (int q = 0; q < TC_THREADS / 32; q++) {
+          const int c = wcnt[q];
+          before += q < warp ? c : 0;
+          tot += c;
+        }
+        if (isnew) {
+          const int pos = le + nst + before + __popc(bal & lt);
+          if (pos < CAP) disc[pos] = w;
+          hkey[h] = (unsigned)w;  // settled: tag 0
+        }
+        nst += tot;
+        __syncthreads();
+        if (le + nst > CAP) {
+          ovf = true;
+          break;
+        }
+      }
+      le += nst;
+      __syncthreads();
+    }
+    if (ovf) {
+      if (tid == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+    } else if (tid == 0) {
+      out_cnt[item] = count;
+    }
+    __syncthreads();
+  }
+  if (work && tid == 0) {
+    atomicAdd(work, w_scanned);
+    atomicAdd(work + 1, w_expanded);
+  }
+}
+
 // ----------------------------------------------------------------- tier 2
 // Exact FIFO emulation: parents in queue order, each parent's sorted
 // adjacency in 32-entry chunks; per-warp stamp array (value s+1) of n ints.
@@ -943,6 +1178,23 @@ cudaError_t launch_lean_big(int sms, long long n, const int* indptr, const int* 
       ovf_out, ovf_cnt, work, st);
 }
 
+// tier C: one 256-thread CTA per big-ball source (ids below 2^23 - 1)
+cudaError_t launch_cta(int sms, const int* indptr, const int* indices, int k,
+                       unsigned long long seed, long long src_begin, const int* list,
+                       const int* list_count, int* out_nbr, int* out_dist, int* out_count,
+                       int* ovf_out, int* ovf_cnt, unsigned long long* work, cudaStream_t st) {
+  constexpr size_t smem = sizeof(int) * TierC::WORDS;
+  cudaError_t e = cudaFuncSetAttribute(pbfs_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pbfs_cta, TC_THREADS, smem);
+  if (e != cudaSuccess) return e;
+  const unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1);
+  pbfs_cta<<<blocks, TC_THREADS, smem, st>>>(indptr, indices, k, seed, src_begin, list, list_count,
+                                              out_nbr, out_dist, out_count, ovf_out, ovf_cnt, work);
+  return cudaGetLastError();
+}
+
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -1005,8 +1257,16 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
       GU_CHECK(launch_lean(sms, n, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
                            out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
     }
-    GU_CHECK(launch_lean_big(sms, n, indptr, indices, k, seed, src_begin, nsrc, ws.ovfA, ws.counts + 0,
-                             out_nbr, out_dist, out_count, ws.ovfB, ws.counts + 1, work, st));
+    // big balls: the CTA tier when ids fit its 23-bit packed keys
+    static const char* env_big = getenv("GU_PBFS_BIG");
+    if (n < (1 << 23) - 1 && !(env_big && !strcmp(env_big, "warp"))) {
+      GU_CHECK(launch_cta(sms, indptr, indices, k, seed, src_begin, ws.ovfA, ws.counts + 0,
+                          out_nbr, out_dist, out_count, ws.ovfB, ws.counts + 1, work, st));
+    } else {
+      GU_CHECK(launch_lean_big(sms, n, indptr, indices, k, seed, src_begin, nsrc, ws.ovfA,
+                               ws.counts + 0, out_nbr, out_dist, out_count, ws.ovfB, ws.counts + 1,
+                               work, st));
+    }
   } else {
     // k > group size: every source goes straight to the exact tier-2 path
     fill_range_list<<<(unsigned)((nsrc + 255) / 256), 256, 0, st>>>(ws.ovfB, ws.counts + 1,

@@ -590,18 +590,20 @@ def test_sgd_range_records_rgg(gu):
     assert abs(ratio - 1.0) < 0.025
 
 
-def test_partial_bfs_large_ids_unpacked_path(gu, oracle):
-    """n >= 2^24 - 1: tier F switches from packed (tag << 24 | id) hash keys
-    to the MATCH election.  A scale-free graph relabelled onto the top ids of
-    a 2^24 + 7 vertex space (the rest isolated); the range of its sources
-    must equal the oracle's rows (_kernels.py:60-131)."""
+@pytest.mark.parametrize("n", [(1 << 23) + 5, (1 << 24) + 7])
+def test_partial_bfs_large_ids_unpacked_path(gu, oracle, n):
+    """Large ids: from n >= 2^23 - 1 big balls leave the CTA tier (23-bit
+    packed keys) for the 1024-id warp tier, and from n >= 2^24 - 1 tiers F /
+    1a / 1b switch from packed (tag << 24 | id) keys to the MATCH election.
+    A scale-free graph relabelled onto the top ids of an n-vertex space (the
+    rest isolated); its sources' rows must equal the oracle's
+    (_kernels.py:60-131)."""
     import torch
 
     from paper_2509_19703_b200.device import device_csr
     from paper_2509_19703_b200.fixtures import canonical_edges, graph_from_edges
     from paper_2509_19703_b200.neighbors import partial_bfs_records
 
-    n = (1 << 24) + 7
     base = gu.synth_graph("scale_free", 20000, seed=5, m0=3)
     off = n - base.n
     src = np.repeat(np.arange(base.n), np.diff(base.adj_indptr))
