@@ -739,7 +739,10 @@ struct TierC {
   static constexpr int WORDS = TC_HC + TC_CAP + 2 * TC_PCAP + 2 * TW + 32 + 8;
 };
 
-__global__ void __launch_bounds__(TC_THREADS, 1)
+#ifndef TC_MINB
+#define TC_MINB 5
+#endif
+__global__ void __launch_bounds__(TC_THREADS, TC_MINB)
     pbfs_cta(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
              unsigned long long seed, long long src_begin, const int* __restrict__ list,
              const int* __restrict__ list_count, int* __restrict__ out_nbr,
@@ -859,9 +862,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           b = __ldg(indptr + u);
           d = __ldg(indptr + u + 1) - b;
         }
-        int dtot, ntot;
-        const int dex = block_scan(d, dtot);
-        const int rex = block_scan(d > 0 ? 1 : 0, ntot);
+        // one scan for both prefixes: degree (low 22 bits; T > TCAP
+        // overflows long before) and nonzero-degree rank (high bits)
+        int ptot2;
+        const int px = block_scan(d | (d > 0 ? 1 << 22 : 0), ptot2);
+        const int dex = px & ((1 << 22) - 1), rex = px >> 22;
+        const int dtot = ptot2 & ((1 << 22) - 1), ntot = ptot2 >> 22;
         if (d > 0) {
           const int r = nne + rex;
           const int p0 = carry + dex;
@@ -882,27 +888,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       __syncthreads();
       // prefix popcounts of the start bitmap (one word per thread)
       {
-        int ptot, pcarry = 0;
-        for (int w0 = 0; w0 < TW; w0 += TC_THREADS) {
-          const int w = w0 + tid;
-          const int c = w < TW ? __popc(bmap[w]) : 0;
-          const int ex = block_scan(c, ptot);
-          if (w < TW) pcnt[w] = pcarry + ex;
-          pcarry += ptot;
+        const int nw = (T + 31) >> 5;  // words that hold entries
+        if (nw <= 32) {
+          if (warp == 0) {
+            const int c = lane < nw ? __popc(bmap[lane]) : 0;
+            pcnt[lane] = warp_incl_scan(c) - c;
+          }
+        } else {
+          int ptot, pcarry = 0;
+          for (int w0 = 0; w0 < nw; w0 += TC_THREADS) {
+            const int w = w0 + tid;
+            const int c = w < nw ? __popc(bmap[w]) : 0;
+            const int ex = block_scan(c, ptot);
+            if (w < nw) pcnt[w] = pcarry + ex;
+            pcarry += ptot;
+          }
         }
         __syncthreads();
       }
       lb = le;
       nst = 0;
       depth++;
+      // entry t's id (0 past T); the next chunk's load is issued before this
+      // chunk's hash work
+      auto entry = [&](int t) -> int {
+        if (t >= T) return 0;
+        const int p = pcnt[t >> 5] + __popc(bmap[t >> 5] & ((2u << (t & 31)) - 1u)) - 1;
+        return __ldg(indices + pbeg[p] + (t - ppre[p]));
+      };
+      int w_next = entry(tid);
       for (int t0 = 0; t0 < T; t0 += TC_THREADS) {
         const int t = t0 + tid;
         const bool valid = t < T;
-        int w = 0;
-        if (valid) {
-          const int p = pcnt[t >> 5] + __popc(bmap[t >> 5] & ((2u << (t & 31)) - 1u)) - 1;
-          w = __ldg(indices + pbeg[p] + (t - ppre[p]));
-        }
+        const int w = w_next;
+        w_next = entry(t + TC_THREADS);
         const unsigned key = ((unsigned)(tid + 1) << 23) | (unsigned)w;
         unsigned h = hash_slot<HC>(w), old = 0u;
         if (valid) {
