@@ -314,9 +314,10 @@ def run_ours(args):
                      "traffic": traffic, "peak_source": peak_kind,
                      "kernel": "gu_partial_bfs_knn (tier F pbfs_fast<8>, 98% of the call)",
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4),
-                     "limiter": "issue + dependent latency, not HBM: ~640 warp instructions per "
-                                "source at 69% of peak issue, ~4 dependent memory round trips per "
-                                "source, DRAM at 18% of peak (profiles/r01_ncu_fast4.txt, DESIGN.md K3)"},
+                     "limiter": "issue + shared-memory pipe, not HBM: ~620 warp instructions per "
+                                "source at 81% of peak issue, LSU wavefronts at 82% of peak (hash "
+                                "CAS / atomicMin / clears), DRAM at 23% of peak "
+                                "(profiles/r02_ncu_pbfs_fast_final.txt, DESIGN.md K3)"},
         # per step: tier F, tiers 1a / 1b, slot clear, tier 2 -- once, or once
         # per exchange round at N > 1 (NCCL and dtype-cast kernels not counted)
         "gpu_launches": 5 * args.steps * (4 if ws > 1 else 1),
@@ -487,10 +488,10 @@ def _sgd_bench(gu, g, args, dev, peak):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": _profile_traffic("sgd_epoch_kernel"),
                          "alg_bytes_per_update": 88,
-                         "limiter": "per-visit latency and issue: 47% occupancy (64 registers), "
-                                    "57% issue active; stalls long-scoreboard 34%, wait 23%; the "
-                                    "128-bit filter test is ~27% of the instructions; DRAM at 10% "
-                                    "of peak (profiles/r02_ncu_sgd_rec32.txt, DESIGN.md K7)"},
+                         "limiter": "per-visit latency: 48% occupancy (64 registers), 39% issue "
+                                    "active; stalls long-scoreboard 47%, short-scoreboard 24%; "
+                                    "DRAM at 8% of peak, the 32 MB coordinates L2-resident "
+                                    "(profiles/r02_ncu_sgd_range_current.txt, DESIGN.md K7)"},
             "diverged": int(div.item()) != INT32_MAX}
 
 
