@@ -585,6 +585,12 @@ static int sgd_lanes(long long concurrency) {
     const char* v = getenv("GU_SGD_MIN_LANES");
     return (v && atoi(v) >= 32) ? 32 : 16;
   }();
+  // 8 visits per warp when the cap fits the 3-CTA/SM kernel: the same visits
+  // in flight as 4x the warps of the 32-lane kernel (c3 SL 200 epochs 8.1 ->
+  // 7.8 ms, c1 GUMAP 15.1 -> 14.7 ms: profiles/r02_ab_sgd_lanes8.log)
+  if (concurrency > 0 && concurrency < resident && min_lanes == 16 &&
+      (concurrency * 32) / 8 <= 148LL * 3 * 256)
+    return 8;
   if (concurrency > 0 && concurrency < resident && min_lanes == 16 &&
       (concurrency * 32) / 16 <= 148LL * 2 * 256)  // fits the 2-CTA/SM kernel
     return 16;
@@ -666,6 +672,10 @@ static EpochKernel epoch_kernel(int lanes, int mode) {
     return mode == REC_RANGE   ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_RANGE>
            : mode == REC_BLOOM ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_BLOOM>
                                : sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_TABLE>;
+  if (lanes == 8)
+    return mode == REC_RANGE   ? sgd_epoch_kernel<8, 3, REC_RANGE>
+           : mode == REC_BLOOM ? sgd_epoch_kernel<8, 3, REC_BLOOM>
+                               : sgd_epoch_kernel<8, 3, REC_TABLE>;
   return mode == REC_RANGE   ? sgd_epoch_kernel<16, 2, REC_RANGE>
          : mode == REC_BLOOM ? sgd_epoch_kernel<16, 2, REC_BLOOM>
                              : sgd_epoch_kernel<16, 2, REC_TABLE>;

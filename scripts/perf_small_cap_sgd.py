@@ -24,5 +24,5 @@ for name, g, gk, win, samp in cases:
         torch.cuda.synchronize(); t0 = time.perf_counter()
         f(gk, init, cfg)
         torch.cuda.synchronize(); ts.append(1e3 * (time.perf_counter() - t0))
-    print(f"{name}: 200 epochs {min(ts):.2f} ms (multi={os.environ.get('GU_SGD_MULTI_EPOCH', '1')} drift={os.environ.get('GU_SGD_EPOCH_DRIFT', '0')})",
+    print(f"{name}: 200 epochs {min(ts):.2f} ms",
           flush=True)
