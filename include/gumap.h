@@ -180,6 +180,22 @@ int gu_bfs_order(int64_t n, const int32_t* indptr, const int32_t* indices, int32
                  void* workspace, size_t ws_bytes, void* stream);
 int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr, const int32_t* nbr_indices,
                            void* filter_out, void* stream);
+/* Exact neighbour sets for small concurrency caps (record_mode 3): vertex u's
+ * neighbour ids in a linear-probing table of S_u = next_pow2(4 deg(u)) int32
+ * slots (empty = -1) at table[off[u] ..).  _layout writes off (int32[n+1],
+ * exclusive sums of S_u) and the total slot count to *host_slots
+ * (synchronous; GU_ERR_UNSUPPORTED when a row exceeds 8192 ids or the total
+ * 2^28 slots); gu_sgd_neighbor_hash fills the table (`slots` int32).  The
+ * table is then the nbr_filter argument of gu_sgd_epochs for record_mode 3,
+ * whose records come from gu_sgd_prepare_edges_hash: {src, dst,
+ * float-bits(h), off[src] << 4 | log2 S_src} in the shuffled order. */
+int gu_sgd_neighbor_hash_layout(int64_t n, const int32_t* nbr_indptr, int32_t* off,
+                                int64_t* host_slots, void* stream);
+int gu_sgd_neighbor_hash(int64_t n, const int32_t* nbr_indptr, const int32_t* nbr_indices,
+                         const int32_t* off, int32_t* table, int64_t slots, void* stream);
+int gu_sgd_prepare_edges_hash(int64_t E, const int32_t* sym_src, const int32_t* sym_dst,
+                              const double* sym_w, const int32_t* off, uint64_t seed, void* edges,
+                              int32_t* perm_out, void* stream);
 int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void* edges,
                   int32_t record_mode, const int32_t* nbr_indptr, const int32_t* nbr_indices,
                   const void* nbr_filter, float a, float b,

@@ -28,6 +28,8 @@
 #include <cstring>
 #include <type_traits>
 
+#include <cub/device/device_scan.cuh>
+
 #include "common.cuh"
 #include "gumap.h"
 
@@ -152,7 +154,18 @@ enum RecMode : int {
   REC_BLOOM = 1,  // 32 bytes; + the head's 128-bit / 3-hash Bloom word
   REC_RANGE = 2,  // 32 bytes; + [min, max] of the head's neighbour ids and its
                   // 64-bit / 2-hash word (ids in a locality order, csrc/order.cu)
+  REC_HASH = 3,   // 16 bytes {src, dst, h, off << 4 | log2 size}: an exact
+                  // open-addressing set of the head's neighbour ids (small caps)
 };
+
+// Exact neighbour sets (REC_HASH): vertex u's neighbour ids in a linear-
+// probing table of S_u = next_pow2(4 deg(u)) int32 slots (load <= 1/4, empty
+// = -1) at off[u]; home slot = top log2(S_u) bits of the Fibonacci product.
+// A candidate is rejected or accepted after ~1.2 probes on average, with no
+// Bloom filter and no row search.
+__device__ __forceinline__ unsigned hset_home(int c, unsigned lg) {
+  return ((unsigned)c * 0x9E3779B1u) >> (32u - lg);
+}
 
 template <class F>
 __device__ __forceinline__ unsigned filt_bit(int c, int j) {
@@ -350,7 +363,7 @@ __global__ void __launch_bounds__(256, MINB)
     if (!act) p = 0;
     // streamed once per epoch: evict-first, keep L2 for x / filter / rows
     using F = typename std::conditional<MODE == REC_BLOOM, Filt128, Filt64>::type;
-    const int4 rec = act ? __ldcs(edges + (MODE == REC_TABLE ? 1 : 2) * p) : make_int4(0, 0, 0, 0);
+    const int4 rec = act ? __ldcs(edges + ((MODE == REC_TABLE || MODE == REC_HASH) ? 1 : 2) * p) : make_int4(0, 0, 0, 0);
     const int u = rec.x, v = rec.y;
     typename F::Word fw;
     int rlo = INT_MIN, rhi = INT_MAX;  // REC_RANGE: the head's neighbour-id window
@@ -363,6 +376,8 @@ __global__ void __launch_bounds__(256, MINB)
       rhi = f4.y;
       const uint2 f2 = make_uint2((unsigned)f4.z, (unsigned)f4.w);
       memcpy(&fw, &f2, sizeof(fw));
+    } else if (MODE == REC_HASH) {
+      memset(&fw, 0, sizeof(fw));
     } else if (filt) {
       memcpy(&fw, filt + u, sizeof(fw));
     } else {
@@ -400,7 +415,7 @@ __global__ void __launch_bounds__(256, MINB)
     // of x_u, as in the reference sweep.
     const unsigned long long vbase = mix64(rkey ^ (unsigned long long)p);
     int rb = 0, re = 0;
-    if (act) {
+    if (act && MODE != REC_HASH) {
       if (rec.w >= 0) {
         rb = rec.w >> 6;
         re = rb + (rec.w & 63);
@@ -418,13 +433,39 @@ __global__ void __launch_bounds__(256, MINB)
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         draw_q[q] = draw32(vbase, q0 + q, 0);
         cand[q] = (int)__umulhi(draw_q[q], (unsigned)n);
-        if (act && q < nq && cand[q] >= rlo && cand[q] <= rhi && filt_maybe<F>(fw, cand[q]))
+        if (MODE != REC_HASH && act && q < nq && cand[q] >= rlo && cand[q] <= rhi &&
+            filt_maybe<F>(fw, cand[q]))
           mm |= 1u << q;
       }
       float2 xc[SGD_NEG_BLOCK];
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++)
         xc[q] = (act && q < nq) ? xy[cand[q]] : make_float2(0.f, 0.f);
+      unsigned hset_hit = 0;
+      if (MODE == REC_HASH && act) {
+        // exact set test: all first probes in flight together, then the
+        // (rare) longer chains one by one
+        const int* __restrict__ tab = reinterpret_cast<const int*>(filt);
+        const unsigned hoff = (unsigned)rec.w >> 4, lg = (unsigned)rec.w & 15u;
+        const unsigned hmask = (1u << lg) - 1u;
+        unsigned hh[SGD_NEG_BLOCK];
+        int x0[SGD_NEG_BLOCK];
+#pragma unroll
+        for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+          hh[q] = hset_home(cand[q], lg);
+          x0[q] = q < nq ? __ldg(tab + hoff + hh[q]) : -1;
+        }
+#pragma unroll
+        for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+          int x = x0[q];
+          unsigned h = hh[q];
+          while (x >= 0 && x != cand[q]) {
+            h = (h + 1) & hmask;
+            x = __ldg(tab + hoff + h);
+          }
+          if (x == cand[q]) hset_hit |= 1u << q;
+        }
+      }
       // warp-cooperative neighbour test of the filter hits
       const int cnt = __popc(mm);
       int incl = cnt;
@@ -469,6 +510,7 @@ __global__ void __launch_bounds__(256, MINB)
         hit = sh_hit[wib][lane];
         __syncwarp();  // the buffers are reused by the next slot block
       }
+      if (MODE == REC_HASH) hit = hset_hit;
       if (!act) continue;
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
@@ -481,7 +523,21 @@ __global__ void __launch_bounds__(256, MINB)
           for (int t = 1; t < 8; t++) {
             const unsigned rr = draw32(vbase, q0 + q, t);
             const int cc = (int)__umulhi(rr, (unsigned)n);
-            if (cc == u || is_neighbor(nip, nix, u, cc)) continue;
+            bool nb;
+            if (MODE == REC_HASH) {
+              const int* __restrict__ tab = reinterpret_cast<const int*>(filt);
+              const unsigned hoff = (unsigned)rec.w >> 4, lg = (unsigned)rec.w & 15u;
+              unsigned h = hset_home(cc, lg);
+              int x = __ldg(tab + hoff + h);
+              while (x >= 0 && x != cc) {
+                h = (h + 1) & ((1u << lg) - 1u);
+                x = __ldg(tab + hoff + h);
+              }
+              nb = x == cc;
+            } else {
+              nb = is_neighbor(nip, nix, u, cc);
+            }
+            if (cc == u || nb) continue;
             c = cc;
             draw = rr;
             break;
@@ -651,6 +707,124 @@ static void epoch_range(int64_t E, int32_t epoch, int64_t window, int32_t window
   }
 }
 
+namespace gu {
+namespace {
+__global__ void hset_sizes(int n, const int* __restrict__ nip, int* __restrict__ sz,
+                           int* __restrict__ bad) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int d = nip[v + 1] - nip[v];
+    int S = 0;
+    if (d > 0) {
+      S = 2;
+      while (S < 4 * d && S < (1 << 16)) S <<= 1;
+      if (S < 4 * d || S > (1 << 15)) atomicExch(bad, 1);  // log2 S must fit 4 bits
+    }
+    sz[v] = S;
+  }
+}
+// one warp per vertex: its neighbour ids inserted by CAS with linear probing
+__global__ void hset_build(int n, const int* __restrict__ nip, const int* __restrict__ nix,
+                           const int* __restrict__ off, int* __restrict__ tab) {
+  const int lane = threadIdx.x & 31;
+  for (long long v = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+       v += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int b = nip[v], e = nip[v + 1];
+    const int S = off[v + 1] - off[v];
+    if (S == 0) continue;
+    const unsigned lg = 31u - (unsigned)__clz(S), mask = (unsigned)S - 1u;
+    int* const t = tab + off[v];
+    for (int p = b + lane; p < e; p += 32) {
+      const int c = nix[p];
+      unsigned h = hset_home(c, lg);
+      for (;;) {
+        const int old = atomicCAS(t + h, -1, c);
+        if (old == -1 || old == c) break;
+        h = (h + 1) & mask;
+      }
+    }
+  }
+}
+__global__ void prepare_edges_hash_kernel(long long E, const int* __restrict__ src,
+                                          const int* __restrict__ dst,
+                                          const double* __restrict__ w,
+                                          const int* __restrict__ off, unsigned long long key,
+                                          int4* __restrict__ out, int* __restrict__ perm_out) {
+  Feistel perm((unsigned long long)E, key);
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < E;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long e = (long long)perm((unsigned long long)p);
+    const int u = src[e], v = dst[e];
+    const int o = off[u], S = off[u + 1] - o;
+    const int lg = S > 0 ? 31 - __clz(S) : 0;
+    out[p] = make_int4(u, v, __float_as_int((float)w[e]), (o << 4) | lg);
+    if (perm_out) perm_out[p] = (int)e;
+  }
+}
+}  // namespace
+}  // namespace gu
+
+extern "C" int gu_sgd_neighbor_hash_layout(int64_t n, const int32_t* nbr_indptr, int32_t* off,
+                                           int64_t* host_slots, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0 || n >= INT_MAX) {
+    set_error("gu_sgd_neighbor_hash_layout: bad n=%lld", (long long)n);
+    return GU_ERR_ARG;
+  }
+  int* bad = nullptr;  // [0] flag, [1 ..] the sizes (scanned into off)
+  void* tmp = nullptr;
+  size_t tb = 0;
+  GU_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, off, off, (int)n + 1, st));
+  GU_CHECK(cudaMallocAsync((void**)&bad, sizeof(int) * (size_t)(n + 2), st));
+  GU_CHECK(cudaMallocAsync(&tmp, tb, st));
+  int* sz = bad + 1;
+  GU_CHECK(cudaMemsetAsync(bad, 0, sizeof(int) * (size_t)(n + 2), st));
+  hset_sizes<<<grid_for(n), 256, 0, st>>>((int)n, nbr_indptr, sz, bad);
+  GU_CHECK_LAUNCH("hset_sizes");
+  // total slots = 4 deg rounded up <= 8 * nnz: fits int32 whenever nnz < 2^28
+  GU_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, sz, off, (int)n + 1, st));
+  int h_bad = 0, h_tot = 0;
+  GU_CHECK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GU_CHECK(cudaMemcpyAsync(&h_tot, off + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GU_CHECK(cudaFreeAsync(bad, st));
+  GU_CHECK(cudaFreeAsync(tmp, st));
+  GU_CHECK(cudaStreamSynchronize(st));
+  if (h_bad || h_tot < 0 || h_tot >= (1 << 28)) {
+    set_error("gu_sgd_neighbor_hash_layout: a row above 8192 ids or 2^28 slots in total");
+    return GU_ERR_UNSUPPORTED;
+  }
+  *host_slots = h_tot;
+  return GU_OK;
+}
+
+extern "C" int gu_sgd_neighbor_hash(int64_t n, const int32_t* nbr_indptr,
+                                    const int32_t* nbr_indices, const int32_t* off,
+                                    int32_t* table, int64_t slots, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0 || n >= INT_MAX || slots < 0) {
+    set_error("gu_sgd_neighbor_hash: bad arguments");
+    return GU_ERR_ARG;
+  }
+  GU_CHECK(cudaMemsetAsync(table, 0xff, sizeof(int32_t) * (size_t)slots, st));
+  hset_build<<<grid_for(n * 32), 256, 0, st>>>((int)n, nbr_indptr, nbr_indices, off, table);
+  GU_CHECK_LAUNCH("hset_build");
+  return GU_OK;
+}
+
+extern "C" int gu_sgd_prepare_edges_hash(int64_t E, const int32_t* sym_src,
+                                         const int32_t* sym_dst, const double* sym_w,
+                                         const int32_t* off, uint64_t seed, void* edges,
+                                         int32_t* perm_out, void* stream) {
+  if (E < 0 || E >= INT_MAX) {
+    set_error("gu_sgd_prepare_edges_hash: unsupported E=%lld", (long long)E);
+    return GU_ERR_UNSUPPORTED;
+  }
+  if (E == 0) return GU_OK;
+  prepare_edges_hash_kernel<<<grid_for(E), 256, 0, (cudaStream_t)stream>>>(
+      E, sym_src, sym_dst, sym_w, off, seed, (int4*)edges, perm_out);
+  GU_CHECK_LAUNCH("prepare_edges_hash_kernel");
+  return GU_OK;
+}
+
 extern "C" int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr,
                                       const int32_t* nbr_indices, void* filter_out, void* stream) {
   if (n <= 0 || n >= INT_MAX) {
@@ -671,13 +845,16 @@ static EpochKernel epoch_kernel(int lanes, int mode) {
   if (lanes == 32)
     return mode == REC_RANGE   ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_RANGE>
            : mode == REC_BLOOM ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_BLOOM>
+           : mode == REC_HASH  ? sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_HASH>
                                : sgd_epoch_kernel<32, SGD_MIN_BLOCKS, REC_TABLE>;
   if (lanes == 8)
     return mode == REC_RANGE   ? sgd_epoch_kernel<8, 3, REC_RANGE>
            : mode == REC_BLOOM ? sgd_epoch_kernel<8, 3, REC_BLOOM>
+           : mode == REC_HASH  ? sgd_epoch_kernel<8, 3, REC_HASH>
                                : sgd_epoch_kernel<8, 3, REC_TABLE>;
   return mode == REC_RANGE   ? sgd_epoch_kernel<16, 2, REC_RANGE>
          : mode == REC_BLOOM ? sgd_epoch_kernel<16, 2, REC_BLOOM>
+         : mode == REC_HASH  ? sgd_epoch_kernel<16, 2, REC_HASH>
                              : sgd_epoch_kernel<16, 2, REC_TABLE>;
 }
 
@@ -688,7 +865,7 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
                              int32_t n_neg, int64_t window, int32_t windowed, uint64_t seed,
                              int64_t concurrency, int32_t* diverged, void* stream) {
   if (n <= 0 || n >= INT_MAX || E < 0 || t < 0 || epoch_begin < 0 || epoch_end > t ||
-      record_mode < REC_TABLE || record_mode > REC_RANGE || (windowed && (window < 1 || window > E))) {
+      record_mode < REC_TABLE || record_mode > REC_HASH || (windowed && (window < 1 || window > E))) {
     set_error("gu_sgd_epochs: bad arguments");
     return GU_ERR_ARG;
   }
@@ -722,7 +899,7 @@ extern "C" int gu_sgd_epochs_deterministic(int64_t n, int64_t E, float* coords_x
                                            int64_t batch, int64_t* acc, int32_t* diverged,
                                            void* stream) {
   if (n <= 0 || n >= INT_MAX || E < 0 || t < 0 || epoch_begin < 0 || epoch_end > t ||
-      batch < 32 || !acc || record_mode < REC_TABLE || record_mode > REC_RANGE ||
+      batch < 32 || !acc || record_mode < REC_TABLE || record_mode > REC_HASH ||
       (windowed && (window < 1 || window > E))) {
     set_error("gu_sgd_epochs_deterministic: bad arguments");
     return GU_ERR_ARG;

@@ -477,22 +477,72 @@ def test_partial_bfs_host_path_matches_records(gu):
     assert np.array_equal(dset.indptr, knn.indptr)
 
 
-def test_sgd_neighbor_filter_covers_neighbors(gu):
-    """The SGD negative-sampling Bloom words (csrc/sgd.cu) have the bit of
-    every neighbour set, so skipping the row search on a clear bit never
-    accepts a neighbour."""
-    from paper_2509_19703_b200.layout import _plan_for
+def test_sgd_neighbor_filter_covers_neighbors(gu, monkeypatch):
+    """The SGD negative-sampling Bloom words (csrc/sgd.cu, REC_TABLE: small
+    caps when the exact sets are off) have the bit of every neighbour set, so
+    skipping the row search on a clear bit never accepts a neighbour."""
+    from paper_2509_19703_b200.layout import REC_TABLE, SgdPlan
     import torch
 
+    monkeypatch.setenv("GU_SGD_HASH", "0")
     g = gu.synth_graph("scale_free", 5000, seed=4, m0=3)
     _, knn = gu.partial_bfs(g, 15, seed=1)
     gk = gu.smooth_knn_weights(knn)
-    plan = _plan_for(gk, 0, torch.device("cuda"))
+    plan = SgdPlan(gk, 0, torch.device("cuda"))
+    assert plan.record_mode == REC_TABLE
     filt = plan.filter.cpu().numpy().view(np.uint32)
     ip, ix = gk.nbr_indptr, gk.nbr_indices
     src = np.repeat(np.arange(gk.n), np.diff(ip))
     assert filt.shape == (gk.n, 2)
     _bloom_covers(filt[src], ix, (0x9E3779B1, 0x85EBCA77), 26)
+
+
+def test_sgd_neighbor_hash_exact(gu):
+    """Small caps use exact open-addressing sets of each head's neighbour ids
+    (REC_HASH): every record points at its head's table, the table holds
+    exactly the head's row, and the kernel's probe sequence (home slot = top
+    log2(S) bits of the Fibonacci product, linear probing to the first empty
+    slot) finds every neighbour and rejects every other id tried."""
+    from paper_2509_19703_b200.layout import REC_HASH, _plan_for
+    import torch
+
+    g = gu.synth_graph("scale_free", 5000, seed=4, m0=3)  # hubs: long rows
+    _, knn = gu.partial_bfs(g, 15, seed=1)
+    gk = gu.smooth_knn_weights(knn)
+    plan = _plan_for(gk, 0, torch.device("cuda"))
+    assert plan.record_mode == REC_HASH
+    tab = plan.filter.cpu().numpy()
+    rec = plan.edges.cpu().numpy()
+    perm = plan.perm.cpu().numpy()
+    assert np.array_equal(rec[:, 0], gk.sym_src[perm]) and np.array_equal(rec[:, 1], gk.sym_dst[perm])
+    ip, ix = gk.nbr_indptr, gk.nbr_indices
+    off = np.zeros(gk.n, np.int64)
+    lg = np.zeros(gk.n, np.int64)
+    off[rec[:, 0]] = rec[:, 3].astype(np.uint32) >> 4
+    lg[rec[:, 0]] = rec[:, 3] & 15
+    rng = np.random.default_rng(3)
+
+    def member(u, c):
+        S = 1 << int(lg[u])
+        h = ((int(c) * 0x9E3779B1) & 0xFFFFFFFF) >> (32 - int(lg[u]))
+        while True:
+            x = tab[off[u] + h]
+            if x == c:
+                return True
+            if x < 0:
+                return False
+            h = (h + 1) & (S - 1)
+
+    for u in np.unique(rec[:, 0]):
+        row = ix[ip[u]:ip[u + 1]]
+        S = 1 << int(lg[u])
+        assert S >= 4 * row.shape[0]
+        slots = tab[off[u]:off[u] + S]
+        assert np.array_equal(np.sort(slots[slots >= 0]), np.sort(row))
+        if u % 7 == 0:
+            assert all(member(u, c) for c in row)
+            others = np.setdiff1d(rng.integers(0, gk.n, 40), row)
+            assert not any(member(u, c) for c in others)
 
 
 def _bloom_covers(words, ids, mults, shift):
