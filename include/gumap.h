@@ -181,8 +181,8 @@ int gu_bfs_order(int64_t n, const int32_t* indptr, const int32_t* indices, int32
 int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr, const int32_t* nbr_indices,
                            void* filter_out, void* stream);
 /* Exact neighbour sets for small concurrency caps (record_mode 3): vertex u's
- * neighbour ids in a linear-probing table of S_u = next_pow2(4 deg(u)) int32
- * slots (empty = -1) at table[off[u] ..).  _layout writes off (int32[n+1],
+ * neighbour ids in a table of S_u = next_pow2(4 deg(u)) >= 4 int32 slots
+ * (empty = -1) at table[off[u] ..), probed in buckets of 4 slots (16 bytes).  _layout writes off (int32[n+1],
  * exclusive sums of S_u) and the total slot count to *host_slots
  * (synchronous; GU_ERR_UNSUPPORTED when a row exceeds 8192 ids or the total
  * 2^28 slots); gu_sgd_neighbor_hash fills the table (`slots` int32).  The

@@ -158,13 +158,15 @@ enum RecMode : int {
                   // open-addressing set of the head's neighbour ids (small caps)
 };
 
-// Exact neighbour sets (REC_HASH): vertex u's neighbour ids in a linear-
-// probing table of S_u = next_pow2(4 deg(u)) int32 slots (load <= 1/4, empty
-// = -1) at off[u]; home slot = top log2(S_u) bits of the Fibonacci product.
-// A candidate is rejected or accepted after ~1.2 probes on average, with no
-// Bloom filter and no row search.
-__device__ __forceinline__ unsigned hset_home(int c, unsigned lg) {
-  return ((unsigned)c * 0x9E3779B1u) >> (32u - lg);
+// Exact neighbour sets (REC_HASH): vertex u's neighbour ids in a table of
+// S_u = next_pow2(4 deg(u)) >= 4 int32 slots (load <= 1/4, empty = -1) at
+// off[u], as buckets of 4 slots; home bucket = top log2(S_u / 4) bits of the
+// Fibonacci product, linear probing over buckets.  One 16-byte load answers
+// almost every candidate, with no Bloom filter and no row search.
+// (buckets of 4 slots, one 16-byte load each: a set at load <= 1/4 answers
+// almost every lookup with its home bucket)
+__device__ __forceinline__ unsigned hset_bucket(int c, unsigned lg) {
+  return lg > 2 ? ((unsigned)c * 0x9E3779B1u) >> (34u - lg) : 0u;
 }
 
 template <class F>
@@ -445,36 +447,40 @@ __global__ void __launch_bounds__(256, MINB)
       if (MODE == REC_HASH && act) {
         // exact set test: all first probes in flight together, then the
         // (rare) longer chains one by one
-        const int* __restrict__ tab = reinterpret_cast<const int*>(filt);
+        const int4* __restrict__ tab = reinterpret_cast<const int4*>(filt);
         const unsigned hoff = (unsigned)rec.w >> 4, lg = (unsigned)rec.w & 15u;
-        const unsigned hmask = (1u << lg) - 1u;
-        unsigned hh[SGD_NEG_BLOCK];
-        int x0[SGD_NEG_BLOCK];
+        const unsigned b0 = hoff >> 2, bmask = (1u << (lg - 2)) - 1u;
+        unsigned hb[SGD_NEG_BLOCK];
+        int4 x0[SGD_NEG_BLOCK];
 #pragma unroll
         for (int q = 0; q < SGD_NEG_BLOCK; q++) {
-          hh[q] = hset_home(cand[q], lg);
-          x0[q] = q < nq ? __ldg(tab + hoff + hh[q]) : -1;
+          hb[q] = hset_bucket(cand[q], lg);
+          x0[q] = q < nq ? __ldg(tab + b0 + hb[q]) : make_int4(-1, -1, -1, -1);
         }
 #pragma unroll
         for (int q = 0; q < SGD_NEG_BLOCK; q++) {
-          int x = x0[q];
-          unsigned h = hh[q];
-          while (x >= 0 && x != cand[q]) {
-            h = (h + 1) & hmask;
-            x = __ldg(tab + hoff + h);
+          int4 x = x0[q];
+          unsigned h = hb[q];
+          const int c = cand[q];
+          // a full bucket of other ids sends the probe to the next bucket
+          while (x.x != c && x.y != c && x.z != c && x.w != c && (x.x | x.y | x.z | x.w) >= 0) {
+            h = (h + 1) & bmask;
+            x = __ldg(tab + b0 + h);
           }
-          if (x == cand[q]) hset_hit |= 1u << q;
+          if (x.x == c || x.y == c || x.z == c || x.w == c) hset_hit |= 1u << q;
         }
       }
       // warp-cooperative neighbour test of the filter hits
       const int cnt = __popc(mm);
-      int incl = cnt;
+      int incl = cnt, total = 0;
+      if (MODE != REC_HASH) {  // exact sets need no row search
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += y;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += y;
+        }
+        total = __shfl_sync(FULL, incl, 31);
       }
-      const int total = __shfl_sync(FULL, incl, 31);
       unsigned hit = 0;
       if (total > 0) {  // warp-uniform
         int pos = incl - cnt;
@@ -525,15 +531,16 @@ __global__ void __launch_bounds__(256, MINB)
             const int cc = (int)__umulhi(rr, (unsigned)n);
             bool nb;
             if (MODE == REC_HASH) {
-              const int* __restrict__ tab = reinterpret_cast<const int*>(filt);
+              const int4* __restrict__ tab = reinterpret_cast<const int4*>(filt);
               const unsigned hoff = (unsigned)rec.w >> 4, lg = (unsigned)rec.w & 15u;
-              unsigned h = hset_home(cc, lg);
-              int x = __ldg(tab + hoff + h);
-              while (x >= 0 && x != cc) {
-                h = (h + 1) & ((1u << lg) - 1u);
-                x = __ldg(tab + hoff + h);
+              const unsigned b0 = hoff >> 2;
+              unsigned h = hset_bucket(cc, lg);
+              int4 x = __ldg(tab + b0 + h);
+              while (x.x != cc && x.y != cc && x.z != cc && x.w != cc && (x.x | x.y | x.z | x.w) >= 0) {
+                h = (h + 1) & ((1u << (lg - 2)) - 1u);
+                x = __ldg(tab + b0 + h);
               }
-              nb = x == cc;
+              nb = x.x == cc || x.y == cc || x.z == cc || x.w == cc;
             } else {
               nb = is_neighbor(nip, nix, u, cc);
             }
@@ -715,7 +722,7 @@ __global__ void hset_sizes(int n, const int* __restrict__ nip, int* __restrict__
     const int d = nip[v + 1] - nip[v];
     int S = 0;
     if (d > 0) {
-      S = 2;
+      S = 4;
       while (S < 4 * d && S < (1 << 16)) S <<= 1;
       if (S < 4 * d || S > (1 << 15)) atomicExch(bad, 1);  // log2 S must fit 4 bits
     }
@@ -731,15 +738,16 @@ __global__ void hset_build(int n, const int* __restrict__ nip, const int* __rest
     const int b = nip[v], e = nip[v + 1];
     const int S = off[v + 1] - off[v];
     if (S == 0) continue;
-    const unsigned lg = 31u - (unsigned)__clz(S), mask = (unsigned)S - 1u;
+    const unsigned lg = 31u - (unsigned)__clz(S), bmask = ((unsigned)S >> 2) - 1u;
     int* const t = tab + off[v];
     for (int p = b + lane; p < e; p += 32) {
       const int c = nix[p];
-      unsigned h = hset_home(c, lg);
-      for (;;) {
-        const int old = atomicCAS(t + h, -1, c);
-        if (old == -1 || old == c) break;
-        h = (h + 1) & mask;
+      unsigned h = hset_bucket(c, lg);
+      for (bool done = false; !done; h = (h + 1) & bmask) {
+        for (int j = 0; j < 4 && !done; j++) {
+          const int old = atomicCAS(t + 4 * h + j, -1, c);
+          done = old == -1 || old == c;
+        }
       }
     }
   }

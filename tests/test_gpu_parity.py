@@ -500,9 +500,10 @@ def test_sgd_neighbor_filter_covers_neighbors(gu, monkeypatch):
 def test_sgd_neighbor_hash_exact(gu):
     """Small caps use exact open-addressing sets of each head's neighbour ids
     (REC_HASH): every record points at its head's table, the table holds
-    exactly the head's row, and the kernel's probe sequence (home slot = top
-    log2(S) bits of the Fibonacci product, linear probing to the first empty
-    slot) finds every neighbour and rejects every other id tried."""
+    exactly the head's row, and the kernel's probe sequence (buckets of 4
+    slots, home bucket = top log2(S / 4) bits of the Fibonacci product, linear
+    probing over buckets until one holds the id or an empty slot) finds every
+    neighbour and rejects every other id tried."""
     from paper_2509_19703_b200.layout import REC_HASH, _plan_for
     import torch
 
@@ -523,15 +524,15 @@ def test_sgd_neighbor_hash_exact(gu):
     rng = np.random.default_rng(3)
 
     def member(u, c):
-        S = 1 << int(lg[u])
-        h = ((int(c) * 0x9E3779B1) & 0xFFFFFFFF) >> (32 - int(lg[u]))
+        nb = (1 << int(lg[u])) // 4
+        h = ((int(c) * 0x9E3779B1) & 0xFFFFFFFF) >> (34 - int(lg[u])) if lg[u] > 2 else 0
         while True:
-            x = tab[off[u] + h]
-            if x == c:
+            x = tab[off[u] + 4 * h: off[u] + 4 * h + 4]
+            if (x == c).any():
                 return True
-            if x < 0:
+            if (x < 0).any():
                 return False
-            h = (h + 1) & (S - 1)
+            h = (h + 1) % nb
 
     for u in np.unique(rec[:, 0]):
         row = ix[ip[u]:ip[u + 1]]
