@@ -669,3 +669,23 @@ def test_partial_bfs_large_ids_unpacked_path(gu, oracle, n):
     assert np.array_equal(cnt.cpu().numpy(), o_c)
     assert np.array_equal(nb.cpu().numpy().reshape(-1), o_n)
     assert np.array_equal(dd.cpu().numpy().reshape(-1), o_d)
+
+
+def test_sgd_hash_fallback_for_huge_rows(gu):
+    """A row above 8192 neighbour ids (a star's hub) cannot use the exact
+    neighbour sets: the small-cap plan falls back to the gathered Bloom
+    table (REC_TABLE) and the epochs still run."""
+    from paper_2509_19703_b200.fixtures import canonical_edges, graph_from_edges
+    from paper_2509_19703_b200.layout import REC_TABLE, _plan_for
+    import torch
+
+    n = 10000
+    pairs = np.stack([np.zeros(n - 1, np.int64), np.arange(1, n)], axis=1)
+    g = graph_from_edges(n, canonical_edges(n, pairs))
+    _, knn = gu.partial_bfs(g, 15, seed=0)
+    gk = gu.smooth_knn_weights(knn)
+    assert int(np.diff(gk.nbr_indptr).max()) > 8192
+    plan = _plan_for(gk, 0, torch.device("cuda"))
+    assert plan.record_mode == REC_TABLE
+    lay = gu.optimize_full(gk, gu.random_init(g, 0), gu.OptimizerConfig(iterations=5, k=15, seed=0))
+    assert np.all(np.isfinite(lay.coords))
