@@ -18,9 +18,15 @@
 // Tiers (no host sync between them; overflow lists live in device memory):
 //   tier F   register fast path: levels 1-2 reach k, deg(s) <= 32 (default)
 //   tier 1a  lean warp per source, shared hash, CAP=128 discovered vertices
-//   tier 1b  lean warp per source, shared hash, CAP=1024
+//   tier C   one 256-thread CTA per source, 4096-slot shared hash, CAP=3072
+//            (hub-adjacent balls; ids < 2^23 - 1)
+//   tier 1b  lean warp per source, shared hash, CAP=1024 (tier C's role
+//            when ids >= 2^23 - 1)
 //   tier 2   per-warp global stamp array of n ints, parents expanded
 //            sequentially in queue order (any level size, any k)
+// First occurrences within a chunk are found by packed (tag << 24 | id)
+// keys and a shared atomicMin when ids < 2^24 - 1, by a MATCH election
+// otherwise (a MATCH costs an ADU slot per distinct value: see tier F).
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
