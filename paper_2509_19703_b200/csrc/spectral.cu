@@ -141,7 +141,10 @@ int launch_dots(int n, const double* B, int nb, const double* x, double* partial
 // order (deterministic).  Replaces four cuBLAS GEMV passes, a norm and a
 // scale per step (the torch loop of round 1).
 constexpr int LZ_MAX_ROWS = SP_MAX_BASIS + 36;  // B rows + V rows (ncv <= 35)
-constexpr int LZ_BLOCKS = 148 * 4;
+#ifndef LZ_BLOCKS_PER_SM
+#define LZ_BLOCKS_PER_SM 2  // lz_rows keeps <= 40 row values per thread: 2 CTAs per SM
+#endif
+constexpr int LZ_BLOCKS = 148 * LZ_BLOCKS_PER_SM;  // one wave
 
 struct LzWs {
   double* y;        // n
@@ -313,8 +316,19 @@ __global__ void lz_final(const double* __restrict__ partial, int nr, int nblocks
   __shared__ double s[LZ_MAX_ROWS + 1];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int r = wid; r < nr; r += blockDim.x >> 5) {
-    double v = 0.0;
-    for (int k = lane; k < nblocks; k += 32) v += partial[(long long)r * nblocks + k];
+    // four independent partial sums per lane (loads in flight together),
+    // combined in a fixed order: deterministic
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    const double* pr = partial + (long long)r * nblocks;
+    int k = lane;
+    for (; k + 96 < nblocks; k += 128) {
+      v0 += pr[k];
+      v1 += pr[k + 32];
+      v2 += pr[k + 64];
+      v3 += pr[k + 96];
+    }
+    for (; k < nblocks; k += 32) v0 += pr[k];
+    double v = (v0 + v1) + (v2 + v3);
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
     if (lane == 0) s[r] = v;
   }
@@ -336,9 +350,17 @@ __global__ void lz_write_h(const double* __restrict__ hsum, const double* __rest
                            int nb, int jrows, const double* __restrict__ partial_norm,
                            int nblocks, double* __restrict__ H, int ncv, int j,
                            double* __restrict__ beta) {
+  // ||w||^2 from the block partials: strided per-thread sums, then a fixed
+  // shuffle / shared tree (deterministic; was one thread's serial loop)
+  __shared__ double sw[32];
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < nblocks; k += blockDim.x) acc += partial_norm[k];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(FULL, acc, o);
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = acc;
+  __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int k = 0; k < nblocks; k++) s += partial_norm[k];
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += sw[w];
     const double bt = sqrt(s);
     *beta = bt;
     H[(long long)(j + 1) * ncv + j] = bt;
