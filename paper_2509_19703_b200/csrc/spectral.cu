@@ -141,8 +141,13 @@ int launch_dots(int n, const double* B, int nb, const double* x, double* partial
 // order (deterministic).  Replaces four cuBLAS GEMV passes, a norm and a
 // scale per step (the torch loop of round 1).
 constexpr int LZ_MAX_ROWS = SP_MAX_BASIS + 36;  // B rows + V rows (ncv <= 35)
+#ifndef LZ_ACC
+#define LZ_ACC 1
+#endif
 #ifndef LZ_BLOCKS_PER_SM
-#define LZ_BLOCKS_PER_SM 2  // lz_rows keeps <= 40 row values per thread: 2 CTAs per SM
+// lz_rows keeps <= 40 row values per thread (2 CTAs per SM); lz_rows_acc
+// also keeps 40 accumulators (1 CTA per SM)
+#define LZ_BLOCKS_PER_SM (LZ_ACC ? 1 : 2)
 #endif
 constexpr int LZ_BLOCKS = 148 * LZ_BLOCKS_PER_SM;  // one wave
 
@@ -285,6 +290,62 @@ __global__ void __launch_bounds__(SP_THREADS, 2)
     double s = 0.0;
     for (int k = 0; k < SP_THREADS / 32; k++) s += sh[r][k];
     partial[(long long)r * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// lz_rows with the dots accumulated per thread in registers (one shuffle
+// reduction per row at the end instead of per 32 elements): ~2x the
+// registers, one CTA per SM, a row pass bound by its loads.  Same
+// partial[r][block] contract; the sums' order differs from lz_rows (both
+// are fixed, so each is deterministic).
+template <bool DOTS, bool NORM, int NRMAX>
+__global__ void __launch_bounds__(SP_THREADS, 1)
+    lz_rows_acc(int n, const double* __restrict__ B, int nb, const double* __restrict__ V,
+                int nr, const double* __restrict__ coef, const double* __restrict__ x,
+                double* __restrict__ out, double* __restrict__ partial) {
+  __shared__ double c[NRMAX];
+  __shared__ double sh[NRMAX + 1][SP_THREADS / 32];
+  for (int r = threadIdx.x; r < NRMAX; r += blockDim.x) c[r] = (coef && r < nr) ? coef[r] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double acc[NRMAX];
+#pragma unroll
+  for (int r = 0; r < NRMAX; r++) acc[r] = 0.0;
+  double nacc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double vals[NRMAX];
+#pragma unroll
+    for (int r = 0; r < NRMAX; r++) vals[r] = r < nr ? __ldg(lz_row(B, nb, V, n, r) + i) : 0.0;
+    double o = x[i];
+    if (coef) {
+#pragma unroll
+      for (int r = 0; r < NRMAX; r++) o -= vals[r] * c[r];
+    }
+    if (out) out[i] = o;
+    if (DOTS) {
+#pragma unroll
+      for (int r = 0; r < NRMAX; r++) acc[r] = fma(vals[r], o, acc[r]);
+    }
+    if (NORM) nacc = fma(o, o, nacc);
+  }
+  if (DOTS) {
+#pragma unroll
+    for (int r = 0; r < NRMAX; r++) {
+      double v = acc[r];
+      for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(FULL, v, m);
+      if (lane == 0 && r < nr) sh[r][wid] = v;
+    }
+  }
+  if (NORM) {
+    for (int m = 16; m > 0; m >>= 1) nacc += __shfl_xor_sync(FULL, nacc, m);
+    if (lane == 0) sh[nr][wid] = nacc;
+  }
+  __syncthreads();
+  const int r0 = DOTS ? 0 : nr, r1 = NORM ? nr + 1 : nr;
+  for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
+    double sum = 0.0;
+    for (int k = 0; k < SP_THREADS / 32; k++) sum += sh[r][k];
+    partial[(long long)r * gridDim.x + blockIdx.x] = sum;
   }
 }
 
@@ -508,13 +569,22 @@ extern "C" int gu_lanczos_step(int64_t n, const int32_t* indptr, const int32_t* 
   spec_spmv<<<(unsigned)sblocks, SP_THREADS, 0, st>>>(N, indptr, indices, inv_sqrt, ws.xp, ws.z,
                                                       ws.y);
   GU_CHECK_LAUNCH("spec_spmv");
-  lz_rows<true, false><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, nullptr, ws.y,
-                                                         nullptr, ws.partial);
+  const bool acc_mode = LZ_ACC;
+  if (acc_mode)
+    lz_rows_acc<true, false, LZ_MAX_ROWS><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(
+        N, basis, nb, V, nr, nullptr, ws.y, nullptr, ws.partial);
+  else
+    lz_rows<true, false><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, nullptr, ws.y,
+                                                           nullptr, ws.partial);
   GU_CHECK_LAUNCH("lz_rows");
   lz_final<<<1, SP_THREADS, 0, st>>>(ws.partial, nr, LZ_BLOCKS, nb, jrows, VB, 1, ws.coef,
                                      ws.hsum);
   GU_CHECK_LAUNCH("lz_final");
   // pass 2: w = y - B c - V h, dots [B; V]^T w
+  if (acc_mode)
+    lz_rows_acc<true, false, LZ_MAX_ROWS><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(
+        N, basis, nb, V, nr, ws.coef, ws.y, ws.w, ws.partial);
+  else
   lz_rows<true, false><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, ws.coef, ws.y,
                                                          ws.w, ws.partial);
   GU_CHECK_LAUNCH("lz_rows");
@@ -522,6 +592,10 @@ extern "C" int gu_lanczos_step(int64_t n, const int32_t* indptr, const int32_t* 
                                      nullptr);
   GU_CHECK_LAUNCH("lz_final");
   // pass 3: w -= B c' + V h', ||w||^2 (partial row nr)
+  if (acc_mode)
+    lz_rows_acc<false, true, LZ_MAX_ROWS><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(
+        N, basis, nb, V, nr, ws.coef, ws.w, ws.w, ws.partial);
+  else
   lz_rows<false, true><<<LZ_BLOCKS, SP_THREADS, 0, st>>>(N, basis, nb, V, nr, ws.coef, ws.w,
                                                          ws.w, ws.partial);
   GU_CHECK_LAUNCH("lz_rows");
