@@ -178,6 +178,12 @@ size_t gu_bfs_order_workspace_size(int64_t n, int64_t m);
 int gu_bfs_order(int64_t n, const int32_t* indptr, const int32_t* indices, int32_t* order,
                  int32_t* perm, int32_t* new_indptr, int32_t* new_indices, int32_t* host_levels,
                  void* workspace, size_t ws_bytes, void* stream);
+/* numpy.random.default_rng(seed).uniform(low, high, count) (PCG64 seeded by
+ * SeedSequence(seed), numpy's next_double and random_uniform), bit-exact, into
+ * device float64 out[count]; replaces random_init's draws (layout.py:307-311)
+ * for large n. */
+int gu_random_uniform(int64_t count, uint64_t seed, double low, double high, double* out,
+                      void* stream);
 int gu_sgd_neighbor_filter(int64_t n, const int32_t* nbr_indptr, const int32_t* nbr_indices,
                            void* filter_out, void* stream);
 /* Exact neighbour sets for small concurrency caps (record_mode 3): vertex u's

@@ -99,6 +99,7 @@ SIGNATURES = {
     "gu_bfs_order_workspace_size": (_c_sz, [_c_i64, _c_i64]),
     "gu_bfs_order": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_sz, _vp]),
     "gu_sgd_neighbor_filter": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp]),
+    "gu_random_uniform": (ctypes.c_int, [_c_i64, _c_u64, _c_f64, _c_f64, _vp, _vp]),
     "gu_sgd_neighbor_hash_layout": (ctypes.c_int, [_c_i64, _vp, _vp, ctypes.POINTER(_c_i64), _vp]),
     "gu_sgd_neighbor_hash": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _c_i64, _vp]),
     "gu_sgd_prepare_edges_hash": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _c_u64, _vp, _vp,

@@ -143,6 +143,45 @@ size_t scan_workspace(long long nrows) {
 
 using namespace gu;
 
+namespace gu {
+namespace {
+// numpy Generator(PCG64(SeedSequence(seed))).uniform(low, high, count):
+// element f = low + (high - low) * ((next_uint64 >> 11) * 2^-53) of the f-th
+// draw (numpy distributions.c random_uniform / next_double; no FMA).  Each
+// thread jumps its generator to its first element (pcg64_advance) and walks
+// a run of consecutive elements.
+constexpr int RU_RUN = 64;
+__global__ void random_uniform_kernel(long long count, unsigned long long seed, double low,
+                                      double range, double* __restrict__ out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long f0 = t * RU_RUN;
+  if (f0 >= count) return;
+  Pcg64 r;
+  pcg64_from_seedseq(r, seed, 0, false);
+  pcg64_advance(r, (unsigned long long)f0);
+  const long long f1 = f0 + RU_RUN < count ? f0 + RU_RUN : count;
+  for (long long f = f0; f < f1; f++) {
+    const double d = (double)(r.next64() >> 11) * (1.0 / 9007199254740992.0);
+    out[f] = __dadd_rn(low, __dmul_rn(range, d));
+  }
+}
+}  // namespace
+}  // namespace gu
+
+extern "C" int gu_random_uniform(int64_t count, uint64_t seed, double low, double high,
+                                 double* out, void* stream) {
+  if (count < 0) {
+    gu::set_error("gu_random_uniform: negative count");
+    return GU_ERR_ARG;
+  }
+  if (count == 0) return GU_OK;
+  const long long threads = (count + gu::RU_RUN - 1) / gu::RU_RUN;
+  gu::random_uniform_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      count, seed, low, high - low, out);
+  GU_CHECK_LAUNCH("random_uniform_kernel");
+  return GU_OK;
+}
+
 extern "C" int gu_version(void) { return 1; }
 extern "C" const char* gu_last_error(void) { return g_err; }
 

@@ -134,7 +134,9 @@ __device__ __forceinline__ uint32_t ss_mix(uint32_t x, uint32_t y) {
   r ^= r >> 16;
   return r;
 }
-__device__ inline void pcg64_from_seedseq(Pcg64& r, uint64_t seed, uint64_t key) {
+// has_key false: SeedSequence(seed) without a spawn key (np.random.default_rng(seed))
+__device__ inline void pcg64_from_seedseq(Pcg64& r, uint64_t seed, uint64_t key,
+                                          bool has_key = true) {
   uint32_t ent[8];
   int ne = 0;
   if (seed == 0) {
@@ -146,8 +148,9 @@ __device__ inline void pcg64_from_seedseq(Pcg64& r, uint64_t seed, uint64_t key)
       x >>= 32;
     }
   }
-  while (ne < 4) ent[ne++] = 0;
-  if (key == 0) {
+  while (ne < 4) ent[ne++] = 0;  // (without a key: hashmix(0) fills the pool alike)
+  if (!has_key) {
+  } else if (key == 0) {
     ent[ne++] = 0;
   } else {
     uint64_t x = key;
@@ -194,6 +197,22 @@ __device__ inline void pcg64_from_seedseq(Pcg64& r, uint64_t seed, uint64_t key)
   r.buf32 = 0;
 }
 
+
+// PCG64 jump ahead by `delta` steps (LCG power by squaring, mod 2^128)
+__device__ inline void pcg64_advance(Pcg64& r, uint64_t delta) {
+  const u128 M = {0x2360ED051FC65DA4ULL, 0x4385DF649FCCF645ULL};
+  u128 acc_mult = {0, 1}, acc_plus = {0, 0}, cur_mult = M, cur_plus = r.inc;
+  while (delta) {
+    if (delta & 1ull) {
+      acc_mult = mul128(acc_mult, cur_mult);
+      acc_plus = add128(mul128(acc_plus, cur_mult), cur_plus);
+    }
+    cur_plus = mul128(add128(cur_mult, u128{0, 1}), cur_plus);
+    cur_mult = mul128(cur_mult, cur_mult);
+    delta >>= 1;
+  }
+  r.state = add128(mul128(acc_mult, r.state), acc_plus);
+}
 
 // ------------------------------------------------------------ warp utils
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }

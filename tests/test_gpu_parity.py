@@ -689,3 +689,23 @@ def test_sgd_hash_fallback_for_huge_rows(gu):
     assert plan.record_mode == REC_TABLE
     lay = gu.optimize_full(gk, gu.random_init(g, 0), gu.OptimizerConfig(iterations=5, k=15, seed=0))
     assert np.all(np.isfinite(lay.coords))
+
+
+def test_random_uniform_matches_numpy(gu):
+    """gu_random_uniform == numpy default_rng(seed).uniform(low, high, count)
+    bit for bit (PCG64 jump-ahead per thread run), and random_init's GPU path
+    equals the reference's numpy draws."""
+    import torch
+
+    from paper_2509_19703_b200 import _lib
+    from paper_2509_19703_b200.device import stream_ptr
+
+    for seed, count, lo, hi in ((0, 1, -10.0, 10.0), (2, 200_003, -10.0, 10.0),
+                                (2**40 + 3, 4097, -1.5, 3.25), (2**64 - 1, 777, 0.0, 1.0)):
+        out = torch.empty(count, dtype=torch.float64, device="cuda")
+        _lib.call("gu_random_uniform", count, seed, lo, hi, _lib.ptr(out), stream_ptr())
+        ref = np.random.default_rng(seed).uniform(lo, hi, count)
+        assert np.array_equal(out.cpu().numpy(), ref), seed
+    g = gu.synth_graph("scale_free", 100_000, seed=2, m0=3)
+    lay = gu.random_init(g, 7, 10.0)
+    assert np.array_equal(lay.coords, np.random.default_rng(7).uniform(-10.0, 10.0, (g.n, 2)))
