@@ -72,7 +72,7 @@ def test_partial_bfs_c3_bitexact(gu):
 def test_partial_bfs_all_tiers_and_large_k(gu, oracle):
     """k > 32 (tier 2 only) and hub-heavy balls (tier 1b / 2) vs the oracle."""
     g = gu.synth_graph("scale_free", 3000, seed=5, m0=2)
-    for k in (15, 40, 100):
+    for k in (1, 3, 15, 32, 40, 100):
         _, knn = gu.partial_bfs(g, k, seed=11)
         ip, dst, dist = oracle.partial_bfs(g, k, seed=11, nthreads=4)
         assert np.array_equal(knn.indptr, ip) and np.array_equal(knn.dst, dst)
@@ -709,3 +709,18 @@ def test_random_uniform_matches_numpy(gu):
     g = gu.synth_graph("scale_free", 100_000, seed=2, m0=3)
     lay = gu.random_init(g, 7, 10.0)
     assert np.array_equal(lay.coords, np.random.default_rng(7).uniform(-10.0, 10.0, (g.n, 2)))
+
+
+def test_sgd_negative_counts_small_cap(gu):
+    """Small-cap epochs (exact neighbour sets) with 0 and 7 negatives per
+    visit (two slot blocks): finite layouts; 0 negatives moves the layout by
+    attraction only (the points contract)."""
+    g = gu.synth_graph("grid", 2500)
+    gk = gu.smooth_knn_weights(gu.knn_from_full_distances(gu.all_pairs_bfs(g), 15, seed=0))
+    init = gu.random_init(g, 0, 10.0)
+    for nn in (0, 7):
+        cfg = gu.OptimizerConfig(iterations=20, k=15, seed=0, negative_sample_count=nn)
+        lay = gu.optimize_full(gk, init, cfg)
+        assert np.all(np.isfinite(lay.coords))
+        if nn == 0:
+            assert np.std(lay.coords) < np.std(init.coords)
