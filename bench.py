@@ -312,7 +312,8 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "peak_source": peak_kind,
-                     "kernel": "gu_partial_bfs_knn (tier F pbfs_fast<8>, 98% of the call)",
+                     "kernel": "gu_partial_bfs_knn (tier F pbfs_fast<8>: 96% of the call's kernel time, "
+                               "profiles/r02_bench_launches_summary.txt)",
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4),
                      "limiter": "issue + shared-memory pipe, not HBM: ~620 warp instructions per "
                                 "source at 81% of peak issue, LSU wavefronts at 82% of peak (hash "
