@@ -43,16 +43,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef SGD_SCAN
 #define SGD_SCAN 16  // neighbour-row entries compared with independent loads
 #endif
-#ifndef SGD_LDMODE
-#define SGD_LDMODE 1  // L2-only coordinate gathers: c5 epoch 2.352 -> 2.33 ms, c4 0.600 -> 0.590 ms
-#endif
-#if SGD_LDMODE == 1
+// coordinate gathers cached in L2 only (the 32 MB array never fits L1):
+// c5 epoch 2.352 -> 2.33 ms, c4 0.600 -> 0.590 ms (profiles/r02_ab_sgd_ldcg.log)
 #define SGD_LD(p) __ldcg(p)
-#elif SGD_LDMODE == 2
-#define SGD_LD(p) __ldlu(p)
-#else
-#define SGD_LD(p) (*(p))
-#endif
 #ifndef SGD_MIN_BLOCKS
 #define SGD_MIN_BLOCKS 4  // <= 64 registers: 32 warps per SM
 #endif  // negatives handled in lockstep per block
