@@ -724,3 +724,36 @@ def test_sgd_negative_counts_small_cap(gu):
         assert np.all(np.isfinite(lay.coords))
         if nn == 0:
             assert np.std(lay.coords) < np.std(init.coords)
+
+
+@pytest.mark.parametrize("case", ["n1", "n2", "k20_1", "k20_15", "k20_19", "k20_25", "star_15",
+                                  "star_32", "star_33", "path_15"])
+def test_partial_bfs_edge_shapes(gu, oracle, case):
+    """Degenerate shapes against the oracle: a single vertex, no edges, a
+    clique at k up to and beyond n - 1 (level-1 crossings of every size), a
+    1000-leaf star around k = 32 (hub rows: tier C / tier 2) and a path."""
+    from paper_2509_19703_b200.fixtures import canonical_edges, graph_from_edges
+
+    def g_of(n, pairs):
+        return graph_from_edges(n, canonical_edges(n, np.asarray(pairs, np.int64).reshape(-1, 2)))
+
+    kind, _, kk = case.partition("_")
+    if kind == "n1":
+        g, k = g_of(1, []), 5
+    elif kind == "n2":
+        g, k = g_of(2, []), 1
+    elif kind == "k20":
+        g = g_of(20, [(i, j) for i in range(20) for j in range(i + 1, 20)])
+        k = int(kk)
+    elif kind == "star":
+        g = g_of(1000, [(0, j) for j in range(1, 1000)])
+        k = int(kk)
+    else:
+        g = g_of(300, [(i, i + 1) for i in range(299)])
+        k = int(kk)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        _, knn = gu.partial_bfs(g, k, seed=3)
+        ip, dst, dist = oracle.partial_bfs(g, k, seed=3)
+    assert np.array_equal(knn.indptr, ip) and np.array_equal(knn.dst, dst)
+    assert np.array_equal(knn.dist, dist)
