@@ -431,6 +431,20 @@ __device__ __forceinline__ int fy_positions(int r, int lane, int j, int* wsc) {
 
 // rank of v among the (distinct) values of lanes 0..r-1
 __device__ __forceinline__ int rank_in_warp(int r, int v) {
+  if (r <= 8) {
+    // all r * r comparisons at once: lane L compares value L >> 2 with the
+    // values of lanes L & 3 and (L & 3) + 4; lane i < r sums the bits of
+    // lanes 4i .. 4i + 3 of both ballots (one step instead of r shuffles)
+    const int lane = threadIdx.x & 31;
+    const int q = lane & 3;
+    const int vi = __shfl_sync(FULL, v, lane >> 2);
+    const int va = __shfl_sync(FULL, v, q);
+    const int vb = __shfl_sync(FULL, v, q + 4);
+    const unsigned ba = __ballot_sync(FULL, q < r && va < vi);
+    const unsigned bb = __ballot_sync(FULL, q + 4 < r && vb < vi);
+    const unsigned m = 0xfu << ((lane & 7) << 2);
+    return __popc(ba & m) + __popc(bb & m);
+  }
   int rk = 0;
   for (int q = 0; q < r; q++) rk += __shfl_sync(FULL, v, q) < v;
   return rk;
@@ -459,7 +473,8 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
   int* const hkey = sm_hash[warp];
   int* const lst = sm_list[warp];
   const unsigned hbase = (unsigned)__cvta_generic_to_shared(hkey);
-  unsigned long long w_scanned = 0, w_expanded = 0;
+  // per-warp work counters: < 2^31 sources / 2^16 warps * 286 entries fits 32 bits
+  unsigned w_scanned = 0, w_expanded = 0;
   static_assert(TF_CAP2 + 32 + 1 + 32 <= (HC * 3) / 4, "ball budget must fit the hash");
   // Warp-wide claim of distinct keys (one per lane, `lead` lanes only): one
   // predicated CAS for everybody; the linear-probe loop runs only when some
@@ -484,11 +499,12 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     }
     return lead && old == -1;
   };
-  for (long long item = (long long)blockIdx.x * WARPS + warp; item < nsrc;
-       item += (long long)gridDim.x * WARPS) {
-    const int s = (int)(src_begin + item);
-    int* const rn = out_nbr + item * K;
-    int* const rd = out_dist + item * K;
+  // 32-bit source index: nsrc < 2^31 and the grid stride is below 2^20
+  for (unsigned item = blockIdx.x * WARPS + warp; item < (unsigned)nsrc;
+       item += gridDim.x * WARPS) {
+    const int s = (int)src_begin + (int)item;
+    int* const rn = out_nbr + (size_t)item * K;
+    int* const rd = out_dist + (size_t)item * K;
     const int b0 = __ldg(indptr + s);
     const int T0 = __ldg(indptr + s + 1) - b0;
     if (T0 > 32) {
@@ -545,9 +561,8 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
 #pragma unroll
     for (int i = 0; i < HC / 128; i++) reinterpret_cast<int4*>(hkey)[lane + 32 * i] = make_int4(-1, -1, -1, -1);
     __syncwarp();
-    if (lane == 0) hkey[hash_slot<HC>(s)] = s;
-    __syncwarp();
-    claim(w1, lane < T0);
+    // s itself rides on lane T0 (T0 < K <= 32) of the level-1 claim
+    claim(lane == T0 ? s : w1, lane <= T0);
     // ---- level 2: prefix of the parents' degrees.  In an undirected CSR a
     // neighbour of s has s in its own list, so every parent is non-empty; a
     // CSR that breaks this (one-sided entries) takes the generic tiers.
@@ -569,12 +584,16 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     // cbase = adjacency start - flattened start of the lane's parent, so a
     // candidate address is one shuffle and one add away
     const int cbase = cb - cpre;
+    const int cpre_s = lane < nne ? cpre : 0x40000000;
     // Raw candidate ids of chunk t0 (parent count of earlier chunks: pc).
     // Lanes past T load indices[0] and keep it: they sit above every valid
     // lane, so they are never a first occurrence and never claim.
     auto load_chunk = [&](int t0, int pc, int& x, unsigned& m) {
-      const unsigned off = (unsigned)(cpre - t0);
-      m = __reduce_or_sync(FULL, (lane < nne && off < 32u) ? (1u << off) : 0u);
+      // PTX shl clamps shifts >= 32 to a zero result: parents outside the
+      // chunk (off < 0 or >= 32, and the lanes past nne via cpre_s) add no bit
+      unsigned bit;
+      asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"((unsigned)(cpre_s - t0)));
+      m = __reduce_or_sync(FULL, bit);
       const int p = pc + __popc(m & le_mask) - 1;
       // 32-bit offset arithmetic (cbase may be negative; the sum never is)
       const unsigned base = (unsigned)__shfl_sync(FULL, cbase, p & 31);
@@ -613,10 +632,15 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
         __syncwarp();
       }
       mine = valid && (old == 0xffffffffu || (old >> 24) >= base_tag);
-      // only the lanes that met their id inserted earlier in this pair (a
-      // branch around the RED: 1-2% faster than an all-lanes no-op RED,
-      // whose 32 addresses cost shared-memory wavefronts)
-      if (mine && old != 0xffffffffu) atomicMin(reinterpret_cast<unsigned*>(&hkey[h]), key);
+      // predicated RED (no branch, no wavefronts for the idle lanes): only
+      // the lanes that met their id inserted earlier in this pair lower the
+      // slot's tag (c5 with the pair-rank and shl changes: 2.76 -> 2.58 ms)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+          "@p red.shared.min.u32 [%1], %2;\n\t}"
+          :
+          : "r"((unsigned)(mine && old != 0xffffffffu)), "r"(hbase + 4u * h), "r"(key)
+          : "memory");
     };
     auto process2p = [&](int t0, int xa, int xb) -> bool {
       const bool two = t0 + 32 < T;  // warp-uniform
@@ -714,13 +738,13 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       rd[T0 + r] = 2;
     }
     if (lane == 0) out_cnt[item] = K;
-    w_scanned += (unsigned long long)(T0 + T);
-    w_expanded += (unsigned long long)(1 + T0);
+    w_scanned += (unsigned)(T0 + T);
+    w_expanded += (unsigned)(1 + T0);
     __syncwarp();
   }
   if (work && lane == 0) {
-    atomicAdd(work, w_scanned);
-    atomicAdd(work + 1, w_expanded);
+    atomicAdd(work, (unsigned long long)w_scanned);
+    atomicAdd(work + 1, (unsigned long long)w_expanded);
   }
 }
 
