@@ -429,6 +429,25 @@ __device__ __forceinline__ int fy_positions(int r, int lane, int j, int* wsc) {
   return prev ? vL : j;
 }
 
+// inclusive warp scan: the validity predicate of shfl.up replaces the
+// per-step lane test
+template <int O>
+__device__ __forceinline__ void scan_step(int& v) {
+  asm("{\n\t.reg .s32 t;\n\t.reg .pred p;\n\t"
+      "shfl.sync.up.b32 t|p, %0, %1, 0, -1;\n\t"
+      "@p add.s32 %0, %0, t;\n\t}"
+      : "+r"(v)
+      : "n"(O));
+}
+__device__ __forceinline__ int warp_incl_scan_p(int v) {
+  scan_step<1>(v);
+  scan_step<2>(v);
+  scan_step<4>(v);
+  scan_step<8>(v);
+  scan_step<16>(v);
+  return v;
+}
+
 // rank of v among the (distinct) values of lanes 0..r-1
 __device__ __forceinline__ int rank_in_warp(int r, int v) {
   if (r <= 8) {
@@ -566,16 +585,14 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     // ---- level 2: prefix of the parents' degrees.  In an undirected CSR a
     // neighbour of s has s in its own list, so every parent is non-empty; a
     // CSR that breaks this (one-sided entries) takes the generic tiers.
-    if (__any_sync(FULL, lane < T0 && pd <= 0)) {
-      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
-      continue;
-    }
+    // One vote for both exits: an empty parent, or (PACKED) a level too
+    // long for the 8-bit tags t + 1.
     const int nne = T0;
     const int cb = pb, cdv = pd;
-    const int inc = warp_incl_scan(cdv);
+    const int inc = warp_incl_scan_p(cdv);
     const int cpre = inc - cdv;
     const int T = __shfl_sync(FULL, inc, 31);
-    if (PACKED && T > 254) {  // tags t + 1 must fit in 8 bits
+    if (__any_sync(FULL, (lane < T0 && pd <= 0) || (PACKED && T > 254))) {
       if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
       continue;
     }
@@ -614,24 +631,27 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       // value was 20% slower: lanes past T all hold the same id, so their
       // CASes serialise on one slot); the probe loop runs only when some lane
       // hit another id's slot.
+      // Invalid lanes keep old = w (their own id with tag 0): neither a
+      // collision nor a first occurrence, with no test of `valid` below; the
+      // empty key's tag (255) is above every base tag.
       h = hash_slot<HC>(w);
-      unsigned old = key;
+      unsigned old = (unsigned)w;
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
           "@p atom.shared.cas.b32 %0, [%2], -1, %3;\n\t}"
           : "+r"(old)
           : "r"((unsigned)valid), "r"(hbase + 4u * h), "r"(key)
           : "memory");
-      bool coll = valid && old != 0xffffffffu && (old & 0xffffffu) != (unsigned)w;
+      bool coll = old != 0xffffffffu && ((old ^ (unsigned)w) << 8) != 0u;
       if (__any_sync(FULL, coll)) {
         while (coll) {
           h = (h + 1) & (HC - 1);
           old = (unsigned)atomicCAS(&hkey[h], -1, (int)key);
-          coll = old != 0xffffffffu && (old & 0xffffffu) != (unsigned)w;
+          coll = old != 0xffffffffu && ((old ^ (unsigned)w) << 8) != 0u;
         }
         __syncwarp();
       }
-      mine = valid && (old == 0xffffffffu || (old >> 24) >= base_tag);
+      mine = (old >> 24) >= base_tag;
       // predicated RED (no branch, no wavefronts for the idle lanes): only
       // the lanes that met their id inserted earlier in this pair lower the
       // slot's tag (c5 with the pair-rank and shl changes: 2.76 -> 2.58 ms)
@@ -730,7 +750,8 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     int pos = lane;
     if (nst > remaining && lane < remaining)
       pos = lane + umod64_tab(splitmix_at(fy_base, lane), nst - lane);
-    if (nst > remaining) pos = fy_positions(remaining, lane, pos, lst + TF_CAP2 + 32);
+    // one pick (remaining == 1): its draw is its position
+    if (nst > remaining && remaining > 1) pos = fy_positions(remaining, lane, pos, lst + TF_CAP2 + 32);
     const int v = lst[pos];
     const int r = rank_in_warp(remaining, v);
     if (lane < remaining) {
