@@ -57,6 +57,10 @@ int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_t* indices,
 /* synchronous: sources that fell from tier 0 (thread per source) to tier 1a,
  * to tier 1b and to tier 2 in the last call on this workspace (3 ints) */
 int gu_partial_bfs_overflow_counts(void* workspace, int64_t nsrc, int32_t* host_out3);
+/* synchronous: sources that left tier F (to 1a), tier 1a (to the hub tier H),
+ * tier H (to tier C / 1b) and tier C / 1b (to tier 2) in the last call on
+ * this workspace (4 ints) */
+int gu_partial_bfs_tier_counts(void* workspace, int64_t nsrc, int32_t* host_out4);
 
 /* ----------------------------------------------- C0 full BFS (bitset)
  * Replaces _kernels.py:33-57 apsp_rows via neighbors.py:120 all_pairs_bfs:

@@ -74,6 +74,7 @@ SIGNATURES = {
     "gu_partial_bfs_knn": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i32, _c_u64, _c_i64, _c_i64,
                                           _vp, _vp, _vp, _vp, _vp, _c_sz, _c_i32, _vp]),
     "gu_partial_bfs_overflow_counts": (ctypes.c_int, [_vp, _c_i64, _vp]),
+    "gu_partial_bfs_tier_counts": (ctypes.c_int, [_vp, _c_i64, _vp]),
     "gu_full_bfs_workspace_size": (_c_sz, [_c_i64, _c_i32, _c_i32]),
     "gu_apsp_rows": (ctypes.c_int, [_c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _vp, _c_sz,
                                     _c_i32, _vp]),

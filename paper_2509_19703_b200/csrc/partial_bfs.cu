@@ -397,6 +397,7 @@ __device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
 #ifndef TF_MINB
 #define TF_MINB 8
 #endif
+constexpr int TH_DMIN = 64;  // tier H: smallest degree of an implicit (hub) parent
 
 // Partial Fisher-Yates in closed form.  Lane i < r holds its draw j_i (>= i)
 // of the reference's sequential swaps swap(a[i], a[j_i]), i = 0..r-1
@@ -481,6 +482,7 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
               unsigned long long seed, long long src_begin, long long nsrc,
               int* __restrict__ out_nbr, int* __restrict__ out_dist, int* __restrict__ out_cnt,
               int* __restrict__ ovf_list, int* __restrict__ ovf_count,
+              int* __restrict__ hub_list, int* __restrict__ hub_count, int* __restrict__ hub_direct,
               unsigned long long* __restrict__ work) {
   constexpr int HC = TF_HC;
   __shared__ __align__(16) int sm_hash[WARPS][HC];
@@ -593,7 +595,18 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     const int cpre = inc - cdv;
     const int T = __shfl_sync(FULL, inc, 31);
     if (__any_sync(FULL, (lane < T0 && pd <= 0) || (PACKED && T > 254))) {
-      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+      // a long level next to a high-degree parent: straight to the hub tier
+      // (tier 1a would scan the hub's row only to overflow)
+      const bool hub = hub_list && !__any_sync(FULL, lane < T0 && pd <= 0) &&
+                       __reduce_max_sync(FULL, pd) >= TH_DMIN;
+      if (lane == 0) {
+        if (hub) {
+          hub_list[atomicAdd(hub_count, 1)] = s;
+          atomicAdd(hub_direct, 1);
+        } else {
+          ovf_list[atomicAdd(ovf_count, 1)] = s;
+        }
+      }
       continue;
     }
     int nst = 0, pcount = 0;
@@ -742,7 +755,17 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
     }
     const int remaining = K - T0;
     if (ovf || nst < remaining) {  // level 2 does not reach k (or too big): generic path
-      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+      // a ball above this tier's budget is above tier 1a's too: hand it to
+      // the hub tier (which passes what it cannot take on to the big-ball tiers)
+      const bool hub = ovf && hub_list;
+      if (lane == 0) {
+        if (hub) {
+          hub_list[atomicAdd(hub_count, 1)] = s;
+          atomicAdd(hub_direct, 1);
+        } else {
+          ovf_list[atomicAdd(ovf_count, 1)] = s;
+        }
+      }
       __syncwarp();
       continue;
     }
@@ -766,6 +789,312 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
   if (work && lane == 0) {
     atomicAdd(work, (unsigned long long)w_scanned);
     atomicAdd(work + 1, (unsigned long long)w_expanded);
+  }
+}
+
+// ------------------------------------------------------------- tier H (hub)
+// Sources next to ONE high-degree vertex (scale-free graphs): level 2 is
+// dominated by the hub's adjacency list N(H) (hundreds to thousands of ids),
+// which tiers 1a / C scan and hash in full for every such source.  Here the
+// hub's list is never scanned.  With H the largest-degree parent, level 2 in
+// discovery order is
+//   A    = first occurrences among the parents before H        (explicit)
+//   hubs = N(H) \ X in id order, X = ({s} + N(s) + A) within N(H)  (implicit)
+//   B    = first occurrences among the parents after H, outside N(H) (explicit)
+// because N(H) is sorted and duplicate-free, and a vertex of N(H) is new
+// unless an earlier part of the ball holds it.  Membership x in N(H) is tested
+// as H in N(x) (the graph is undirected; N(x) is short), the members' ranks in
+// N(H) by a 32-ary cooperative search; |hubs| = deg(H) - |X| >= 32 > k - T0,
+// so level 2 is always the crossing level, n2 = |A| + |hubs| + |B|, and the
+// Fisher-Yates picks (closed form, as tier F) index the three parts without
+// materialising the middle one: position q of `hubs` is N(H)[q + #(X-ranks
+// skipped)].  Work per source: O(explicit entries + |X| + k) instead of
+// O(deg(H)).  Sources with other shapes (no big parent, a second hub that
+// overflows the explicit list, > 32 members of X) go on to tier C / 1b.
+constexpr int TH_HC = 512, TH_LCAP = 160, TH_WARPS = 8, TH_XCAP = 32;
+#ifndef TH_MINB
+#define TH_MINB 6
+#endif
+struct TierH {
+  // hkey[HC] lst[LCAP + 32] cpre[32] cb[32] xs[32] wsc[32]
+  static constexpr int WORDS = TH_HC + TH_LCAP + 32 + 4 * 32;
+};
+static_assert(1 + 31 + TH_LCAP + 32 <= (TH_HC * 3) / 4, "explicit ball must fit the hash");
+
+// H in the sorted row indices[b, b + d)?  Long rows (another hub's) narrow
+// 8-fold per round trip: seven independent pivot loads per step.
+__device__ __forceinline__ bool row_has(const int* __restrict__ indices, int b, int d, int H) {
+  int lo = b, len = d;
+  while (len > 8) {
+    const int step = (len + 7) >> 3;
+    int c = 0;  // blocks [lo + i * step, +step) entirely below H form a prefix
+#pragma unroll
+    for (int i = 0; i < 7; i++) {
+      const int last = lo + (i + 1) * step - 1;
+      c += last < lo + len && __ldg(indices + last) < H;
+    }
+    lo += c * step;
+    len = min(step, len - c * step);
+  }
+  bool f = false;
+#pragma unroll
+  for (int q = 0; q < 8; q++) f |= q < len && __ldg(indices + lo + q) == H;
+  return f;
+}
+
+// ranks of up to 4 members x[0..m) in the sorted row nh[0, D): the warp
+// narrows every member's range 32-fold per step, the loads of the members of
+// a step in flight together (two round trips for D <= 1024)
+__device__ __forceinline__ void hub_rank4(const int* __restrict__ nh, int D, const int (&x)[4], int m,
+                                          int lane, int (&rank)[4]) {
+  int lo[4], hi[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    lo[i] = 0;
+    hi[i] = i < m ? D : 0;
+  }
+  for (int span = D; span > 32;) {  // every live range has this length bound
+    const int step = (span + 31) >> 5;
+    int v[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int bl = lo[i] + lane * step;
+      v[i] = bl < hi[i] ? __ldg(nh + min(bl + step, hi[i]) - 1) : INT_MAX;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int c = __popc(__ballot_sync(FULL, v[i] < x[i]));  // blocks entirely below x
+      lo[i] += c * step;
+      hi[i] = min(lo[i] + step, hi[i]);
+    }
+    span = step;
+  }
+  int v[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) v[i] = lo[i] + lane < hi[i] ? __ldg(nh + lo[i] + lane) : INT_MAX;
+#pragma unroll
+  for (int i = 0; i < 4; i++) rank[i] = lo[i] + __popc(__ballot_sync(FULL, v[i] < x[i]));
+}
+
+__global__ void __launch_bounds__(TH_WARPS * 32, TH_MINB)
+    pbfs_hub(const int* __restrict__ indptr, const int* __restrict__ indices, int K,
+             unsigned long long seed, long long src_begin, const int* __restrict__ list,
+             const int* __restrict__ list_count, int* __restrict__ out_nbr,
+             int* __restrict__ out_dist, int* __restrict__ out_cnt, int* __restrict__ ovf_list,
+             int* __restrict__ ovf_count, int* __restrict__ queue,
+             unsigned long long* __restrict__ work) {
+  constexpr int HC = TH_HC;
+  extern __shared__ __align__(16) int smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int* const hkey = smem + warp * TierH::WORDS;
+  int* const lst = hkey + HC;
+  int* const cpre_sh = lst + TH_LCAP + 32;
+  int* const cb_sh = cpre_sh + 32;
+  int* const xs = cb_sh + 32;
+  int* const wsc = xs + 32;
+  unsigned long long w_scanned = 0, w_expanded = 0;
+  const int total = *list_count;
+  // sources are handed out one at a time (per-source latency varies a lot and
+  // the list is only a few rounds of the resident warps long)
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(queue, 1);
+    it = __shfl_sync(FULL, it, 0);
+    if (it >= total) break;
+    const int s = __ldg(list + it);
+    const long long item = (long long)s - src_begin;
+    int* const rn = out_nbr + item * K;
+    int* const rd = out_dist + item * K;
+    const int b0 = __ldg(indptr + s);
+    const int T0 = __ldg(indptr + s + 1) - b0;
+    bool ok = T0 >= 1 && T0 < K && T0 <= 31;
+    int w1 = -1, pb = 0, pd = 0;
+    if (ok && lane < T0) {
+      w1 = __ldg(indices + b0 + lane);
+      pb = __ldg(indptr + w1);
+      pd = __ldg(indptr + w1 + 1) - pb;
+    }
+    // the hub: the largest-degree parent (lowest lane among equals)
+    const int D = __reduce_max_sync(FULL, pd);
+    const int hl = __ffs(__ballot_sync(FULL, lane < T0 && pd == D)) - 1;
+    if (__any_sync(FULL, lane < T0 && pd <= 0) || D < TH_DMIN) ok = false;
+    if (!ok) {
+      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+      continue;
+    }
+    const int H = __shfl_sync(FULL, w1, hl);
+    const int* const nh = indices + __shfl_sync(FULL, pb, hl);
+    // flattened adjacency of the explicit parents (the hub contributes nothing)
+    const int pde = lane == hl ? 0 : pd;
+    const int inc = warp_incl_scan(pde);
+    const int Ts = __shfl_sync(FULL, inc, 31);
+    const int Tsplit = __shfl_sync(FULL, inc - pde, hl);  // entries of the parents before H
+    __syncwarp();  // the previous source's reads of the tables are done
+    cpre_sh[lane] = lane < T0 ? inc - pde : INT_MAX;
+    cb_sh[lane] = pb;
+#pragma unroll
+    for (int i = 0; i < HC / 128; i++)
+      reinterpret_cast<int4*>(hkey)[lane + 32 * i] = make_int4(-1, -1, -1, -1);
+    __syncwarp();
+    if (lane <= T0) {  // s and level 1: distinct ids, tag 0
+      const int w = lane == T0 ? s : w1;
+      unsigned h = hash_slot<HC>(w);
+      while (atomicCAS(&hkey[h], -1, w) != -1) h = (h + 1) & (HC - 1);
+    }
+    __syncwarp();
+    int nl = 0;
+    // first occurrences of flattened entries [tbeg, tend) appended to lst in
+    // order (tier 1a's packed lane-tag claim); false: the list overflows
+    auto expand = [&](int tbeg, int tend) -> bool {
+      // candidate id of flattened entry t (parent by a search of the prefix table)
+      auto cand = [&](int t) -> int {
+        if (t >= tend) return 0;
+        int p = 0;
+#pragma unroll
+        for (int st = 16; st; st >>= 1)
+          if (cpre_sh[p + st] <= t) p += st;
+        return __ldg(indices + cb_sh[p] + (t - cpre_sh[p]));
+      };
+      int wn = tbeg < tend ? cand(tbeg + lane) : 0;
+      for (int t0 = tbeg; t0 < tend; t0 += 32) {
+        const bool valid = t0 + lane < tend;
+        const int w = wn;
+        if (t0 + 32 < tend) wn = cand(t0 + 32 + lane);  // next chunk's load in flight
+        const unsigned key = ((unsigned)(lane + 1) << 24) | (unsigned)w;
+        unsigned h = hash_slot<HC>(w);
+        unsigned old = valid ? (unsigned)atomicCAS(&hkey[h], -1, (int)key) : 0u;
+        bool coll = valid && old != 0xffffffffu && (old & 0xffffffu) != (unsigned)w;
+        if (__any_sync(FULL, coll)) {
+          while (coll) {
+            h = (h + 1) & (HC - 1);
+            old = (unsigned)atomicCAS(&hkey[h], -1, (int)key);
+            coll = old != 0xffffffffu && (old & 0xffffffu) != (unsigned)w;
+          }
+        }
+        const bool mine = valid && (old == 0xffffffffu || (old >> 24) != 0u);
+        if (mine && old != 0xffffffffu) atomicMin(reinterpret_cast<unsigned*>(&hkey[h]), key);
+        __syncwarp();
+        const bool isnew = mine && (unsigned)hkey[h] == key;
+        __syncwarp();
+        if (isnew) hkey[h] = w;
+        const unsigned bal = __ballot_sync(FULL, isnew);
+        if (isnew) lst[nl + __popc(bal & lt)] = w;
+        nl += __popc(bal);
+        if (nl > TH_LCAP) return false;
+        __syncwarp();
+      }
+      return true;
+    };
+    ok = expand(0, Tsplit);
+    const int nA = nl;
+    // ---- X: the members of N(H) among s, N(s) and A, as ascending ranks
+    int nx = 0;
+    if (ok) {
+      // s is a member (H is its neighbour); level 1 by the rows already located
+      const bool m1 = lane < T0 && lane != hl && row_has(indices, pb, pd, H);
+      const unsigned bm1 = __ballot_sync(FULL, m1);
+      if (lane == 0) xs[0] = s;
+      if (m1) xs[1 + __popc(bm1 & lt)] = w1;
+      nx = 1 + __popc(bm1);  // <= 32
+      for (int c0 = 0; c0 < nA && ok; c0 += 32) {
+        const int c = c0 + lane;
+        bool m = false;
+        int x = 0;
+        if (c < nA) {
+          x = lst[c];
+          const int bx = __ldg(indptr + x);
+          m = row_has(indices, bx, __ldg(indptr + x + 1) - bx, H);
+        }
+        const unsigned bm = __ballot_sync(FULL, m);
+        if (nx + __popc(bm) > TH_XCAP) {
+          ok = false;
+          break;
+        }
+        if (m) xs[nx + __popc(bm & lt)] = x;
+        nx += __popc(bm);
+      }
+    }
+    if (ok) {
+      __syncwarp();
+      int myrank = INT_MAX;
+      for (int i0 = 0; i0 < nx; i0 += 4) {
+        int xq[4], rq[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) xq[i] = xs[min(i0 + i, nx - 1)];
+        hub_rank4(nh, D, xq, min(4, nx - i0), lane, rq);
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if (lane == i0 + i) myrank = rq[i];
+      }
+      int posx = 0;  // ascending order of the (distinct) ranks
+      for (int i = 0; i < nx; i++) posx += __shfl_sync(FULL, myrank, i) < myrank;
+      __syncwarp();
+      if (lane < nx) xs[posx] = myrank;
+      // ---- B: candidates new to the explicit ball, then minus N(H)
+      ok = expand(Tsplit, Ts);
+    }
+    if (ok) {
+      int kept = nA;
+      for (int c0 = nA; c0 < nl; c0 += 32) {
+        const int c = c0 + lane;
+        bool keep = false;
+        int x = 0;
+        if (c < nl) {
+          x = lst[c];
+          const int bx = __ldg(indptr + x);
+          keep = !row_has(indices, bx, __ldg(indptr + x + 1) - bx, H);
+        }
+        const unsigned bk = __ballot_sync(FULL, keep);
+        __syncwarp();  // the chunk is read before it is overwritten
+        if (keep) lst[kept + __popc(bk & lt)] = x;
+        kept += __popc(bk);
+      }
+      nl = kept;
+      __syncwarp();
+    }
+    if (!ok) {
+      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = s;
+      continue;
+    }
+    // ---- crossing level 2: n2 ids, r picks
+    const int S = D - nx, n2 = nA + S + (nl - nA), r = K - T0;
+    const unsigned long long fy_base = seed + SPLIT_GAMMA * (unsigned long long)(s + 1);
+    int pos = lane;
+    if (lane < r) {
+      const unsigned long long z = splitmix_at(fy_base, lane);
+      pos = lane + (n2 - lane <= 4096 ? umod64_tab(z, n2 - lane) : umod64_small(z, n2 - lane));
+    }
+    if (r > 1) pos = fy_positions(r, lane, pos, wsc);  // one pick: its draw is its position
+    int v = 0;
+    if (lane < r) {
+      if (pos < nA) {
+        v = lst[pos];
+      } else if (pos < nA + S) {
+        int q = pos - nA;
+        for (int i = 0; i < nx && xs[i] <= q; i++) q++;
+        v = __ldg(nh + q);
+      } else {
+        v = lst[pos - S];
+      }
+    }
+    const int rk = rank_in_warp(r, v);
+    if (lane < T0) {
+      rn[lane] = w1;
+      rd[lane] = 1;
+    }
+    if (lane < r) {
+      rn[T0 + rk] = v;
+      rd[T0 + rk] = 2;
+    }
+    if (lane == 0) out_cnt[item] = K;
+    w_scanned += (unsigned long long)(T0 + Ts + D);
+    w_expanded += (unsigned long long)(1 + T0);
+    __syncwarp();
+  }
+  if (work && lane == 0) {
+    atomicAdd(work, w_scanned);
+    atomicAdd(work + 1, w_expanded);
   }
 }
 
@@ -1150,7 +1479,7 @@ struct PbfsWs {
   int* ovfA;
   int* ovfB;
   int* ovf0;
-  int* counts;  // [0]=ovfA count, [1]=ovfB count, [2]=ovf0 count
+  int* counts;  // [0]=ovfA count, [1]=ovfB count, [2]=ovf0 count, [3]=tier H rejects, [4]=F -> H directly, [5]=tier H work queue head
   unsigned long long* work;
   int* slots;
 };
@@ -1167,7 +1496,7 @@ size_t pbfs_ws_layout(long long n, long long nsrc, int slots, char* base, PbfsWs
   size_t oA = take(sizeof(int) * (size_t)(nsrc + 1));
   size_t oB = take(sizeof(int) * (size_t)(nsrc + 1));
   size_t o0 = take(sizeof(int) * (size_t)(nsrc + 1));
-  size_t oC = take(sizeof(int) * 4);
+  size_t oC = take(sizeof(int) * 8);
   size_t oW = take(sizeof(unsigned long long) * 2);
   size_t oS = take(sizeof(int) * 2 * (size_t)n * (size_t)slots);
   if (ws && base) {
@@ -1186,7 +1515,8 @@ constexpr int TF_WARPS = 8;
 cudaError_t launch_fast(int sms, long long n, const int* indptr, const int* indices, int k,
                         unsigned long long seed, long long src_begin, long long nsrc,
                         int* out_nbr, int* out_dist, int* out_count, int* ovf_out, int* ovf_cnt,
-                        unsigned long long* work, cudaStream_t st) {
+                        int* hub_out, int* hub_cnt, int* hub_direct, unsigned long long* work,
+                        cudaStream_t st) {
   // packed tags need ids below 2^24 - 1 (the empty key is all ones)
   auto kern = n < (1 << 24) - 1 ? pbfs_fast<TF_WARPS, true> : pbfs_fast<TF_WARPS, false>;
   int per_sm = 0;
@@ -1197,7 +1527,7 @@ cudaError_t launch_fast(int sms, long long n, const int* indptr, const int* indi
   if (blocks > cap) blocks = cap;
   kern<<<(unsigned)blocks, TF_WARPS * 32, 0, st>>>(indptr, indices, k, seed, src_begin, nsrc,
                                                    out_nbr, out_dist, out_count, ovf_out, ovf_cnt,
-                                                   work);
+                                                   hub_out, hub_cnt, hub_direct, work);
   return cudaGetLastError();
 }
 
@@ -1245,6 +1575,23 @@ cudaError_t launch_lean_big(int sms, long long n, const int* indptr, const int* 
   return launch_warp_tier<T1B_CAP, T1B_PCAP, T1B_TCAP, 2, 1>(
       sms, n, indptr, indices, k, seed, src_begin, nsrc, list, list_count, out_nbr, out_dist, out_count,
       ovf_out, ovf_cnt, work, st);
+}
+
+// tier H: hub-adjacent sources of the list, one warp each (ids below 2^24 - 1)
+cudaError_t launch_hub(int sms, const int* indptr, const int* indices, int k,
+                       unsigned long long seed, long long src_begin, const int* list,
+                       const int* list_count, int* out_nbr, int* out_dist, int* out_count,
+                       int* ovf_out, int* ovf_cnt, int* queue, unsigned long long* work,
+                       cudaStream_t st) {
+  constexpr size_t smem = sizeof(int) * TierH::WORDS * TH_WARPS;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pbfs_hub, TH_WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  const unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1);
+  pbfs_hub<<<blocks, TH_WARPS * 32, smem, st>>>(indptr, indices, k, seed, src_begin, list, list_count,
+                                                out_nbr, out_dist, out_count, ovf_out, ovf_cnt, queue,
+                                                work);
+  return cudaGetLastError();
 }
 
 // tier C: one 256-thread CTA per big-ball source (ids below 2^23 - 1)
@@ -1306,7 +1653,7 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
   }
   unsigned long long* work = (unsigned long long*)work_counters;
   if (work) GU_CHECK(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), st));
-  GU_CHECK(cudaMemsetAsync(ws.counts, 0, 4 * sizeof(int), st));
+  GU_CHECK(cudaMemsetAsync(ws.counts, 0, 8 * sizeof(int), st));
   if (k == 0) {
     GU_CHECK(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * nsrc, st));
     return GU_OK;
@@ -1317,24 +1664,41 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
     // -> tier 1b (CAP 1024) -> tier 2.  GU_PBFS_MODE=lean skips tier F
     // (comparison only; every path is exact).
     static const char* env_mode = getenv("GU_PBFS_MODE");
+    // tier H (hub-adjacent sources) needs ids below 2^24 - 1; GU_PBFS_HUB=0
+    // skips it (comparison only)
+    static const char* env_hub = getenv("GU_PBFS_HUB");
+    const bool use_hub = n < (1 << 24) - 1 && !(env_hub && !strcmp(env_hub, "0"));
     if (!env_mode || strcmp(env_mode, "lean")) {
       GU_CHECK(launch_fast(sms, n, indptr, indices, k, seed, src_begin, nsrc, out_nbr, out_dist,
-                           out_count, ws.ovf0, ws.counts + 2, work, st));
+                           out_count, ws.ovf0, ws.counts + 2, use_hub ? ws.ovfA : nullptr,
+                           ws.counts + 0, ws.counts + 4, work, st));
       GU_CHECK(launch_lean(sms, n, indptr, indices, k, seed, src_begin, nsrc, ws.ovf0, ws.counts + 2,
                            out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
     } else {
       GU_CHECK(launch_lean(sms, n, indptr, indices, k, seed, src_begin, nsrc, nullptr, nullptr,
                            out_nbr, out_dist, out_count, ws.ovfA, ws.counts + 0, work, st));
     }
+    // hub-adjacent sources (tier H): tier 1a's overflow and tier F's direct
+    // hand-offs; what it cannot take goes on to the big-ball tiers.  Its
+    // reject list borrows ovf0 (tier 1a has consumed it) and counts[3].
+    const int* big_list = ws.ovfA;
+    const int* big_count = ws.counts + 0;
+    if (use_hub) {
+      GU_CHECK(launch_hub(sms, indptr, indices, k, seed, src_begin, ws.ovfA, ws.counts + 0, out_nbr,
+                          out_dist, out_count, ws.ovf0, ws.counts + 3, ws.counts + 5, work, st));
+      big_list = ws.ovf0;
+      big_count = ws.counts + 3;
+    } else {
+      GU_CHECK(cudaMemcpyAsync(ws.counts + 3, ws.counts + 0, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    }
     // big balls: the CTA tier when ids fit its 23-bit packed keys
     static const char* env_big = getenv("GU_PBFS_BIG");
     if (n < (1 << 23) - 1 && !(env_big && !strcmp(env_big, "warp"))) {
-      GU_CHECK(launch_cta(sms, indptr, indices, k, seed, src_begin, ws.ovfA, ws.counts + 0,
-                          out_nbr, out_dist, out_count, ws.ovfB, ws.counts + 1, work, st));
+      GU_CHECK(launch_cta(sms, indptr, indices, k, seed, src_begin, big_list, big_count, out_nbr,
+                          out_dist, out_count, ws.ovfB, ws.counts + 1, work, st));
     } else {
-      GU_CHECK(launch_lean_big(sms, n, indptr, indices, k, seed, src_begin, nsrc, ws.ovfA,
-                               ws.counts + 0, out_nbr, out_dist, out_count, ws.ovfB, ws.counts + 1,
-                               work, st));
+      GU_CHECK(launch_lean_big(sms, n, indptr, indices, k, seed, src_begin, nsrc, big_list, big_count,
+                               out_nbr, out_dist, out_count, ws.ovfB, ws.counts + 1, work, st));
     }
   } else {
     // k > group size: every source goes straight to the exact tier-2 path
@@ -1355,13 +1719,25 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
   return GU_OK;
 }
 
+extern "C" int gu_partial_bfs_tier_counts(void* workspace, int64_t nsrc, int32_t* host_out4) {
+  PbfsWs ws;
+  pbfs_ws_layout(1, nsrc, 1, (char*)workspace, &ws);
+  int c[5];
+  GU_CHECK(cudaMemcpy(c, ws.counts, 5 * sizeof(int), cudaMemcpyDeviceToHost));
+  host_out4[0] = c[2] + c[4];  // left tier F (to tier 1a, or straight to tier H)
+  host_out4[1] = c[0];         // entered tier H (from tier 1a or tier F)
+  host_out4[2] = c[3];         // entered tier C / 1b
+  host_out4[3] = c[1];         // entered tier 2
+  return GU_OK;
+}
+
 extern "C" int gu_partial_bfs_overflow_counts(void* workspace, int64_t nsrc, int32_t* host_out3) {
   PbfsWs ws;
   pbfs_ws_layout(1, nsrc, 1, (char*)workspace, &ws);
-  int c[3];
-  GU_CHECK(cudaMemcpy(c, ws.counts, 3 * sizeof(int), cudaMemcpyDeviceToHost));
-  host_out3[0] = c[2];  // fell from tier 0 to tier 1a
-  host_out3[1] = c[0];  // fell to tier 1b
-  host_out3[2] = c[1];  // fell to tier 2
+  int c[5];
+  GU_CHECK(cudaMemcpy(c, ws.counts, 5 * sizeof(int), cudaMemcpyDeviceToHost));
+  host_out3[0] = c[2] + c[4];  // left tier F
+  host_out3[1] = c[3];         // reached the big-ball tier (C / 1b)
+  host_out3[2] = c[1];         // reached tier 2
   return GU_OK;
 }

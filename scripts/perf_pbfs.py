@@ -45,8 +45,8 @@ for name in names:
               g.n, _lib.ptr(nb), _lib.ptr(dd), _lib.ptr(cc), None, _lib.ptr(ws), ws.numel(), tw,
               stream_ptr())
     torch.cuda.synchronize()
-    oc = (ctypes.c_int32 * 3)()
-    lib.gu_partial_bfs_overflow_counts(ctypes.c_void_p(ws.data_ptr()), g.n, oc)
+    oc = (ctypes.c_int32 * 4)()
+    lib.gu_partial_bfs_tier_counts(ctypes.c_void_p(ws.data_ptr()), g.n, oc)
     ovf = list(oc)
     alg = 8 * ex + 4 * sc + 8 * 15 * g.n
     # sample check vs oracle
@@ -55,4 +55,4 @@ for name in names:
     ok = np.array_equal(nbr[s0:s0 + 5000].cpu().numpy().reshape(-1), on)
     print(f"{name}: n={g.n} m={g.m} gen={gen:.1f}s  {ms:.3f} ms  GTEPS={sc/ms/1e6:.1f}  "
           f"alg={alg/1e9:.3f} GB -> {alg/ms/1e6:.0f} GB/s  sample_ok={ok}  scanned/src={sc/g.n:.1f} "
-          f"expanded/src={ex/g.n:.2f} overflow(t0->1a,1b,2)={ovf}", flush=True)
+          f"expanded/src={ex/g.n:.2f} left tier (F,1a,H,C)={ovf}", flush=True)

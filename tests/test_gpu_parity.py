@@ -757,3 +757,51 @@ def test_partial_bfs_edge_shapes(gu, oracle, case):
         ip, dst, dist = oracle.partial_bfs(g, k, seed=3)
     assert np.array_equal(knn.indptr, ip) and np.array_equal(knn.dst, dst)
     assert np.array_equal(knn.dist, dist)
+
+
+@pytest.mark.parametrize("k", [2, 5, 15, 31])
+@pytest.mark.parametrize("hub_pos", ["low", "mid", "high"])
+def test_partial_bfs_hub_tier(gu, oracle, k, hub_pos):
+    """Tier H (csrc/partial_bfs.cu): sources next to one high-degree vertex,
+    whose row is handled implicitly.  Hubs with low / middle / high ids (the
+    hub before, between and after the other parents in queue order), hubs
+    adjacent to each other (members of N(H) among N(s)), leaves shared by two
+    hubs (explicit second hub), and a sparse background -- every row against
+    the oracle, and the tier is checked to have run."""
+    import ctypes
+    from paper_2509_19703_b200 import _lib
+    from paper_2509_19703_b200.device import device_csr, workspace
+    from paper_2509_19703_b200.fixtures import canonical_edges, graph_from_edges
+    from paper_2509_19703_b200.neighbors import _tier2_warps, partial_bfs_records
+
+    rng = np.random.default_rng(100 + k)
+    n = 6000
+    hubs = {"low": np.arange(4), "mid": np.arange(3000, 3004),
+            "high": np.arange(n - 4, n)}[hub_pos]
+    pairs = []
+    others = np.setdiff1d(np.arange(n), hubs)
+    # a sparse background (ring + random chords)
+    pairs += [(int(others[i]), int(others[(i + 1) % len(others)])) for i in range(len(others))]
+    pairs += [tuple(int(x) for x in rng.choice(others, 2, replace=False)) for _ in range(4000)]
+    # hubs of degree ~700, ~400, ~150, ~80; the first two share 60 leaves
+    for h, d in zip(hubs, (700, 400, 150, 80)):
+        pairs += [(int(h), int(x)) for x in rng.choice(others, d, replace=False)]
+    shared = rng.choice(others, 60, replace=False)
+    pairs += [(int(hubs[0]), int(x)) for x in shared] + [(int(hubs[1]), int(x)) for x in shared]
+    pairs += [(int(hubs[0]), int(hubs[1])), (int(hubs[1]), int(hubs[2]))]
+    g = graph_from_edges(n, canonical_edges(n, np.asarray(pairs, np.int64)))
+    csr = device_csr(g)
+    t2 = _tier2_warps(g.n)
+    lib = _lib.load()
+    ws = workspace(lib.gu_partial_bfs_workspace_size(g.n, g.n, t2), csr.device)
+    nbr, dist, cnt = partial_bfs_records(csr, k, 9, 0, g.n, tier2_warps=t2, ws=ws)
+    tiers = (ctypes.c_int32 * 4)()
+    assert lib.gu_partial_bfs_tier_counts(ctypes.c_void_p(ws.data_ptr()), g.n, tiers) == 0
+    o_n, o_d, o_c = oracle.partial_bfs_raw(g, k, 9, nthreads=4)
+    assert np.array_equal(cnt.cpu().numpy(), o_c)
+    assert np.array_equal(nbr.cpu().numpy().reshape(-1), o_n)
+    assert np.array_equal(dist.cpu().numpy().reshape(-1), o_d)
+    entered_h, entered_big = int(tiers[1]), int(tiers[2])
+    print(f"k={k} hubs {hub_pos}: left F {tiers[0]}, entered H {entered_h}, big-ball tier {entered_big}")
+    if k >= 5:  # (k = 2: only degree-1 sources stop at level 2, the tier has nothing to do)
+        assert entered_h > 0 and entered_big < entered_h  # tier H ran and finished sources
