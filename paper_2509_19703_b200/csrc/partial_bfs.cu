@@ -811,7 +811,13 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
 // skipped)].  Work per source: O(explicit entries + |X| + k) instead of
 // O(deg(H)).  Sources with other shapes (no big parent, a second hub that
 // overflows the explicit list, > 32 members of X) go on to tier C / 1b.
-constexpr int TH_HC = 512, TH_LCAP = 160, TH_WARPS = 8, TH_XCAP = 32;
+#ifndef TH_HC
+#define TH_HC 512
+#endif
+#ifndef TH_LCAP
+#define TH_LCAP 160
+#endif
+constexpr int TH_WARPS = 8, TH_XCAP = 32;
 #ifndef TH_MINB
 #define TH_MINB 6
 #endif

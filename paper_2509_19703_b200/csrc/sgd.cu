@@ -46,6 +46,12 @@ constexpr unsigned FULL = 0xffffffffu;
 // coordinate gathers cached in L2 only (the 32 MB array never fits L1):
 // c5 epoch 2.352 -> 2.33 ms, c4 0.600 -> 0.590 ms (profiles/r02_ab_sgd_ldcg.log)
 #define SGD_LD(p) __ldcg(p)
+#ifndef SGD_POOL
+#define SGD_POOL 1  // warp-pooled first-try negatives on GPU-filling epochs
+#endif
+#ifndef SGD_LOCKSTEP
+#define SGD_LOCKSTEP 1  // a block of negatives reads one x_u (see the epoch kernel)
+#endif
 #ifndef SGD_MIN_BLOCKS
 #define SGD_MIN_BLOCKS 4  // <= 64 registers: 32 warps per SM
 #endif  // negatives handled in lockstep per block
@@ -314,6 +320,7 @@ __global__ void __launch_bounds__(256, MINB)
                      unsigned long long seed, int* __restrict__ diverged,
                      long long ibase = 0, long long* __restrict__ acc = nullptr) {
   constexpr int lanes = LANES;
+  constexpr bool POOL = SGD_POOL && LANES == 32 && (MODE == REC_BLOOM || MODE == REC_RANGE);
   // (candidate, row begin, row end, owner lane * 8 + slot) of the warp's
   // filter hits, and each lane's bitmask of slots found to be neighbours
   __shared__ int4 sh_pairs[SGD_WARPS][32 * SGD_NEG_BLOCK];
@@ -366,6 +373,20 @@ __global__ void __launch_bounds__(256, MINB)
       if (p >= E) act = false;  // partial last tile maps onto itself
     }
     if (!act) p = 0;
+    // GPU-filling epochs are bound by L2 tag lookups (12.7 requests per visit,
+    // 73% of the L2 peak: profiles/r02_ncu_sgd_l2.txt), five of them the
+    // random first-try negatives.  POOL: each lane draws ONE uniform vertex per
+    // warp step and gathers its coordinates; the 32 visits of the step take
+    // their first tries from these 32 (each still uniform on [0, n), only
+    // correlated across the visits of one step, which never write them).
+    int pool_c = 0;
+    float2 pool_xy = make_float2(0.f, 0.f);
+    if (POOL) {
+      const unsigned pd = fmix32(fmix32((unsigned)i ^ (unsigned)rkey) + (unsigned)(rkey >> 32) +
+                                 (unsigned)((unsigned long long)i >> 32));
+      pool_c = (int)__umulhi(pd, (unsigned)n);
+      pool_xy = SGD_LD(&xy[pool_c]);
+    }
     // streamed once per epoch: evict-first, keep L2 for x / filter / rows
     using F = typename std::conditional<MODE == REC_BLOOM, Filt128, Filt64>::type;
     const int4 rec = act ? __ldcs(edges + ((MODE == REC_TABLE || MODE == REC_HASH) ? 1 : 2) * p) : make_int4(0, 0, 0, 0);
@@ -433,19 +454,38 @@ __global__ void __launch_bounds__(256, MINB)
       const int nq = min(SGD_NEG_BLOCK, n_neg - q0);
       int cand[SGD_NEG_BLOCK];
       unsigned draw_q[SGD_NEG_BLOCK];
-      unsigned mm = 0;  // slots whose filter bit is set
-#pragma unroll
-      for (int q = 0; q < SGD_NEG_BLOCK; q++) {
-        draw_q[q] = draw32(vbase, q0 + q, 0);
-        cand[q] = (int)__umulhi(draw_q[q], (unsigned)n);
-        if (MODE != REC_HASH && act && q < nq && cand[q] >= rlo && cand[q] <= rhi &&
-            filt_maybe<F>(fw, cand[q]))
-          mm |= 1u << q;
-      }
       float2 xc[SGD_NEG_BLOCK];
+      unsigned mm = 0;  // slots whose filter bit is set
+      if (POOL) {
+        // first tries from the warp's pool: slot q reads the vertex and the
+        // coordinates of lane (start + (q0 + q) * stride) & 31, stride odd
+        // (distinct lanes for up to 32 slots), start / stride from the visit's
+        // own draw
+        const unsigned d0 = draw32(vbase, 0, 0);
+        const unsigned stride = ((d0 >> 5) & 15u) * 2u + 1u;
 #pragma unroll
-      for (int q = 0; q < SGD_NEG_BLOCK; q++)
-        xc[q] = (act && q < nq) ? SGD_LD(&xy[cand[q]]) : make_float2(0.f, 0.f);
+        for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+          const int ln = (int)((d0 + (unsigned)(q0 + q) * stride) & 31u);
+          cand[q] = __shfl_sync(FULL, pool_c, ln);
+          xc[q].x = __shfl_sync(FULL, pool_xy.x, ln);
+          xc[q].y = __shfl_sync(FULL, pool_xy.y, ln);
+          draw_q[q] = 0;  // (the slow path redraws)
+          if (act && q < nq && cand[q] >= rlo && cand[q] <= rhi && filt_maybe<F>(fw, cand[q]))
+            mm |= 1u << q;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+          draw_q[q] = draw32(vbase, q0 + q, 0);
+          cand[q] = (int)__umulhi(draw_q[q], (unsigned)n);
+          if (MODE != REC_HASH && act && q < nq && cand[q] >= rlo && cand[q] <= rhi &&
+              filt_maybe<F>(fw, cand[q]))
+            mm |= 1u << q;
+        }
+#pragma unroll
+        for (int q = 0; q < SGD_NEG_BLOCK; q++)
+          xc[q] = (act && q < nq) ? SGD_LD(&xy[cand[q]]) : make_float2(0.f, 0.f);
+      }
       unsigned hset_hit = 0;
       if (MODE == REC_HASH && act) {
         // exact set test: all first probes in flight together, then the
@@ -521,12 +561,44 @@ __global__ void __launch_bounds__(256, MINB)
       }
       if (MODE == REC_HASH) hit = hset_hit;
       if (!act) continue;
+#if SGD_LOCKSTEP
+      // the block's repulsions all read x_u as it stands after the attraction
+      // and the earlier blocks (branch-free: the five gradient chains
+      // interleave); a rejected first try or a coincident point takes the
+      // sequential path below
+      unsigned redo = 0;
+      {
+        float sx = 0.f, sy = 0.f;
+#pragma unroll
+        for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+          const bool ok = q < nq && cand[q] != u && !((hit >> q) & 1u);
+          const float dx = xu.x - xc[q].x, dy = xu.y - xc[q].y;
+          const float d2 = dx * dx + dy * dy;
+          const float g = __fdividef(2.0f * b, (0.001f + d2) * (a * __powf(d2, b) + 1.0f));
+          const bool good = ok && d2 > 0.f;
+          sx += good ? clip4(g * dx) : 0.f;
+          sy += good ? clip4(g * dy) : 0.f;
+          if (q < nq && !good) redo |= 1u << q;
+        }
+        sx *= lr;
+        sy *= lr;
+        dux += sx;
+        duy += sy;
+        xu.x += sx;
+        xu.y += sy;
+      }
+      if (redo == 0) continue;
+#else
+      const unsigned redo = 0xffffffffu;
+#endif
 #pragma unroll
       for (int q = 0; q < SGD_NEG_BLOCK; q++) {
         if (q >= nq) break;
+        if (!((redo >> q) & 1u)) continue;
         const bool ok = cand[q] != u && !((hit >> q) & 1u);
         int c = ok ? cand[q] : -1;
-        unsigned draw = draw_q[q];  // the accepted try's draw (angle source)
+        // the accepted try's draw (angle source)
+        unsigned draw = POOL ? draw32(vbase, q0 + q, 0) : draw_q[q];
         if (!ok) {
           // retries 2..8 of this slot (rare)
           for (int t = 1; t < 8; t++) {
