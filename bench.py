@@ -319,9 +319,9 @@ def run_ours(args):
                                 "source at 81% of peak issue, LSU wavefronts at 82% of peak (hash "
                                 "CAS / atomicMin / clears), DRAM at 23% of peak "
                                 "(profiles/r02_ncu_pbfs_fast_final.txt, DESIGN.md K3)"},
-        # per step: tier F, tiers 1a / 1b, slot clear, tier 2 -- once, or once
+        # per step: tiers F, 1a, H, C (or 1b), slot clear, tier 2 -- once, or once
         # per exchange round at N > 1 (NCCL and dtype-cast kernels not counted)
-        "gpu_launches": 5 * args.steps * (4 if ws > 1 else 1),
+        "gpu_launches": 6 * args.steps * (4 if ws > 1 else 1),
         "clocks": clk.summary(),
         "fixture_gen_s": round(gen_s, 2),
     }
@@ -489,10 +489,12 @@ def _sgd_bench(gu, g, args, dev, peak):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": _profile_traffic("sgd_epoch_kernel"),
                          "alg_bytes_per_update": 88,
-                         "limiter": "per-visit latency: 48% occupancy (64 registers), 39% issue "
-                                    "active; stalls long-scoreboard 47%, short-scoreboard 24%; "
-                                    "DRAM at 8% of peak, the 32 MB coordinates L2-resident "
-                                    "(profiles/r02_ncu_sgd_range_current.txt, DESIGN.md K7)"},
+                         "limiter": "per-visit latency after the warp-pooled negatives took L2 "
+                                    "tag lookups from 73% to 50% of peak (612M -> 403M L2 requests "
+                                    "per epoch): 46% occupancy (64 registers), 42% issue active, "
+                                    "long-scoreboard stalls; DRAM at 8% of peak, the 32 MB "
+                                    "coordinates L2-resident (profiles/r02_ncu_sgd_l2.txt, "
+                                    "DESIGN.md K7)"},
             "diverged": int(div.item()) != INT32_MAX}
 
 

@@ -128,6 +128,15 @@ int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* 
                   const double* w, int32_t* sym_src, int32_t* sym_dst, double* sym_w,
                   int64_t* nbr_indptr, int64_t* host_E, void* workspace,
                   size_t ws_bytes, void* stream);
+/* The same call for weights that gu_smooth_knn just produced: smooth_workspace
+ * is that call's workspace (same n, untouched since).  The backward side of
+ * the union then reads each weight from the memoised per-profile table in it
+ * instead of gathering w[] in destination order -- identical output.  A null
+ * or short smooth_workspace makes it gu_symmetrize. */
+int gu_symmetrize_memo(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* dst,
+                       const double* w, int32_t* sym_src, int32_t* sym_dst, double* sym_w,
+                       int64_t* nbr_indptr, int64_t* host_E, void* workspace, size_t ws_bytes,
+                       const void* smooth_workspace, size_t smooth_ws_bytes, void* stream);
 
 /* ---------------------------------------------------- C2 SGD (Hogwild fp32)
  * The layout epochs of layout.py:314-360 / sgd_sweep (_kernels.py:158-223)

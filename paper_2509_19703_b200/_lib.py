@@ -92,6 +92,8 @@ SIGNATURES = {
     "gu_symmetrize_workspace_size": (_c_sz, [_c_i64, _c_i64]),
     "gu_symmetrize": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      ctypes.POINTER(_c_i64), _vp, _c_sz, _vp]),
+    "gu_symmetrize_memo": (ctypes.c_int, [_c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                          ctypes.POINTER(_c_i64), _vp, _c_sz, _vp, _c_sz, _vp]),
     "gu_sgd_record_bytes_for": (_c_i32, [_c_i64]),
     "gu_sgd_prepare_edges": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_u64,
                                             _vp, _vp, _vp]),

@@ -237,4 +237,27 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// ---- memoised-sigma profile table of K5 (smooth.cu), read back by K6
+// (symmetrize.cu).  Lives in the caller's gu_smooth_knn workspace, followed
+// (256-byte aligned) by one int slot per row (-1: the row was solved directly).
+constexpr int SIG_TABLE = 8192;
+constexpr unsigned long long SIG_EMPTY = 0ull;
+struct SigTable {
+  unsigned long long key[SIG_TABLE];
+  long long rep[SIG_TABLE];
+  double val[SIG_TABLE];
+  double rho[SIG_TABLE];
+  double w[SIG_TABLE][4];    // weight of each run
+  unsigned ends[SIG_TABLE];  // cumulative run ends, 8 bits each (255 past the last run)
+};
+constexpr size_t SIG_TABLE_BYTES = (sizeof(SigTable) + 255) & ~(size_t)255;
+
+// weight of entry `i` (position inside its row) of a row with profile `slot`:
+// the precomputed weight of the run that holds position i
+__device__ __forceinline__ double memo_weight(const SigTable* __restrict__ tab, int slot, unsigned i) {
+  const unsigned ends = tab->ends[slot];
+  const int j = (i >= (ends & 255u)) + (i >= ((ends >> 8) & 255u)) + (i >= ((ends >> 16) & 255u));
+  return tab->w[slot][j];
+}
+
 }  // namespace gu

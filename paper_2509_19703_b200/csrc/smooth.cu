@@ -128,19 +128,8 @@ __device__ double row_sigma(const int* d, int c, int kmax, double target, double
 // table entry on a representative row, and every row reads it back.  Rows
 // that do not fit a key, or find the table full, are solved directly.  The
 // result is the same float64 computation on the same operands: bit-identical.
-constexpr int SIG_TABLE = 8192;
-constexpr unsigned long long SIG_EMPTY = 0ull;
-// the profile table lives in the caller's workspace (per call: concurrent
-// calls on different streams never share it)
-struct SigTable {
-  unsigned long long key[SIG_TABLE];
-  long long rep[SIG_TABLE];
-  double val[SIG_TABLE];
-  double rho[SIG_TABLE];
-  double w[SIG_TABLE][4];    // weight of each run
-  unsigned ends[SIG_TABLE];  // cumulative run ends, 8 bits each
-};
-
+// (SigTable and its constants live in common.cuh: symmetrize.cu reads the
+// per-run weights back through memo_weight)
 __device__ __forceinline__ unsigned long long sig_mix(unsigned long long x) {
   x ^= x >> 33;
   x *= 0xff51afd7ed558ccdULL;
@@ -288,10 +277,7 @@ __global__ void __launch_bounds__(128)
       if (e < e1) {
         double w;
         if (r_slot >= 0) {  // profiled row: its run's precomputed weight
-          const unsigned ends = tab->ends[r_slot];
-          const unsigned i = (unsigned)(e - r_lo);
-          const int j = (i >= (ends & 255u)) + (i >= ((ends >> 8) & 255u)) + (i >= ((ends >> 16) & 255u));
-          w = tab->w[r_slot][j];
+          w = memo_weight(tab, r_slot, (unsigned)(e - r_lo));
         } else {
           w = exp(-((double)dist[e] - r_rho) / r_sig);
         }
@@ -312,7 +298,7 @@ constexpr long long SMOOTH_MEMO_MIN_ROWS = 4096;
 
 extern "C" size_t gu_smooth_knn_workspace_size(int64_t n) {
   if (n < SMOOTH_MEMO_MIN_ROWS) return 0;
-  return ((sizeof(SigTable) + 255) & ~(size_t)255) + sizeof(int) * (size_t)n;
+  return SIG_TABLE_BYTES + sizeof(int) * (size_t)n;
 }
 
 extern "C" int gu_smooth_knn(int64_t n, const int64_t* indptr, const int32_t* dist, int32_t kmax,
@@ -332,7 +318,7 @@ extern "C" int gu_smooth_knn(int64_t n, const int64_t* indptr, const int32_t* di
     return GU_ERR_WORKSPACE;
   }
   SigTable* tab = need ? (SigTable*)workspace : nullptr;
-  int* slots = need ? (int*)((char*)workspace + ((sizeof(SigTable) + 255) & ~(size_t)255))
+  int* slots = need ? (int*)((char*)workspace + SIG_TABLE_BYTES)
                     : nullptr;
   if (slots) {
     sig_clear<<<8, 256, 0, st>>>(tab);

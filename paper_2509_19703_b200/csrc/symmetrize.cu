@@ -90,6 +90,28 @@ struct RowOf {
   }
 };
 
+// Weight of directed entry e, for the BACKWARD side of the merge.  Gathering
+// w[e] for 60M in-edges in destination order is 60M random 8-byte reads of a
+// 480 MB array (c5: 7.5 GB of DRAM sectors, the bulk of fx_merge16's time).
+// When K5 memoised the rows' sigma (gu_symmetrize_memo), the weight is read
+// from its profile table instead: the source row's slot (4 bytes, an array
+// that stays in L2) and the run that holds e's position -- the very double
+// smooth_kernel stored in w[e].  Rows without a profile gather w[e].
+struct WOf {
+  const double* w;
+  const int* slot;      // null: always gather
+  const SigTable* tab;
+  RowOf row_of;
+  __device__ __forceinline__ double operator()(int e) const {
+    if (slot) {
+      const int src = row_of(e);
+      const int sl = __ldg(slot + src);
+      if (sl >= 0) return memo_weight(tab, sl, (unsigned)(e - src * row_of.k));
+    }
+    return w[e];
+  }
+};
+
 // one warp per vertex u: forward entries u*k .. u*k+k-1 (sorted by (id, i)
 // in registers) merged with the backward entries in_e[in_ptr[u] ..) whose
 // source rows are ascending; equal ids: forward first, each side in original
@@ -100,7 +122,7 @@ struct RowOf {
 // key's first forward weight a and first backward weight b (0 when absent)
 // and the flag h != 0; every other entry of the key gets flag 0.
 __global__ void fx_merge(long long n, int kfix, RowOf row_of, long long nnz, const int* __restrict__ dst,
-                         const double* __restrict__ w, const long long* __restrict__ in_ptr,
+                         const double* __restrict__ w, WOf wof, const long long* __restrict__ in_ptr,
                          const int* __restrict__ in_e, int* __restrict__ other,
                          double* __restrict__ hval, int* __restrict__ rowcnt) {
   const int lane = threadIdx.x & 31;
@@ -155,7 +177,7 @@ __global__ void fx_merge(long long n, int kfix, RowOf row_of, long long nnz, con
         double b = 0.0;
         if (lo < m) {
           const int e = m <= 32 ? e_lo : in_e[ib + lo];
-          if (row_of(e) == fid) b = w[e];  // first backward entry of this id
+          if (row_of(e) == fid) b = wof(e);  // first backward entry of this id
         }
         h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
         kept += h != 0.0;
@@ -191,7 +213,7 @@ __global__ void fx_merge(long long n, int kfix, RowOf row_of, long long nnz, con
         other[o] = bid;
         double h = 0.0;
         if (!in_fwd && prev != bid) {  // key with no forward entry: its first backward one
-          const double a = 0.0, b = w[e];
+          const double a = 0.0, b = wof(e);
           h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
           kept += h != 0.0;
         }
@@ -209,7 +231,7 @@ __global__ void fx_merge(long long n, int kfix, RowOf row_of, long long nnz, con
 // registers (longer ones searched in memory), backward entries 16 at a time
 // (the warp loops to the longer of its two in-rows).  Bit-identical output.
 __global__ void fx_merge16(long long n, int kfix, RowOf row_of, long long nnz,
-                           const int* __restrict__ dst, const double* __restrict__ w,
+                           const int* __restrict__ dst, const double* __restrict__ w, WOf wof,
                            const long long* __restrict__ in_ptr, const int* __restrict__ in_e,
                            int* __restrict__ other, double* __restrict__ hval,
                            int* __restrict__ rowcnt) {
@@ -265,7 +287,7 @@ __global__ void fx_merge16(long long n, int kfix, RowOf row_of, long long nnz,
         double b = 0.0;
         if (lo < m) {
           const int e = m <= 16 ? e_lo : in_e[ib + lo];
-          if (row_of(e) == fid) b = w[e];
+          if (row_of(e) == fid) b = wof(e);
         }
         h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
         kept += h != 0.0;
@@ -299,7 +321,7 @@ __global__ void fx_merge16(long long n, int kfix, RowOf row_of, long long nnz,
         other[o] = bid;
         double h = 0.0;
         if (!in_fwd && prev != bid) {
-          const double a = 0.0, b = w[e];
+          const double a = 0.0, b = wof(e);
           h = __dsub_rn(__dadd_rn(a, b), __dmul_rn(a, b));
           kept += h != 0.0;
         }
@@ -515,10 +537,32 @@ extern "C" size_t gu_symmetrize_workspace_size(int64_t n, int64_t nnz) {
   return sym_layout(n, nnz, nullptr, nullptr);
 }
 
+static int symmetrize_impl(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* dst,
+                           const double* w, int32_t* sym_src, int32_t* sym_dst, double* sym_w,
+                           int64_t* nbr_indptr, int64_t* host_E, void* workspace, size_t ws_bytes,
+                           const void* smooth_ws, size_t smooth_ws_bytes, void* stream);
+
 extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* dst,
                              const double* w, int32_t* sym_src, int32_t* sym_dst, double* sym_w,
                              int64_t* nbr_indptr, int64_t* host_E, void* workspace,
                              size_t ws_bytes, void* stream) {
+  return symmetrize_impl(n, nnz, indptr, dst, w, sym_src, sym_dst, sym_w, nbr_indptr, host_E,
+                         workspace, ws_bytes, nullptr, 0, stream);
+}
+
+extern "C" int gu_symmetrize_memo(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* dst,
+                                  const double* w, int32_t* sym_src, int32_t* sym_dst,
+                                  double* sym_w, int64_t* nbr_indptr, int64_t* host_E,
+                                  void* workspace, size_t ws_bytes, const void* smooth_workspace,
+                                  size_t smooth_ws_bytes, void* stream) {
+  return symmetrize_impl(n, nnz, indptr, dst, w, sym_src, sym_dst, sym_w, nbr_indptr, host_E,
+                         workspace, ws_bytes, smooth_workspace, smooth_ws_bytes, stream);
+}
+
+static int symmetrize_impl(int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* dst,
+                           const double* w, int32_t* sym_src, int32_t* sym_dst, double* sym_w,
+                           int64_t* nbr_indptr, int64_t* host_E, void* workspace, size_t ws_bytes,
+                           const void* smooth_ws, size_t smooth_ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 0 || nnz < 0 || 2 * nnz >= INT32_MAX || (double)n * (double)n >= 1.8e19) {
     set_error("gu_symmetrize: unsupported size n=%lld nnz=%lld", (long long)n, (long long)nnz);
@@ -575,11 +619,26 @@ extern "C" int gu_symmetrize(int64_t n, int64_t nnz, const int64_t* indptr, cons
         const char* v = getenv("GU_SYM_MERGE16");
         return !(v && v[0] == '0');
       }();
+      // backward weights from K5's profile table when the caller hands over
+      // the gu_smooth_knn workspace of the call that produced w (same n)
+      WOf wof;
+      wof.w = w;
+      wof.row_of = row_of;
+      wof.slot = nullptr;
+      wof.tab = nullptr;
+      static const bool use_memo = [] {
+        const char* v = getenv("GU_SYM_MEMO");
+        return !(v && v[0] == '0');
+      }();
+      if (use_memo && smooth_ws && smooth_ws_bytes >= SIG_TABLE_BYTES + sizeof(int) * (size_t)n) {
+        wof.tab = (const SigTable*)smooth_ws;
+        wof.slot = (const int*)((const char*)smooth_ws + SIG_TABLE_BYTES);
+      }
       if (kfix <= 16 && merge16 && n < (1LL << 27))
-        fx_merge16<<<grid_for(n * 16), 256, 0, st>>>(n, kfix, row_of, nnz, dst, w, ws.pos,
+        fx_merge16<<<grid_for(n * 16), 256, 0, st>>>(n, kfix, row_of, nnz, dst, w, wof, ws.pos,
                                                       vbuf.Current(), ws.v0, ws.h, ws.rowcnt);
       else
-        fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, row_of, nnz, dst, w, ws.pos,
+        fx_merge<<<grid_for(n * 32), 256, 0, st>>>(n, kfix, row_of, nnz, dst, w, wof, ws.pos,
                                                     vbuf.Current(), ws.v0, ws.h, ws.rowcnt);
       GU_CHECK_LAUNCH("fx_merge");
       int r1 = scan_counts(ws.rowcnt, n, (long long*)nbr_indptr, ws.partial, st);

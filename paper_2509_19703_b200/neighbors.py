@@ -621,9 +621,12 @@ def smooth_knn_weights(knn, k=None):
     nbr_indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
     import ctypes
     E = ctypes.c_int64(0)
-    _lib.call("gu_symmetrize", n, nnz, _lib.ptr(indptr), _lib.ptr(dst), _lib.ptr(w),
+    # the smooth workspace rides along: the union reads backward weights from
+    # its per-profile table instead of gathering w in destination order
+    _lib.call("gu_symmetrize_memo", n, nnz, _lib.ptr(indptr), _lib.ptr(dst), _lib.ptr(w),
               _lib.ptr(sym_src), _lib.ptr(sym_dst), _lib.ptr(sym_w), _lib.ptr(nbr_indptr),
-              ctypes.byref(E), _lib.ptr(ws), ws.numel(), st)
+              ctypes.byref(E), _lib.ptr(ws), ws.numel(),
+              _lib.ptr(sws), sws.numel(), st)
     E = int(E.value)
     sym_dst = sym_dst[:E]
     return KnnGraph(n=n, k=k, directed=knn,
