@@ -306,13 +306,16 @@ __global__ void fx_merge16(long long n, int kfix, RowOf row_of, long long nnz,
         e = in_e[ib + j];
         bid = row_of(e);
       }
+      // forward ids <= bid: upper bound in the half's sorted forward row
+      // (five shuffle steps instead of a kfix-long scan)
       int cnt = 0;
-      bool in_fwd = false;
-      for (int q = 0; q < kfix; q++) {
-        const int x = __shfl_sync(FULL_MASK, fid, hb + q);
-        cnt += x <= bid;
-        in_fwd |= x == bid;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int x = __shfl_sync(FULL_MASK, fid, hb + ((cnt + step - 1) & 15));
+        if (cnt + step - 1 < kfix && x <= bid) cnt += step;
       }
+      const int xl = __shfl_sync(FULL_MASK, fid, hb + ((cnt - 1) & 15));
+      const bool in_fwd = cnt > 0 && xl == bid;
       const int up = __shfl_up_sync(FULL_MASK, bid, 1);
       const int prev = hl == 0 ? carry : up;
       carry = __shfl_sync(FULL_MASK, bid, hb + 15);
