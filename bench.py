@@ -312,13 +312,13 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "peak_source": peak_kind,
-                     "kernel": "gu_partial_bfs_knn (tier F pbfs_fast<8>: 96% of the call's kernel time, "
+                     "kernel": "gu_partial_bfs_knn (tier F pbfs_fast<8>: 95% of the call's kernel time, "
                                "profiles/r02_bench_launches_summary.txt)",
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4),
-                     "limiter": "issue + shared-memory pipe, not HBM: ~620 warp instructions per "
-                                "source at 81% of peak issue, LSU wavefronts at 82% of peak (hash "
+                     "limiter": "issue + shared-memory pipe, not HBM: ~570 warp instructions per "
+                                "source at 84% of peak issue, LSU wavefronts at 73% of peak (hash "
                                 "CAS / atomicMin / clears), DRAM at 23% of peak "
-                                "(profiles/r02_ncu_pbfs_fast_final.txt, DESIGN.md K3)"},
+                                "(profiles/r02_ncu_pbfs_fast_micro.txt, DESIGN.md K3)"},
         # per step: tiers F, 1a, H, C (or 1b), slot clear, tier 2 -- once, or once
         # per exchange round at N > 1 (NCCL and dtype-cast kernels not counted)
         "gpu_launches": 6 * args.steps * (4 if ws > 1 else 1),
