@@ -49,6 +49,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef SGD_POOL
 #define SGD_POOL 1  // warp-pooled first-try negatives on GPU-filling epochs
 #endif
+#ifndef SGD_STREAM
+#define SGD_STREAM 1  // window records: pooled tries consumed in place, no per-slot arrays
+#endif
 #ifndef SGD_LOCKSTEP
 #define SGD_LOCKSTEP 1  // a block of negatives reads one x_u (see the epoch kernel)
 #endif
@@ -450,6 +453,91 @@ __global__ void __launch_bounds__(256, MINB)
         re = __ldg(nip + u + 1);
       }
     }
+#if SGD_STREAM
+    if (POOL && MODE == REC_RANGE) {
+      // Streamlined repulsions for window records: a pooled first try outside
+      // the head's neighbour-id window (99.8% of them on c5) needs no further
+      // test, so nothing is kept in per-slot arrays and no filter hits are
+      // published for a cooperative search -- the slot's vertex and
+      // coordinates come by shuffle right where its gradient is evaluated.
+      // The rare slots that need more (in-window with the Bloom bits set: a
+      // neighbour or a false positive; the head itself; a coincident point)
+      // are flagged and redone one by one below.
+      const unsigned d0 = draw32(vbase, 0, 0);
+      const unsigned stride = ((d0 >> 5) & 15u) * 2u + 1u;
+      for (int q0 = 0; q0 < n_neg; q0 += SGD_NEG_BLOCK) {
+        const int nq = min(SGD_NEG_BLOCK, n_neg - q0);
+        unsigned redo = 0;
+        float sx = 0.f, sy = 0.f;
+#pragma unroll
+        for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+          const int ln = (int)((d0 + (unsigned)(q0 + q) * stride) & 31u);
+          const int c = __shfl_sync(FULL, pool_c, ln);
+          const float cx = __shfl_sync(FULL, pool_xy.x, ln);
+          const float cy = __shfl_sync(FULL, pool_xy.y, ln);
+          const bool maybe_nb = c >= rlo && c <= rhi && filt_maybe<F>(fw, c);
+          const float dx = xu.x - cx, dy = xu.y - cy;
+          const float d2 = dx * dx + dy * dy;
+          const float g = __fdividef(2.0f * b, (0.001f + d2) * (a * __powf(d2, b) + 1.0f));
+          const bool live = act && q < nq;
+          const bool good = live && c != u && !maybe_nb && d2 > 0.f;
+          sx += good ? clip4(g * dx) : 0.f;
+          sy += good ? clip4(g * dy) : 0.f;
+          if (live && !good) redo |= 1u << q;
+        }
+        sx *= lr;
+        sy *= lr;
+        dux += sx;
+        duy += sy;
+        xu.x += sx;
+        xu.y += sy;
+        if (!__any_sync(FULL, redo != 0u)) continue;
+#pragma unroll
+        for (int q = 0; q < SGD_NEG_BLOCK; q++) {
+          const int ln = (int)((d0 + (unsigned)(q0 + q) * stride) & 31u);
+          int c = __shfl_sync(FULL, pool_c, ln);
+          float2 xcq;
+          xcq.x = __shfl_sync(FULL, pool_xy.x, ln);
+          xcq.y = __shfl_sync(FULL, pool_xy.y, ln);
+          if (!((redo >> q) & 1u)) continue;
+          unsigned draw = draw32(vbase, q0 + q, 0);
+          if (c == u || (c >= rlo && c <= rhi && is_neighbor(nip, nix, u, c))) {
+            c = -1;
+            for (int t = 1; t < 8; t++) {  // retries 2..8 of this slot
+              const unsigned rr = draw32(vbase, q0 + q, t);
+              const int cc = (int)__umulhi(rr, (unsigned)n);
+              if (cc == u || (cc >= rlo && cc <= rhi && is_neighbor(nip, nix, u, cc))) continue;
+              c = cc;
+              draw = rr;
+              break;
+            }
+            if (c < 0) continue;
+            xcq = xy[c];
+          }
+          const float dx = xu.x - xcq.x, dy = xu.y - xcq.y;
+          const float d2 = dx * dx + dy * dy;
+          float gx, gy;
+          if (d2 > 0.f) {
+            const float g = __fdividef(2.0f * b, (0.001f + d2) * (a * __powf(d2, b) + 1.0f));
+            gx = clip4(g * dx);
+            gy = clip4(g * dy);
+          } else {
+            const float th = (float)theta_draw(draw) * (6.283185307179586f / 4294967296.0f);
+            float sn, cs;
+            __sincosf(th, &sn, &cs);
+            gx = 4.0f * cs;
+            gy = 4.0f * sn;
+          }
+          gx *= lr;
+          gy *= lr;
+          dux += gx;
+          duy += gy;
+          xu.x += gx;
+          xu.y += gy;
+        }
+      }
+    } else
+#endif
     for (int q0 = 0; q0 < n_neg; q0 += SGD_NEG_BLOCK) {
       const int nq = min(SGD_NEG_BLOCK, n_neg - q0);
       int cand[SGD_NEG_BLOCK];
