@@ -489,10 +489,12 @@ def _sgd_bench(gu, g, args, dev, peak):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": _profile_traffic("sgd_epoch_kernel"),
                          "alg_bytes_per_update": 88,
-                         "limiter": "per-visit latency after the warp-pooled negatives took L2 "
-                                    "tag lookups from 73% to 50% of peak (612M -> 403M L2 requests "
-                                    "per epoch): 46% occupancy (64 registers), 42% issue active, "
-                                    "long-scoreboard stalls; DRAM at 8% of peak, the 32 MB "
+                         "limiter": "memory latency (long-scoreboard 69% of stall samples, 42% of "
+                                    "issue slots, 47% of warp slots at 54 registers; 5 CTAs per SM "
+                                    "changed nothing): the warp-pooled first tries took L2 tag "
+                                    "lookups from 73% to 52% of peak (612M -> 373M L2 requests per "
+                                    "epoch) and consuming them in place removed the per-slot arrays "
+                                    "and the cooperative search; DRAM at 10% of peak, the 32 MB "
                                     "coordinates L2-resident (profiles/r02_ncu_sgd_l2.txt, "
                                     "DESIGN.md K7)"},
             "diverged": int(div.item()) != INT32_MAX}
