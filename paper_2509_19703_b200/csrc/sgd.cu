@@ -745,6 +745,154 @@ __global__ void __launch_bounds__(256, MINB)
   if (bad) atomicMin(diverged, epoch);
 }
 
+// Small concurrency caps with exact neighbour sets (REC_HASH): ONE VISIT ON
+// FOUR LANES.  With n / 4 visits in flight (c1: 625, c3: 25,000) an epoch is
+// bound by the length of one visit's dependent chain, not by throughput, so
+// the visit's six gradients are spread over a quad: sub-lane 1 takes the
+// attraction and slot 1, sub-lanes 0 / 2 / 3 take slots {0, 4} / 2 / 3 (slot
+// q on sub-lane q & 3).  Every part reads x_u as the visit found it; a
+// sub-lane applies its own slots in order; the quad's deltas are summed by
+// two shuffles and pushed once.  Same draws as sgd_epoch_kernel (draw32 of
+// the visit base), same rejection rule, same update formulas -- only the
+// order inside a visit is relaxed (check (c): tests/test_gpu_parity.py
+// quality tests, profiles/r02_ab_sgd_split.log).  8 visits per warp.
+__global__ void __launch_bounds__(256, 3)
+    sgd_epoch_split_kernel(int n, long long E, float2* __restrict__ xy,
+                           const int4* __restrict__ edges, const int4* __restrict__ tab, float a,
+                           float b, float lr, int epoch, int n_neg, long long items,
+                           long long start, int windowed, unsigned long long seed,
+                           int* __restrict__ diverged) {
+  constexpr int lanes = 8;
+  const long long ntiles = (E + TILE - 1) / TILE;
+  Feistel tperm((unsigned long long)ntiles, mix64(seed ^ (0x51ED27ull + (unsigned long long)epoch)));
+  const unsigned long long rkey = mix64(seed ^ (0xA5A5A5A5ull * (unsigned long long)(epoch + 1)));
+  const int lane = threadIdx.x & 31, vi = lane >> 2, sub = lane & 3;
+  bool bad = false;
+  const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long stride = (((long long)gridDim.x * blockDim.x) >> 5) * lanes;
+  unsigned tile_batch = 0;
+  int step = 0;
+  for (long long i0 = gwarp * lanes; i0 < items; i0 += stride, step = (step + 1) & 31) {
+    const long long i = i0 + vi;
+    bool act = i < items;
+    long long p = 0;
+    if (windowed) {
+      p = start + i;
+      if (p >= E) p -= E;
+    } else {
+      if (step == 0) {
+        const long long il = i0 + (long long)lane * stride;
+        tile_batch = il < items ? (unsigned)tperm((unsigned long long)(il / TILE)) : 0u;
+      }
+      const long long tile = (long long)__shfl_sync(FULL, tile_batch, step);
+      p = tile * TILE + (i - (i0 / TILE) * TILE);
+      if (p >= E) act = false;  // partial last tile maps onto itself
+    }
+    if (!act) p = 0;
+    const int4 rec = act ? __ldcs(edges + p) : make_int4(0, 0, 0, 0);
+    const int u = rec.x, v = rec.y;
+    const float2 x0 = SGD_LD(&xy[u]);
+    float2 xu = x0;
+    float dux = 0.f, duy = 0.f;
+    const unsigned long long vbase = mix64(rkey ^ (unsigned long long)p);
+    if (act) {
+      const unsigned hoff = (unsigned)rec.w >> 4, lg = (unsigned)rec.w & 15u;
+      const unsigned b0 = hoff >> 2, bmask = (1u << (lg - 2)) - 1u;
+      // first tries of this sub-lane's slots: bucket and coordinates in flight together
+      const int q1 = sub, q2 = sub + 4;
+      const unsigned r1 = draw32(vbase, q1, 0), r2 = draw32(vbase, q2, 0);
+      const int c1 = (int)__umulhi(r1, (unsigned)n), c2 = (int)__umulhi(r2, (unsigned)n);
+      const bool has1 = q1 < n_neg, has2 = q2 < n_neg;
+      int4 k1 = make_int4(-1, -1, -1, -1), k2 = k1;
+      float2 y1 = make_float2(0.f, 0.f), y2 = y1;
+      if (has1) {
+        k1 = __ldg(tab + b0 + hset_bucket(c1, lg));
+        y1 = SGD_LD(&xy[c1]);
+      }
+      if (has2) {
+        k2 = __ldg(tab + b0 + hset_bucket(c2, lg));
+        y2 = SGD_LD(&xy[c2]);
+      }
+      if (sub == 1) {  // attraction
+        const float2 xv = SGD_LD(&xy[v]);
+        const float h = __int_as_float(rec.z);
+        const float dx = x0.x - xv.x, dy = x0.y - xv.y;
+        const float d2 = dx * dx + dy * dy;
+        if (d2 > 0.f) {
+          const float pb = __powf(d2, b);
+          const float g = __fdividef(-2.0f * a * b * h * pb, d2 * (a * pb + 1.0f));
+          const float gx = clip4(g * dx) * lr, gy = clip4(g * dy) * lr;
+          dux += gx;
+          duy += gy;
+          atomicAdd(&xy[v], make_float2(-gx, -gy));
+          if (!isfinite(xv.x - gx) || !isfinite(xv.y - gy)) bad = true;
+        }
+      }
+      // is c in the head's exact neighbour set?  (first bucket already loaded)
+      auto in_set = [&](int c, int4 x) -> bool {
+        unsigned hb = hset_bucket(c, lg);
+        while (x.x != c && x.y != c && x.z != c && x.w != c && (x.x | x.y | x.z | x.w) >= 0) {
+          hb = (hb + 1) & bmask;
+          x = __ldg(tab + b0 + hb);
+        }
+        return x.x == c || x.y == c || x.z == c || x.w == c;
+      };
+      auto repel = [&](int q, int c, unsigned draw, int4 k, float2 y) {
+        if (c == u || in_set(c, k)) {  // retries 2..8 of this slot (rare)
+          c = -1;
+          for (int t = 1; t < 8; t++) {
+            const unsigned rr = draw32(vbase, q, t);
+            const int cc = (int)__umulhi(rr, (unsigned)n);
+            if (cc == u || in_set(cc, __ldg(tab + b0 + hset_bucket(cc, lg)))) continue;
+            c = cc;
+            draw = rr;
+            break;
+          }
+          if (c < 0) return;
+          y = xy[c];
+        }
+        const float dx = xu.x - y.x, dy = xu.y - y.y;
+        const float d2 = dx * dx + dy * dy;
+        float gx, gy;
+        if (d2 > 0.f) {
+          const float g = __fdividef(2.0f * b, (0.001f + d2) * (a * __powf(d2, b) + 1.0f));
+          gx = clip4(g * dx);
+          gy = clip4(g * dy);
+        } else {
+          const float th = (float)theta_draw(draw) * (6.283185307179586f / 4294967296.0f);
+          float sn, cs;
+          __sincosf(th, &sn, &cs);
+          gx = 4.0f * cs;
+          gy = 4.0f * sn;
+        }
+        gx *= lr;
+        gy *= lr;
+        dux += gx;
+        duy += gy;
+        xu.x += gx;
+        xu.y += gy;
+      };
+      if (has1) repel(q1, c1, r1, k1, y1);
+      if (has2) repel(q2, c2, r2, k2, y2);
+      for (int q = sub + 8; q < n_neg; q += 4) {  // more than 8 negatives
+        const unsigned rr = draw32(vbase, q, 0);
+        const int cc = (int)__umulhi(rr, (unsigned)n);
+        repel(q, cc, rr, __ldg(tab + b0 + hset_bucket(cc, lg)), SGD_LD(&xy[cc]));
+      }
+    }
+    // the quad's deltas, summed on every lane (lanes of inactive visits add zeros)
+    dux += __shfl_xor_sync(FULL, dux, 1);
+    duy += __shfl_xor_sync(FULL, duy, 1);
+    dux += __shfl_xor_sync(FULL, dux, 2);
+    duy += __shfl_xor_sync(FULL, duy, 2);
+    if (act && sub == 0) {
+      if (dux != 0.f || duy != 0.f) atomicAdd(&xy[u], make_float2(dux, duy));
+      if (!isfinite(x0.x + dux) || !isfinite(x0.y + duy)) bad = true;
+    }
+  }
+  if (bad) atomicMin(diverged, epoch);
+}
+
 // deterministic mode: x += acc * 2^-32, acc = 0, finiteness check
 __global__ void det_apply_kernel(int n, float2* __restrict__ xy, long long* __restrict__ acc,
                                  int epoch, int* __restrict__ diverged) {
@@ -1051,6 +1199,19 @@ extern "C" int gu_sgd_epochs(int64_t n, int64_t E, float* coords_xy, const void*
     const long long threads = concurrency > 0 ? (concurrency * 32 + lanes - 1) / lanes : 0;
     const unsigned bs = block_for(threads);
     const unsigned gs = bs < 256 ? 1u : grid_for((items * 32 + lanes - 1) / lanes, threads);
+    // small caps on exact neighbour sets: one visit on four lanes
+    // (GU_SGD_SPLIT=0: the one-lane-per-visit kernel, for comparison)
+    static const bool split = [] {
+      const char* v = getenv("GU_SGD_SPLIT");
+      return !(v && v[0] == '0');
+    }();
+    if (split && lanes == 8 && record_mode == REC_HASH && bs == 256) {
+      sgd_epoch_split_kernel<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges,
+                                                (const int4*)nbr_filter, a, b, lr, e, n_neg, items,
+                                                start, windowed, seed, diverged);
+      GU_CHECK_LAUNCH("sgd_epoch_split_kernel");
+      continue;
+    }
     EpochKernel kern = epoch_kernel(lanes, record_mode);
     kern<<<gs, bs, 0, st>>>((int)n, E, (float2*)coords_xy, (const int4*)edges, nbr_indptr,
                             nbr_indices, (const FiltWord*)nbr_filter, a, b, lr, e, n_neg, items,
