@@ -1132,8 +1132,10 @@ __global__ void __launch_bounds__(TC_THREADS, TC_MINB)
              unsigned long long seed, long long src_begin, const int* __restrict__ list,
              const int* __restrict__ list_count, int* __restrict__ out_nbr,
              int* __restrict__ out_dist, int* __restrict__ out_cnt, int* __restrict__ ovf_list,
-             int* __restrict__ ovf_count, unsigned long long* __restrict__ work) {
+             int* __restrict__ ovf_count, int* __restrict__ queue,
+             unsigned long long* __restrict__ work) {
   constexpr int HC = TC_HC, CAP = TC_CAP, PCAP = TC_PCAP, TCAP = TC_TCAP, TW = TierC::TW;
+  __shared__ int s_it;
   constexpr unsigned EMPTY = 0xffffffffu, IDM = (1u << 23) - 1u;
   extern __shared__ __align__(16) int smem[];
   unsigned* const hkey = reinterpret_cast<unsigned*>(smem);
@@ -1173,7 +1175,12 @@ __global__ void __launch_bounds__(TC_THREADS, TC_MINB)
     return before + inc - v;
   };
   const int total_items = *list_count;
-  for (int it = blockIdx.x; it < total_items; it += gridDim.x) {
+  // sources handed out one at a time (ball sizes, hence times, vary widely)
+  for (;;) {
+    if (tid == 0) s_it = atomicAdd(queue, 1);
+    __syncthreads();
+    const int it = s_it;
+    if (it >= total_items) break;
     const int s = list[it];
     const long long item = (long long)s - src_begin;
     int* const rn = out_nbr + item * K;
@@ -1485,7 +1492,7 @@ struct PbfsWs {
   int* ovfA;
   int* ovfB;
   int* ovf0;
-  int* counts;  // [0]=ovfA count, [1]=ovfB count, [2]=ovf0 count, [3]=tier H rejects, [4]=F -> H directly, [5]=tier H work queue head
+  int* counts;  // [0]=ovfA count, [1]=ovfB count, [2]=ovf0 count, [3]=tier H rejects, [4]=F -> H directly, [5]=tier H work queue head, [6]=tier C work queue head
   unsigned long long* work;
   int* slots;
 };
@@ -1604,7 +1611,8 @@ cudaError_t launch_hub(int sms, const int* indptr, const int* indices, int k,
 cudaError_t launch_cta(int sms, const int* indptr, const int* indices, int k,
                        unsigned long long seed, long long src_begin, const int* list,
                        const int* list_count, int* out_nbr, int* out_dist, int* out_count,
-                       int* ovf_out, int* ovf_cnt, unsigned long long* work, cudaStream_t st) {
+                       int* ovf_out, int* ovf_cnt, int* queue, unsigned long long* work,
+                       cudaStream_t st) {
   constexpr size_t smem = sizeof(int) * TierC::WORDS;
   cudaError_t e = cudaFuncSetAttribute(pbfs_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -1613,7 +1621,8 @@ cudaError_t launch_cta(int sms, const int* indptr, const int* indices, int k,
   if (e != cudaSuccess) return e;
   const unsigned blocks = (unsigned)sms * (unsigned)(per_sm > 0 ? per_sm : 1);
   pbfs_cta<<<blocks, TC_THREADS, smem, st>>>(indptr, indices, k, seed, src_begin, list, list_count,
-                                              out_nbr, out_dist, out_count, ovf_out, ovf_cnt, work);
+                                              out_nbr, out_dist, out_count, ovf_out, ovf_cnt, queue,
+                                              work);
   return cudaGetLastError();
 }
 
@@ -1701,7 +1710,7 @@ extern "C" int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_
     static const char* env_big = getenv("GU_PBFS_BIG");
     if (n < (1 << 23) - 1 && !(env_big && !strcmp(env_big, "warp"))) {
       GU_CHECK(launch_cta(sms, indptr, indices, k, seed, src_begin, big_list, big_count, out_nbr,
-                          out_dist, out_count, ws.ovfB, ws.counts + 1, work, st));
+                          out_dist, out_count, ws.ovfB, ws.counts + 1, ws.counts + 6, work, st));
     } else {
       GU_CHECK(launch_lean_big(sms, n, indptr, indices, k, seed, src_begin, nsrc, big_list, big_count,
                                out_nbr, out_dist, out_count, ws.ovfB, ws.counts + 1, work, st));
