@@ -712,13 +712,13 @@ def test_random_uniform_matches_numpy(gu):
 
 
 def test_sgd_negative_counts_small_cap(gu):
-    """Small-cap epochs (exact neighbour sets) with 0 and 7 negatives per
-    visit (two slot blocks): finite layouts; 0 negatives moves the layout by
-    attraction only (the points contract)."""
+    """Small-cap epochs (exact neighbour sets, one visit on four lanes) with
+    0, 7 and 11 negatives per visit: finite layouts; 0 negatives moves the
+    layout by attraction only (the points contract)."""
     g = gu.synth_graph("grid", 2500)
     gk = gu.smooth_knn_weights(gu.knn_from_full_distances(gu.all_pairs_bfs(g), 15, seed=0))
     init = gu.random_init(g, 0, 10.0)
-    for nn in (0, 7):
+    for nn in (0, 7, 11):  # 11: the quad kernel's third slot round (slots 8..10)
         cfg = gu.OptimizerConfig(iterations=20, k=15, seed=0, negative_sample_count=nn)
         lay = gu.optimize_full(gk, init, cfg)
         assert np.all(np.isfinite(lay.coords))
@@ -805,3 +805,53 @@ def test_partial_bfs_hub_tier(gu, oracle, k, hub_pos):
     print(f"k={k} hubs {hub_pos}: left F {tiers[0]}, entered H {entered_h}, big-ball tier {entered_big}")
     if k >= 5:  # (k = 2: only degree-1 sources stop at level 2, the tier has nothing to do)
         assert entered_h > 0 and entered_big < entered_h  # tier H ran and finished sources
+
+
+def test_symmetrize_memo_matches_plain(gu):
+    """gu_symmetrize_memo (backward weights read from K5's profile table, the
+    path smooth_knn_weights takes) against plain gu_symmetrize (weights
+    gathered from w) on the same kNN rows: identical arrays, including rows
+    that have no profile (> 4 distance runs) and therefore gather."""
+    import ctypes
+    import torch
+    from paper_2509_19703_b200 import _lib
+    from paper_2509_19703_b200.device import stream_ptr, workspace
+
+    rng = np.random.default_rng(5)
+    n, k = 20000, 15
+    dist = np.empty((n, k), np.int32)
+    for v in range(n):
+        if v % 9 == 0:   # six runs: no profile key, solved and gathered directly
+            dist[v] = np.sort(rng.integers(1, 7, size=k))
+        else:
+            t0 = int(rng.integers(1, k))
+            dist[v] = [1] * t0 + [2] * (k - t0)
+    dst = np.stack([rng.choice(n - 1, size=k, replace=False) for _ in range(n)]).astype(np.int32)
+    dst += dst >= np.arange(n)[:, None]  # no self entries
+    order = np.lexsort((dst, dist), axis=1)
+    dst = np.take_along_axis(dst, order, 1)
+    dist = np.take_along_axis(dist, order, 1)
+    indptr = (k * np.arange(n + 1)).astype(np.int64)
+    knn = gu.DirectedKnn(n=n, k=k, indptr=indptr, dst=dst.reshape(-1), dist=dist.reshape(-1))
+    gk = gu.smooth_knn_weights(knn)  # memo path
+    dev = torch.device("cuda")
+    lib = _lib.load()
+    nnz = n * k
+    d_ip = torch.from_numpy(indptr).to(dev)
+    d_dst = torch.from_numpy(dst.reshape(-1)).to(dev)
+    d_w = gk._dev["w"]  # the directed weights K5 produced (device-resident)
+    ws = workspace(lib.gu_symmetrize_workspace_size(n, nnz), dev)
+    s_src = torch.empty(2 * nnz, dtype=torch.int32, device=dev)
+    s_dst = torch.empty(2 * nnz, dtype=torch.int32, device=dev)
+    s_w = torch.empty(2 * nnz, dtype=torch.float64, device=dev)
+    nip = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    E = ctypes.c_int64(0)
+    _lib.call("gu_symmetrize", n, nnz, _lib.ptr(d_ip), _lib.ptr(d_dst), _lib.ptr(d_w), _lib.ptr(s_src),
+              _lib.ptr(s_dst), _lib.ptr(s_w), _lib.ptr(nip), ctypes.byref(E), _lib.ptr(ws), ws.numel(),
+              stream_ptr(dev))
+    E = int(E.value)
+    assert E == gk.edge_count
+    assert np.array_equal(s_src[:E].cpu().numpy(), gk.sym_src)
+    assert np.array_equal(s_dst[:E].cpu().numpy(), gk.sym_dst)
+    assert np.array_equal(s_w[:E].cpu().numpy(), gk.sym_w)  # bit-identical
+    assert np.array_equal(nip.cpu().numpy(), gk.nbr_indptr)
