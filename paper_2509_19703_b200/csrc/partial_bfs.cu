@@ -397,6 +397,9 @@ __device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
 #ifndef TF_MINB
 #define TF_MINB 8
 #endif
+#ifndef TF_MERGED_VOTE
+#define TF_MERGED_VOTE 1  // one probe-loop vote per chunk pair
+#endif
 constexpr int TH_DMIN = 64;  // tier H: smallest degree of an implicit (hub) parent
 
 // Partial Fisher-Yates in closed form.  Lane i < r holds its draw j_i (>= i)
@@ -680,10 +683,57 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       const unsigned base_tag = (unsigned)(t0 + 1);
       const unsigned ka = ((unsigned)(t0 + lane + 1) << 24) | (unsigned)xa;
       const unsigned kb = ((unsigned)(t0 + 33 + lane) << 24) | (unsigned)xb;
+#if TF_MERGED_VOTE
+      // both chunks' CASes first, ONE vote for their probe loops (insertion
+      // order is free: equal ids settle on the smallest tag whatever the order)
+      unsigned ha = hash_slot<HC>(xa), hb = hash_slot<HC>(xb);
+      unsigned olda = (unsigned)xa, oldb = (unsigned)xb;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+          "@p atom.shared.cas.b32 %0, [%2], -1, %3;\n\t}"
+          : "+r"(olda)
+          : "r"((unsigned)(t0 + lane < T)), "r"(hbase + 4u * ha), "r"(ka)
+          : "memory");
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+          "@p atom.shared.cas.b32 %0, [%2], -1, %3;\n\t}"
+          : "+r"(oldb)
+          : "r"((unsigned)(two && t0 + 32 + lane < T)), "r"(hbase + 4u * hb), "r"(kb)
+          : "memory");
+      bool ca = olda != 0xffffffffu && ((olda ^ (unsigned)xa) << 8) != 0u;
+      bool cb = oldb != 0xffffffffu && ((oldb ^ (unsigned)xb) << 8) != 0u;
+      if (__any_sync(FULL, ca || cb)) {
+        while (ca) {
+          ha = (ha + 1) & (HC - 1);
+          olda = (unsigned)atomicCAS(&hkey[ha], -1, (int)ka);
+          ca = olda != 0xffffffffu && ((olda ^ (unsigned)xa) << 8) != 0u;
+        }
+        while (cb) {
+          hb = (hb + 1) & (HC - 1);
+          oldb = (unsigned)atomicCAS(&hkey[hb], -1, (int)kb);
+          cb = oldb != 0xffffffffu && ((oldb ^ (unsigned)xb) << 8) != 0u;
+        }
+        __syncwarp();
+      }
+      const bool ma = (olda >> 24) >= base_tag, mb = (oldb >> 24) >= base_tag;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+          "@p red.shared.min.u32 [%1], %2;\n\t}"
+          :
+          : "r"((unsigned)(ma && olda != 0xffffffffu)), "r"(hbase + 4u * ha), "r"(ka)
+          : "memory");
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+          "@p red.shared.min.u32 [%1], %2;\n\t}"
+          :
+          : "r"((unsigned)(mb && oldb != 0xffffffffu)), "r"(hbase + 4u * hb), "r"(kb)
+          : "memory");
+#else
       unsigned ha, hb;
       bool ma, mb;
       insert_tagged(xa, ka, t0 + lane < T, base_tag, ha, ma);
       insert_tagged(xb, kb, two && t0 + 32 + lane < T, base_tag, hb, mb);
+#endif
       __syncwarp();
       const bool na = ma && (unsigned)hkey[ha] == ka;
       const bool nb = mb && (unsigned)hkey[hb] == kb;
