@@ -40,6 +40,9 @@ int gu_host_is_pinned(const void* p); /* 1 if p lies in page-locked host memory 
 /* ---------------------------------------------- C0+C1 partial BFS-kNN
  * Replaces _kernels.py:60-131 partial_bfs_all(indptr, indices, k, seed,
  * nbr_out, dist_out, counts_out), reached via neighbors.py:137 partial_bfs.
+ * indptr / indices: the CSR the reference's Graph holds (graph.py:16-71) --
+ * the SYMMETRIC adjacency of an undirected simple graph, rows sorted
+ * ascending; the hub tier tests "x in N(H)" as "H in N(x)".
  * Sources [src_begin, src_end); row r = s - src_begin of out_nbr/out_dist
  * (stride k) holds the k hop-nearest others of s sorted by (dist, id), ties at
  * the crossing level chosen by the reference's splitmix64 partial
