@@ -22,6 +22,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gumap.h"
 
@@ -44,6 +46,9 @@ __global__ void bfs_init(int n, int* __restrict__ level, int* __restrict__ cnt, 
 // level-synchronous BFS: frontier of level l in q[l & 1] (cnt[l] entries);
 // a vertex joins level l + 1 when its CAS from -1 succeeds.  On exit
 // out[0] = last non-empty level, out[1] = its smallest vertex id.
+#ifndef ORD_GRID_PER_SM
+#define ORD_GRID_PER_SM 2
+#endif
 __global__ void __launch_bounds__(ORD_THREADS)
     bfs_levels_coop(int n, const int* __restrict__ indptr, const int* __restrict__ indices,
                     int* __restrict__ level, int* __restrict__ cnt, int* __restrict__ q0,
@@ -51,17 +56,23 @@ __global__ void __launch_bounds__(ORD_THREADS)
   cg::grid_group grid = cg::this_grid();
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nthr = (long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
   int l = 0;
   for (;;) {
     const int fsize = *(volatile int*)&cnt[l];
     int* cur = (l & 1) ? q1 : q0;
     int* nxt = (l & 1) ? q0 : q1;
-    for (long long i = tid; i < fsize; i += nthr) {
+    // one warp per frontier vertex, its lanes over the adjacency: a level of
+    // a deep BFS (c5's kNN graph: ~1,400 levels of a few thousand vertices) is
+    // then a couple of memory round trips instead of deg(u) dependent atomics;
+    // visited neighbours are skipped by an L2 read before the CAS
+    for (long long i = tid >> 5; i < fsize; i += nthr >> 5) {
       const int u = cur[i];
       const int b = __ldg(indptr + u), e = __ldg(indptr + u + 1);
-      for (int p = b; p < e; p++) {
+      for (int p = b + lane; p < e; p += 32) {
         const int w = __ldg(indices + p);
-        if (atomicCAS(&level[w], -1, l + 1) == -1) nxt[atomicAdd(&cnt[l + 1], 1)] = w;
+        if (__ldcg(&level[w]) == -1 && atomicCAS(&level[w], -1, l + 1) == -1)
+          nxt[atomicAdd(&cnt[l + 1], 1)] = w;
       }
     }
     grid.sync();
@@ -187,7 +198,14 @@ int run_bfs(int n, const int* indptr, const int* indices, int root, const OrdWs&
   GU_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   GU_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_levels_coop, ORD_THREADS, 0));
   if (per_sm < 1) per_sm = 1;
-  const unsigned grid = (unsigned)(sms * (per_sm < 4 ? per_sm : 4));
+  // CTAs per SM: a grid barrier per BFS level costs more the more CTAs join it
+  // (GU_ORD_GRID_PER_SM, default below)
+  static const int want = [] {
+    const char* v = getenv("GU_ORD_GRID_PER_SM");
+    const int x = v ? atoi(v) : 0;
+    return x >= 1 ? x : ORD_GRID_PER_SM;
+  }();
+  const unsigned grid = (unsigned)(sms * (per_sm < want ? per_sm : want));
   const int* ip = indptr;
   const int* ix = indices;
   int* lv = ws.level;
