@@ -57,8 +57,9 @@ int gu_partial_bfs_knn(int64_t n, const int32_t* indptr, const int32_t* indices,
                        int32_t* out_nbr, int32_t* out_dist, int32_t* out_count,
                        uint64_t* work_counters, void* workspace, size_t ws_bytes,
                        int32_t tier2_warps, void* stream);
-/* synchronous: sources that fell from tier 0 (thread per source) to tier 1a,
- * to tier 1b and to tier 2 in the last call on this workspace (3 ints) */
+/* synchronous: sources that left the register tier F, that reached the
+ * big-ball tier (C / 1b) and that reached tier 2 in the last call on this
+ * workspace (3 ints) */
 int gu_partial_bfs_overflow_counts(void* workspace, int64_t nsrc, int32_t* host_out3);
 /* synchronous: sources that left tier F (to 1a), tier 1a (to the hub tier H),
  * tier H (to tier C / 1b) and tier C / 1b (to tier 2) in the last call on
