@@ -397,6 +397,9 @@ __device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
 #ifndef TF_MINB
 #define TF_MINB 8
 #endif
+#ifndef TF_NO_INNER_SYNC
+#define TF_NO_INNER_SYNC 1  // the warp barrier before the read-back orders the atomics; none needed after the probe loops
+#endif
 #ifndef TF_MERGED_VOTE
 #define TF_MERGED_VOTE 1  // one probe-loop vote per chunk pair
 #endif
@@ -713,7 +716,9 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
           oldb = (unsigned)atomicCAS(&hkey[hb], -1, (int)kb);
           cb = oldb != 0xffffffffu && ((oldb ^ (unsigned)xb) << 8) != 0u;
         }
+#if !TF_NO_INNER_SYNC
         __syncwarp();
+#endif
       }
       const bool ma = (olda >> 24) >= base_tag, mb = (oldb >> 24) >= base_tag;
       asm volatile(
