@@ -400,6 +400,9 @@ __device__ __forceinline__ int umod64_tab(unsigned long long x, int d) {
 #ifndef TF_NO_INNER_SYNC
 #define TF_NO_INNER_SYNC 1  // the warp barrier before the read-back orders the atomics; none needed after the probe loops
 #endif
+#ifndef TF_PRED_STORE
+#define TF_PRED_STORE 1  // predicated list stores (no sink-word wavefronts for lanes with nothing new)
+#endif
 #ifndef TF_MERGED_VOTE
 #define TF_MERGED_VOTE 1  // one probe-loop vote per chunk pair
 #endif
@@ -747,9 +750,15 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
       // nst <= TF_CAP2 on entry: a's entries end below TF_CAP2 + 32, b's
       // below TF_CAP2 + 64 (past TF_CAP2 only when overflowing, which
       // discards the list); lanes with nothing new hit their sink
+#if TF_PRED_STORE
+      if (na) lst[nst + __popc(ba & lt)] = xa;
+      nst += __popc(ba);
+      if (nb) lst[nst + __popc(bb & lt)] = xb;
+#else
       lst[na ? nst + __popc(ba & lt) : TF_CAP2 + 32 + lane] = xa;
       nst += __popc(ba);
       lst[nb ? nst + __popc(bb & lt) : TF_CAP2 + 32 + lane] = xb;
+#endif
       nst += __popc(bb);
       return nst > TF_CAP2;
     };
