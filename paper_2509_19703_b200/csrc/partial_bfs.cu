@@ -685,7 +685,9 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
           : "memory");
     };
     auto process2p = [&](int t0, int xa, int xb) -> bool {
+#if !TF_MERGED_VOTE
       const bool two = t0 + 32 < T;  // warp-uniform
+#endif
       const unsigned base_tag = (unsigned)(t0 + 1);
       const unsigned ka = ((unsigned)(t0 + lane + 1) << 24) | (unsigned)xa;
       const unsigned kb = ((unsigned)(t0 + 33 + lane) << 24) | (unsigned)xb;
@@ -704,7 +706,7 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
           "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
           "@p atom.shared.cas.b32 %0, [%2], -1, %3;\n\t}"
           : "+r"(oldb)
-          : "r"((unsigned)(two && t0 + 32 + lane < T)), "r"(hbase + 4u * hb), "r"(kb)
+          : "r"((unsigned)(t0 + 32 + lane < T)), "r"(hbase + 4u * hb), "r"(kb)
           : "memory");
       bool ca = olda != 0xffffffffu && ((olda ^ (unsigned)xa) << 8) != 0u;
       bool cb = oldb != 0xffffffffu && ((oldb ^ (unsigned)xb) << 8) != 0u;
