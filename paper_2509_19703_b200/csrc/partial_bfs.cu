@@ -725,7 +725,8 @@ __global__ void __launch_bounds__(WARPS * 32, TF_MINB)
         __syncwarp();
 #endif
       }
-      const bool ma = (olda >> 24) >= base_tag, mb = (oldb >> 24) >= base_tag;
+      // (tag >= base tag, compared on whole keys: the tag is the top byte)
+      const bool ma = olda >= (base_tag << 24), mb = oldb >= (base_tag << 24);
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
           "@p red.shared.min.u32 [%1], %2;\n\t}"
