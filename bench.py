@@ -315,7 +315,7 @@ def run_ours(args):
                      "kernel": "gu_partial_bfs_knn (tier F pbfs_fast<8>: 95% of the call's kernel time, "
                                "profiles/r02_bench_launches_summary.txt)",
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4),
-                     "limiter": "issue + shared-memory pipe, not HBM: ~540 warp instructions per "
+                     "limiter": "issue + shared-memory pipe, not HBM: ~535 warp instructions per "
                                 "source at 84% of peak issue, LSU wavefronts at 74% of peak (hash "
                                 "CAS / atomicMin / clears), DRAM at 26% of peak "
                                 "(profiles/r02_ncu_pbfs_fast_final.txt, r02_sass_pbfs_fast.txt, DESIGN.md K3)"},
