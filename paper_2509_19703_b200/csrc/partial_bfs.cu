@@ -968,6 +968,7 @@ __global__ void __launch_bounds__(TH_WARPS * 32, TH_MINB)
   int* const wsc = xs + 32;
   unsigned long long w_scanned = 0, w_expanded = 0;
   const int total = *list_count;
+  if (total == 0) return;  // (no storm of queue atomics for an empty list)
   // sources are handed out one at a time (per-source latency varies a lot and
   // the list is only a few rounds of the resident warps long)
   for (;;) {
@@ -1242,6 +1243,7 @@ __global__ void __launch_bounds__(TC_THREADS, TC_MINB)
     return before + inc - v;
   };
   const int total_items = *list_count;
+  if (total_items == 0) return;  // (no storm of queue atomics for an empty list)
   // sources handed out one at a time (ball sizes, hence times, vary widely)
   for (;;) {
     if (tid == 0) s_it = atomicAdd(queue, 1);
